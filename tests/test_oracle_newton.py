@@ -1,0 +1,231 @@
+"""Pins of oracle O4 (energy/gradient), O5 (HVP), O6 (Jacobi diagonal) and O7 (Newton-PCG)
+against finite differences, exact completeness identities, brute force and special cases
+(SURVEY.md §8(c).3 rows O4-O7)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+
+def _setup(dim, seed, cells=(3, 3, 2), u_scale=1e-3, **kw):
+    sc = synth.random_fixture(dim=dim, seed=seed, cells=cells, **kw)
+    gs = oracle.p2g(sc)
+    rng = np.random.default_rng(seed + 100)
+    act = gs.active.astype(bool)
+    u = np.zeros_like(gs.v)
+    u[act] = rng.normal(0.0, u_scale * sc.grid.dx, size=(act.sum(), dim))
+    return sc, gs, u, act, rng
+
+
+def _nodes(grid):
+    d = grid.dim
+    shp = oracle.node_shape(grid)
+    k = np.stack(np.meshgrid(*[np.arange(s) for s in shp], indexing="ij"), -1).reshape(-1, d)
+    return np.asarray(grid.origin[:d]) + k * grid.dx
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_gradient_is_energy_derivative(dim):
+    sc, gs, u, act, rng = _setup(dim, 41)
+    g = oracle.gradient(sc, gs, u)
+    dvec = np.zeros_like(u)
+    dvec[act] = rng.normal(size=(act.sum(), dim)) * sc.grid.dx
+    an = (g * dvec).sum()
+    errs = []
+    for eps in (1e-4, 1e-5):
+        ep, _ = oracle.energy(sc, gs, u + eps * dvec)
+        em, _ = oracle.energy(sc, gs, u - eps * dvec)
+        errs.append(abs((ep - em) / (2 * eps) / an - 1.0))
+    # central differences converge as O(eps^2) to the analytic directional derivative
+    assert errs[1] < 2e-7 and errs[1] < errs[0] / 50
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_hvp_is_gradient_derivative(dim):
+    sc, gs, u, act, rng = _setup(dim, 42)
+    dvec = np.zeros_like(u)
+    dvec[act] = rng.normal(size=(act.sum(), dim)) * sc.grid.dx
+    y = oracle.hvp(sc, gs, u, dvec)
+    errs = []
+    for eps in (1e-4, 1e-5):
+        fd = (oracle.gradient(sc, gs, u + eps * dvec) - oracle.gradient(sc, gs, u - eps * dvec)) / (2 * eps)
+        errs.append(np.abs(fd - y).max() / np.abs(y).max())
+    # O(eps^2) convergence of the central difference
+    assert errs[1] < 2e-8 and (errs[1] < errs[0] / 50 or errs[1] < 1e-11)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_hvp_symmetry_and_positivity(dim):
+    sc, gs, u, act, rng = _setup(dim, 43)
+    a = np.zeros_like(u)
+    b = np.zeros_like(u)
+    a[act] = rng.normal(size=(act.sum(), dim))
+    b[act] = rng.normal(size=(act.sum(), dim))
+    ha = oracle.hvp(sc, gs, u, a)
+    hb = oracle.hvp(sc, gs, u, b)
+    assert (b * ha).sum() == pytest.approx((a * hb).sum(), rel=1e-13)
+    assert (a * ha).sum() > 0
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_hvp_completeness_identities(dim):
+    sc, gs, u, act, rng = _setup(dim, 44)
+    d = dim
+    xi = _nodes(sc.grid)
+    pt = sc.particles
+    mdt = gs.m[:, None] / sc.dt ** 2
+    # (i) translations are in the null space of K; (ii) Σ_i (Kd)_i = 0 for any d
+    c = rng.normal(size=d)
+    K_c = oracle.hvp(sc, gs, u, np.tile(c, (xi.shape[0], 1))) - mdt * c
+    dv = rng.normal(size=u.shape)
+    y = oracle.hvp(sc, gs, u, dv)
+    Kd = y - mdt * dv
+    assert np.abs(K_c).max() <= 1e-12 * np.abs(Kd).max()
+    assert np.abs(Kd.sum(axis=0)).max() <= 1e-12 * np.abs(Kd).max()
+    # (iii) affine d_i = A x_i + c: dF_p = A F_p^n, Σ_i (Kd)_i x_i^T = Σ_p V0 dP(F_p(u); A F_p^n) F_p^nT
+    A = rng.normal(size=(d, d))
+    da = xi @ A.T + c
+    Kda = oracle.hvp(sc, gs, u, da) - mdt * da
+    lhs = Kda.T @ xi
+    rhs = np.zeros((d, d))
+    for p in range(pt.n):
+        st = oracle.stencil(sc.grid, pt.x[p])
+        idx, N, gN, xip = st
+        Fu = (np.eye(d) + u[idx].T @ gN) @ pt.F[p]
+        mu, lam = oracle.lame(*sc.materials[pt.mat[p]])
+        rhs += pt.V0[p] * oracle.dP(Fu, A @ pt.F[p], mu, lam) @ pt.F[p].T
+    np.testing.assert_allclose(lhs, rhs, rtol=1e-11, atol=1e-12 * np.abs(rhs).max())
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_hvp_rest_rotations(dim):
+    # (iv) at rest (F^n = I, u = 0) infinitesimal rotations d_i = W x_i (W skew) give K d = 0
+    sc = synth.random_fixture(dim=dim, seed=45, cells=(3, 3, 2), F_sigma=0.0)
+    gs = oracle.p2g(sc)
+    xi = _nodes(sc.grid)
+    rng = np.random.default_rng(1)
+    W = rng.normal(size=(dim, dim))
+    W = W - W.T
+    dv = xi @ W.T
+    Kd = oracle.hvp(sc, gs, np.zeros_like(gs.v), dv) - gs.m[:, None] / sc.dt ** 2 * dv
+    ref = oracle.hvp(sc, gs, np.zeros_like(gs.v), xi @ (W + W.T + np.eye(dim)).T)
+    assert np.abs(Kd).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_hvp_mass_only_when_no_stiffness():
+    # mu = lam = 0 (E = 0) -> H d = (m / dt^2) d exactly
+    sc = synth.random_fixture(dim=3, seed=46, cells=(3, 2, 2), materials=[(0.0, 0.3), (0.0, 0.3)])
+    gs = oracle.p2g(sc)
+    dv = np.random.default_rng(2).normal(size=gs.v.shape)
+    y = oracle.hvp(sc, gs, np.zeros_like(gs.v), dv)
+    np.testing.assert_array_equal(y, gs.m[:, None] / sc.dt ** 2 * dv)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_diag_brute_force(dim):
+    sc, gs, u, act, rng = _setup(dim, 47, cells=(2, 2, 2))
+    dg = oracle.diag(sc, gs, u)
+    d = dim
+    nodes = np.flatnonzero(act)
+    sel = rng.choice(nodes, size=min(25, nodes.size), replace=False)
+    for i in sel:
+        for a in range(d):
+            e = np.zeros_like(u)
+            e[i, a] = 1.0
+            h = oracle.hvp(sc, gs, u, e)
+            assert dg[i, a] == pytest.approx(h[i, a], rel=1e-13)
+
+
+def _settings(**kw):
+    base = dict(newton_rtol=1e-12, cg_rtol=1e-12, max_cg=2000, max_newton=50)
+    base.update(kw)
+    return oracle.default_settings(**base)
+
+
+def test_newton_all_dirichlet():
+    sc = synth.random_fixture(dim=2, seed=48, cells=(3, 3, 1))
+    gs = oracle.p2g(sc)
+    vD = np.random.default_rng(3).normal(size=gs.v.shape)
+    u, st = oracle.implicit_solve(sc, gs, _settings(), dirichlet_mask=np.ones(gs.v.shape, np.uint8),
+                                  dirichlet_v=vD)
+    act = gs.active.astype(bool)
+    np.testing.assert_array_equal(u[act], sc.dt * vD[act])
+    assert st.cg_iters == 0
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_newton_free_fall_without_stiffness(dim):
+    # no elasticity: the minimiser is xhat = xtilde + dt^2 g, i.e. v^{n+1} = v^n + dt g
+    sc = synth.random_fixture(dim=dim, seed=49, cells=(2, 2, 2), materials=[(0.0, 0.3), (0.0, 0.3)])
+    gs = oracle.p2g(sc)
+    u, st = oracle.implicit_solve(sc, gs, _settings())
+    act = gs.active.astype(bool)
+    vnew = u / sc.dt
+    np.testing.assert_allclose(vnew[act], gs.v[act] + sc.dt * np.asarray(sc.gravity[:dim]), rtol=0, atol=1e-12)
+
+
+def test_newton_matches_brute_force_minimiser():
+    # a few dozen unknowns: Newton-PCG + line search reaches the minimiser of E_h found by an
+    # independent dense brute-force Newton whose Hessian is built column by column from central
+    # differences of the gradient (no HVP, no PCG), with a dense direct solve.
+    sc = synth.random_fixture(dim=2, seed=50, cells=(2, 2, 1), ppa=2, dt=5e-3, v_sigma=0.3)
+    gs = oracle.p2g(sc)
+    act = gs.active.astype(bool)
+    nfree = act.sum() * 2
+    assert nfree <= 60
+    u_n, st = oracle.implicit_solve(sc, gs, _settings())
+    assert st.status == 0
+
+    def grad(z):
+        u = np.zeros_like(gs.v)
+        u[act] = z.reshape(-1, 2)
+        return oracle.gradient(sc, gs, u)[act].ravel()
+
+    def energy(z):
+        u = np.zeros_like(gs.v)
+        u[act] = z.reshape(-1, 2)
+        return oracle.energy(sc, gs, u)[0]
+
+    z = (sc.dt * gs.v[act]).ravel()
+    h = 1e-7
+    for _ in range(60):
+        g = grad(z)
+        if np.linalg.norm(g) < 1e-9 * st.grad_norm0:
+            break
+        H = np.zeros((z.size, z.size))
+        for k in range(z.size):
+            e = np.zeros_like(z)
+            e[k] = h
+            H[:, k] = (grad(z + e) - grad(z - e)) / (2 * h)
+        step = np.linalg.solve(0.5 * (H + H.T), -g)
+        a = 1.0
+        while not energy(z + a * step) < energy(z) and a > 1e-6:
+            a *= 0.5
+        z = z + a * step
+    scale = np.abs(u_n[act]).max()
+    assert np.abs(z.reshape(-1, 2) - u_n[act]).max() <= 1e-8 * scale
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_newton_energy_decreases_and_converges(dim):
+    sc = synth.random_fixture(dim=dim, seed=51, cells=(3, 3, 2), F_sigma=0.1, v_sigma=1.0)
+    gs = oracle.p2g(sc)
+    energies = []
+    for k in range(1, 6):
+        u, st = oracle.implicit_solve(sc, gs, _settings(max_newton=k), raise_on_error=False)
+        energies.append(oracle.energy(sc, gs, u)[0])
+    assert all(b <= a * (1 + 1e-13) + 1e-13 * abs(a) for a, b in zip(energies, energies[1:]))
+    u, st = oracle.implicit_solve(sc, gs, _settings())
+    assert st.status == 0
+    g = oracle.gradient(sc, gs, u)
+    act = gs.active.astype(bool)
+    assert np.linalg.norm(g[act]) <= 1e-12 * st.grad_norm0 * 1.0001
+
+
+def test_newton_fixed_iterations_runs_exact_count():
+    sc = synth.random_fixture(dim=3, seed=52, cells=(2, 2, 2))
+    gs = oracle.p2g(sc)
+    st_set = oracle.default_settings(max_newton=3, max_cg=7, fixed_iters=1)
+    u, st = oracle.implicit_solve(sc, gs, st_set)
+    assert st.newton_iters == 3 and st.cg_iters == 21
