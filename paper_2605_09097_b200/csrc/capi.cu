@@ -1,0 +1,315 @@
+// capi.cu -- the extern "C" boundary of libosmpm (include/osmpm.h): argument checking, dispatch on
+// (dimension, precision), error strings.  No compute happens here.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "coupler.cuh"
+#include "transmit.cuh"
+
+namespace osmpm {
+
+static thread_local std::string g_err;
+
+void set_error(const char* fmt, ...)
+{
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+}
+
+cudaEvent_t Profiler::begin(const std::string& name, cudaStream_t s)
+{
+    Fam& f = fams[name];
+    if (f.used == f.ev.size()) {
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        f.ev.push_back({a, b});
+    }
+    cudaEventRecord(f.ev[f.used].first, s);
+    return f.ev[f.used].first;
+}
+
+void Profiler::end(const std::string& name, cudaStream_t s)
+{
+    Fam& f = fams[name];
+    cudaEventRecord(f.ev[f.used].second, s);
+    f.used++;
+}
+
+osmpm_status Profiler::query(const std::string& name, int64_t* launches, double* ms)
+{
+    *launches = 0;
+    *ms = 0.0;
+    auto it = fams.find(name);
+    if (it == fams.end()) return OSMPM_OK;
+    double tot = 0.0;
+    for (size_t i = 0; i < it->second.used; ++i) {
+        float t = 0.f;
+        OSMPM_CU(cudaEventSynchronize(it->second.ev[i].second));
+        OSMPM_CU(cudaEventElapsedTime(&t, it->second.ev[i].first, it->second.ev[i].second));
+        tot += t;
+    }
+    *launches = (int64_t)it->second.used;
+    *ms = tot;
+    return OSMPM_OK;
+}
+
+void Profiler::reset()
+{
+    for (auto& kv : fams) kv.second.used = 0;
+}
+
+Profiler::~Profiler()
+{
+    for (auto& kv : fams)
+        for (auto& e : kv.second.ev) {
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
+}
+
+}  // namespace osmpm
+
+using namespace osmpm;
+
+#define CHECK_ARG(cond, ...)                                                                        \
+    do {                                                                                            \
+        if (!(cond)) {                                                                              \
+            set_error(__VA_ARGS__);                                                                 \
+            return OSMPM_E_INVALID_ARG;                                                             \
+        }                                                                                           \
+    } while (0)
+
+#define SET_DEVICE(ctx) OSMPM_CU(cudaSetDevice((ctx)->device))
+
+extern "C" {
+
+const char* osmpm_last_error(void) { return g_err.c_str(); }
+const char* osmpm_version(void) { return "osmpm 0.1 (sm_100a)"; }
+
+osmpm_status osmpm_ctx_create(int device, void* cuda_stream, osmpm_ctx** out)
+{
+    CHECK_ARG(out, "out is NULL");
+    osmpm_ctx* c = new osmpm_ctx();
+    c->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        set_error("cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
+        delete c;
+        return OSMPM_E_CUDA;
+    }
+    if (cuda_stream) {
+        c->stream = (cudaStream_t)cuda_stream;
+    } else {
+        cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+        c->own_stream = true;
+    }
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    *out = c;
+    return OSMPM_OK;
+}
+
+void osmpm_ctx_destroy(osmpm_ctx* ctx)
+{
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+osmpm_status osmpm_profile_enable(osmpm_ctx* ctx, int enable)
+{
+    CHECK_ARG(ctx, "ctx is NULL");
+    ctx->prof.on = enable != 0;
+    return OSMPM_OK;
+}
+osmpm_status osmpm_profile_reset(osmpm_ctx* ctx)
+{
+    CHECK_ARG(ctx, "ctx is NULL");
+    SET_DEVICE(ctx);
+    OSMPM_CU(cudaStreamSynchronize(ctx->stream));
+    ctx->prof.reset();
+    return OSMPM_OK;
+}
+osmpm_status osmpm_kernel_time(osmpm_ctx* ctx, const char* family, int64_t* launches, double* ms)
+{
+    CHECK_ARG(ctx && family && launches && ms, "NULL argument");
+    SET_DEVICE(ctx);
+    return ctx->prof.query(family, launches, ms);
+}
+
+osmpm_status osmpm_subdomain_create(osmpm_ctx* ctx, const osmpm_grid_desc* grid, double dt,
+                                    const osmpm_particles_view* particles, const osmpm_material* mats,
+                                    int32_t n_mats, const double gravity[3], osmpm_precision prec,
+                                    osmpm_subdomain** out)
+{
+    CHECK_ARG(ctx && grid && particles && mats && out, "NULL argument");
+    CHECK_ARG(grid->dim == 2 || grid->dim == 3, "dim = %d (must be 2 or 3)", grid->dim);
+    CHECK_ARG(grid->dx > 0, "dx must be > 0");
+    CHECK_ARG(dt > 0, "dt must be > 0");
+    CHECK_ARG(particles->n >= 0 && particles->n < (int64_t(1) << 31), "n = %lld out of range",
+              (long long)particles->n);
+    CHECK_ARG(particles->n == 0 || (particles->x && particles->m && particles->V0), "x, m and V0 are required");
+    for (int a = 0; a < grid->dim; ++a)
+        CHECK_ARG(grid->dims[a] >= 3 && grid->dims[a] < (int64_t(1) << 30), "dims[%d] = %lld out of range", a,
+                  (long long)grid->dims[a]);
+    CHECK_ARG(prec == OSMPM_F64 || prec == OSMPM_F32, "bad precision");
+    SET_DEVICE(ctx);
+    osmpm_subdomain* s = nullptr;
+    osmpm_status rc;
+#define MAKE(DD, RR)                                                                                \
+    {                                                                                               \
+        auto* q = new Sub<DD, RR>();                                                                \
+        q->ctx = ctx;                                                                               \
+        q->dim = DD;                                                                                \
+        q->prec = prec;                                                                             \
+        s = q;                                                                                      \
+        rc = q->create(grid, dt, particles, mats, n_mats, gravity);                                 \
+    }
+    if (grid->dim == 3 && prec == OSMPM_F64) MAKE(3, double)
+    else if (grid->dim == 2 && prec == OSMPM_F64) MAKE(2, double)
+    else if (grid->dim == 3) MAKE(3, float)
+    else MAKE(2, float)
+#undef MAKE
+    if (rc != OSMPM_OK) {
+        delete s;
+        return rc;
+    }
+    *out = s;
+    return OSMPM_OK;
+}
+
+void osmpm_subdomain_destroy(osmpm_subdomain* sub)
+{
+    if (!sub) return;
+    cudaSetDevice(sub->ctx->device);
+    cudaStreamSynchronize(sub->ctx->stream);
+    delete sub;
+}
+
+#define SUB_CALL(sub, expr)                                                                         \
+    do {                                                                                            \
+        CHECK_ARG(sub, "subdomain is NULL");                                                        \
+        SET_DEVICE((sub)->ctx);                                                                     \
+        return (sub)->expr;                                                                         \
+    } while (0)
+
+osmpm_status osmpm_set_gravity(osmpm_subdomain* sub, const double gravity[3])
+{
+    CHECK_ARG(gravity, "gravity is NULL");
+    SUB_CALL(sub, set_gravity(gravity));
+}
+osmpm_status osmpm_set_dt(osmpm_subdomain* sub, double dt) { SUB_CALL(sub, set_dt(dt)); }
+osmpm_status osmpm_set_particles(osmpm_subdomain* sub, const double* x, const double* v, const double* F,
+                                 const double* B, osmpm_memspace space)
+{
+    SUB_CALL(sub, set_particles(x, v, F, B, space));
+}
+osmpm_status osmpm_set_dirichlet(osmpm_subdomain* sub, int64_t n, const int64_t* node_idx, const uint8_t* comp_mask,
+                                 const double* vel, osmpm_memspace space)
+{
+    CHECK_ARG(n >= 0 && (n == 0 || (node_idx && comp_mask && vel)), "bad Dirichlet arguments");
+    SUB_CALL(sub, set_dirichlet(n, node_idx, comp_mask, vel, space));
+}
+osmpm_status osmpm_p2g(osmpm_subdomain* sub) { SUB_CALL(sub, p2g()); }
+osmpm_status osmpm_read_grid(osmpm_subdomain* sub, double* m, double* p, double* v, double* f_ext, double* f_sigma,
+                             uint8_t* active, osmpm_memspace space)
+{
+    SUB_CALL(sub, read_grid(m, p, v, f_ext, f_sigma, active, space));
+}
+osmpm_status osmpm_newton_gradient(osmpm_subdomain* sub, const double* u, double* g, double* E, osmpm_memspace space)
+{
+    CHECK_ARG(u, "u is NULL");
+    SUB_CALL(sub, newton_gradient(u, g, E, space));
+}
+osmpm_status osmpm_newton_hvp(osmpm_subdomain* sub, const double* d, double* y, osmpm_memspace space)
+{
+    CHECK_ARG(d && y, "d / y is NULL");
+    SUB_CALL(sub, newton_hvp(d, y, space));
+}
+osmpm_status osmpm_newton_diag(osmpm_subdomain* sub, double* diag, osmpm_memspace space)
+{
+    CHECK_ARG(diag, "diag is NULL");
+    SUB_CALL(sub, newton_diag(diag, space));
+}
+osmpm_status osmpm_implicit_solve(osmpm_subdomain* sub, const osmpm_newton_settings* settings,
+                                  osmpm_solve_stats* stats)
+{
+    CHECK_ARG(settings, "settings is NULL");
+    CHECK_ARG(settings->max_newton >= 0 && settings->max_cg >= 0, "negative iteration caps");
+    SUB_CALL(sub, implicit_solve(settings, stats));
+}
+osmpm_status osmpm_read_grid_velocity(osmpm_subdomain* sub, double* v, osmpm_memspace space)
+{
+    CHECK_ARG(v, "v is NULL");
+    SUB_CALL(sub, read_grid_velocity(v, space));
+}
+osmpm_status osmpm_set_grid_velocity(osmpm_subdomain* sub, const double* v, osmpm_memspace space)
+{
+    CHECK_ARG(v, "v is NULL");
+    SUB_CALL(sub, set_grid_velocity(v, space));
+}
+osmpm_status osmpm_g2p(osmpm_subdomain* sub) { SUB_CALL(sub, g2p()); }
+osmpm_status osmpm_read_particles(osmpm_subdomain* sub, double* x, double* v, double* F, double* B,
+                                  osmpm_memspace space)
+{
+    SUB_CALL(sub, read_particles(x, v, F, B, space));
+}
+osmpm_status osmpm_subdomain_info(osmpm_subdomain* sub, int64_t* n_particles, int64_t box_lo[3], int64_t box_dims[3])
+{
+    SUB_CALL(sub, info(n_particles, box_lo, box_dims));
+}
+osmpm_status osmpm_sync(osmpm_subdomain* sub) { SUB_CALL(sub, sync()); }
+
+osmpm_status osmpm_transmit(osmpm_subdomain* src, osmpm_subdomain* dst, osmpm_direction dir, double alpha,
+                            double eps_tol, int64_t n_targets, const int64_t* targets, double* v_out,
+                            osmpm_memspace space)
+{
+    CHECK_ARG(src && dst && v_out, "NULL argument");
+    CHECK_ARG(src->dim == dst->dim && src->prec == dst->prec, "transmit: subdomains differ in dim / precision");
+    CHECK_ARG(src->ctx == dst->ctx, "transmit: subdomains belong to different contexts");
+    CHECK_ARG(n_targets >= 0, "n_targets < 0");
+    SET_DEVICE(src->ctx);
+#define TR(DD, RR)                                                                                  \
+    return transmit_impl<DD, RR>(static_cast<Sub<DD, RR>*>(src), static_cast<Sub<DD, RR>*>(dst), dir, alpha,      \
+                                 eps_tol, n_targets, targets, v_out, space)
+    if (src->dim == 3 && src->prec == OSMPM_F64) TR(3, double);
+    if (src->dim == 2 && src->prec == OSMPM_F64) TR(2, double);
+    if (src->dim == 3) TR(3, float);
+    TR(2, float);
+#undef TR
+}
+
+osmpm_status osmpm_coupler_create(osmpm_subdomain* coarse, osmpm_subdomain* fine,
+                                  const osmpm_schwarz_settings* settings, osmpm_coupler** out)
+{
+    CHECK_ARG(coarse && fine && settings && out, "NULL argument");
+    CHECK_ARG(coarse->dim == fine->dim && coarse->prec == fine->prec, "coupler: subdomains differ in dim / precision");
+    CHECK_ARG(coarse->ctx == fine->ctx, "coupler: subdomains belong to different contexts");
+    CHECK_ARG(settings->M >= 1, "M must be >= 1");
+    SET_DEVICE(coarse->ctx);
+    return coupler_create(coarse, fine, settings, out);
+}
+void osmpm_coupler_destroy(osmpm_coupler* cpl) { coupler_destroy(cpl); }
+osmpm_status osmpm_schwarz_prepare(osmpm_coupler* cpl)
+{
+    CHECK_ARG(cpl, "coupler is NULL");
+    return coupler_prepare(cpl);
+}
+osmpm_status osmpm_schwarz_substep(osmpm_coupler* cpl, int32_t m, osmpm_solve_stats* stats)
+{
+    CHECK_ARG(cpl, "coupler is NULL");
+    return coupler_substep(cpl, m, stats);
+}
+osmpm_status osmpm_schwarz_step(osmpm_coupler* cpl, osmpm_schwarz_report* report)
+{
+    CHECK_ARG(cpl, "coupler is NULL");
+    return coupler_step(cpl, report);
+}
+
+}  // extern "C"

@@ -1,0 +1,1193 @@
+// kernels.cuh -- the sm_100a kernels of one implicit MPM sub-step (§2.2, Alg. 1).
+//
+// Data layout:
+//   particles  field-major SoA of R (fp64 or fp32), capacity `cap`, sorted tile-major by cell:
+//              x[D] v[D] F[D*D] B[D*D] m V0   (+ int32 mat, uint8 bnd, int32 pid)
+//   cache      per-particle Newton linearisation, field-major R:
+//              S' = V0 mu F^n F^nT (sym), Ah = (I + grad u)^{-T}, c' = V0 (mu - lam ln J), l' = V0 lam
+//   node box   dense fp64 arrays over the step's tight box (BoxDev), components innermost.
+#pragma once
+#include "device.cuh"
+
+namespace osmpm {
+
+template <int D> struct PL {
+    static constexpr int X = 0, V = D, F = 2 * D, B = 2 * D + D * D, M = 2 * D + 2 * D * D, VOL = M + 1,
+                         NF = VOL + 1;
+};
+template <int D> struct CL {
+    static constexpr int S = 0, A = Sym<D>::N, C = A + D * D, L = C + 1, NF = L + 1;
+};
+
+constexpr int MAX_MATS = 16;
+struct MatTable {
+    int n;
+    double mu[MAX_MATS], lam[MAX_MATS];
+};
+
+// =============================================================================================
+// a1: binning + sort support
+// =============================================================================================
+
+// lowest / highest base node per axis, and the safe-interior check
+template <int D, typename R>
+__global__ void k_bounds(const R* __restrict__ P, int64_t cap, int64_t n, BoxDev g, int* bounds,
+                         const int* __restrict__ pid, ErrLatch* err)
+{
+    int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, hi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            R f;
+            int b = base_of<R>(P[(PL<D>::X + a) * cap + p], g.o[a], g.inv_dx, &f);
+            if (b < 0 || b + 2 > g.gdims[a] - 1) latch_error(err, 2 /*OUT_OF_DOMAIN*/, pid[p]);
+            lo[a] = min(lo[a], b);
+            hi[a] = max(hi[a], b);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        for (int off = 16; off > 0; off >>= 1) {
+            lo[a] = min(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], off));
+            hi[a] = max(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], off));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(&bounds[a], lo[a]);
+            atomicMax(&bounds[3 + a], hi[a]);
+        }
+    }
+}
+
+template <int D, typename R>
+__global__ void k_keys(const R* __restrict__ P, int64_t cap, int64_t n, BoxDev b, uint32_t* keys, int* vals)
+{
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    int c[3] = {0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        R f;
+        c[a] = base_of<R>(P[(PL<D>::X + a) * cap + p], b.o[a], b.inv_dx, &f) - b.lo[a];
+    }
+    keys[p] = cell_key<D>(b, c[0], c[1], c[2]);
+    vals[p] = (int)p;
+}
+
+// gather-permute all real fields (field-major) and the integer fields
+template <typename R>
+__global__ void k_permute(const R* __restrict__ src, R* __restrict__ dst, int nf, int64_t cap, int64_t n,
+                          const int* __restrict__ perm, const int* __restrict__ mat_s, int* __restrict__ mat_d,
+                          const uint8_t* __restrict__ bnd_s, uint8_t* __restrict__ bnd_d,
+                          const int* __restrict__ pid_s, int* __restrict__ pid_d)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int j = perm[i];
+    for (int f = 0; f < nf; ++f) dst[f * cap + i] = src[f * cap + j];
+    mat_d[i] = mat_s[j];
+    bnd_d[i] = bnd_s[j];
+    pid_d[i] = pid_s[j];
+}
+
+// cell_start[k] = first sorted particle with key >= k, for k in [0, ncells]
+__global__ void k_cell_start(const uint32_t* __restrict__ keys, int64_t n, int64_t ncells, int* cell_start)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i > n) return;
+    int64_t lo = (i == 0) ? 0 : (int64_t)keys[i - 1] + 1;
+    int64_t hi = (i == n) ? ncells : (int64_t)keys[i];
+    for (int64_t k = lo; k <= hi; ++k) cell_start[k] = (int)i;
+}
+
+// =============================================================================================
+// a2: APIC P2G of mass, momentum, stress; per-particle scatter (v1)
+// =============================================================================================
+template <int D, typename R>
+__global__ void k_p2g(const R* __restrict__ P, int64_t cap, int64_t n, const int* __restrict__ mat, BoxDev b,
+                      MatTable mt, double* __restrict__ m, double* __restrict__ mom, double* __restrict__ fsig)
+{
+    using L = PL<D>;
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    R w[3][3], dw[3][3], f[3];
+    int c[3] = {0, 0, 0};
+    R inv_dx = (R)b.inv_dx, dx = (R)b.dx;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        c[a] = base_of<R>(P[(L::X + a) * cap + p], b.o[a], b.inv_dx, &f[a]) - b.lo[a];
+        bspline<R>(f[a], inv_dx, w[a], dw[a]);
+    }
+    R F[D * D], B[D * D], v[D];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) {
+        F[k] = P[(L::F + k) * cap + p];
+        B[k] = P[(L::B + k) * cap + p];
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) v[a] = P[(L::V + a) * cap + p];
+    const R mp = P[L::M * cap + p], V0 = P[L::VOL * cap + p];
+    const int mid = mat[p];
+    const R mu = (R)mt.mu[mid], lam = (R)mt.lam[mid];
+    // Kirchhoff stress tau = P F^T = mu F F^T + (lam ln J - mu) I
+    R tau[D * D];
+    const R lnJ = log(det<D, R>(F));
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int bb = 0; bb < D; ++bb) {
+            R s = 0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) s += F[a * D + k] * F[bb * D + k];
+            tau[a * D + bb] = mu * s + (a == bb ? lam * lnJ - mu : R(0));
+        }
+    const R Dinv = R(4) * inv_dx * inv_dx;  // D_p^{-1} = 4/dx^2 I
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int k = 0; k < Tile<D>::K3; ++k) {
+                R N, gN[3], off[3];
+                off[0] = dx * (R(i) - f[0]);
+                off[1] = dx * (R(j) - f[1]);
+                if (D == 3) {
+                    off[2] = dx * (R(k) - f[2]);
+                    N = w[0][i] * w[1][j] * w[2][k];
+                    gN[0] = dw[0][i] * w[1][j] * w[2][k];
+                    gN[1] = w[0][i] * dw[1][j] * w[2][k];
+                    gN[2] = w[0][i] * w[1][j] * dw[2][k];
+                } else {
+                    N = w[0][i] * w[1][j];
+                    gN[0] = dw[0][i] * w[1][j];
+                    gN[1] = w[0][i] * dw[1][j];
+                }
+                int64_t node = box_node<D>(b, c[0] + i, c[1] + j, c[2] + k);
+                const R mN = mp * N;
+                atomicAdd(&m[node], (double)mN);
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    R aff = 0, t = 0;
+#pragma unroll
+                    for (int bb = 0; bb < D; ++bb) {
+                        aff += B[a * D + bb] * off[bb];
+                        t += tau[a * D + bb] * gN[bb];
+                    }
+                    atomicAdd(&mom[node * D + a], (double)(mN * (v[a] + Dinv * aff)));
+                    atomicAdd(&fsig[node * D + a], (double)(-V0 * t));
+                }
+            }
+}
+
+// node pass: active <=> m > thr (R4), v^n = (mv) / m
+template <int D>
+__global__ void k_p2g_nodes(int64_t nn, const double* __restrict__ m, const double* __restrict__ mom,
+                            double* __restrict__ vn, uint8_t* __restrict__ act, double thr)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nn) return;
+    const bool a = m[i] > thr;
+    act[i] = a;
+#pragma unroll
+    for (int k = 0; k < D; ++k) vn[i * D + k] = a ? mom[i * D + k] / m[i] : 0.0;
+}
+
+// boundary-particle mass m^b_i = sum_{p in P^∂} m_p N_ip
+template <int D, typename R>
+__global__ void k_bmass(const R* __restrict__ P, int64_t cap, int64_t n, const uint8_t* __restrict__ bnd, BoxDev b,
+                        double* __restrict__ mb)
+{
+    using L = PL<D>;
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n || !bnd[p]) return;
+    R w[3][3], dw[3][3], f[3];
+    int c[3] = {0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        c[a] = base_of<R>(P[(L::X + a) * cap + p], b.o[a], b.inv_dx, &f[a]) - b.lo[a];
+        bspline<R>(f[a], (R)b.inv_dx, w[a], dw[a]);
+    }
+    const R mp = P[L::M * cap + p];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            for (int k = 0; k < Tile<D>::K3; ++k) {
+                R N = (D == 3) ? w[0][i] * w[1][j] * w[2][k] : w[0][i] * w[1][j];
+                atomicAdd(&mb[box_node<D>(b, c[0] + i, c[1] + j, c[2] + k)], (double)(mp * N));
+            }
+}
+
+// =============================================================================================
+// tiled particle-loop scatter machinery (HVP, gradient, diagonal)
+//   phase 0: stage the tile's (T+2)^D nodes of the input vector in shared memory
+//   phase 1: per particle (thread per particle): weights, gather, per-particle source -> smem
+//   phase 2: per (cell, component) thread: register accumulation of its cell's particles'
+//            contributions to the 3^D stencil nodes (tensor-product evaluation)
+//   phase 3: per (node, component): sum the <= 3^D cell partials, one fp64 RED per node
+// =============================================================================================
+template <int D> struct ChunkLayout {
+    // per-particle smem fields (field-major with stride NT): w[D][3], dw[D][3], G[D][D]
+    static constexpr int W = 0, DW = 3 * D, G = 6 * D, NF = 6 * D + D * D;
+};
+
+template <int D>
+__device__ __forceinline__ void tile_coords(const BoxDev& b, int tile, int* t)
+{
+    if (D == 3) {
+        t[2] = tile % b.nt[2];
+        t[1] = (tile / b.nt[2]) % b.nt[1];
+        t[0] = tile / (b.nt[2] * b.nt[1]);
+    } else {
+        t[2] = 0;
+        t[1] = tile % b.nt[1];
+        t[0] = tile / b.nt[1];
+    }
+}
+
+// phase 0: sv[l*D + a] = vec[global node of tile-local node l][a]
+template <int D, typename R>
+__device__ __forceinline__ void stage_nodes(const BoxDev& b, const int* t, const double* __restrict__ vec, R* sv)
+{
+    using T = Tile<D>;
+    for (int i = threadIdx.x; i < T::NN * D; i += T::NT) {
+        int a = i % D, l = i / D;
+        int l2 = (D == 3) ? l % T::N2 : 0;
+        int l1 = (D == 3) ? (l / T::N2) % T::N1 : l % T::N1;
+        int l0 = (D == 3) ? l / (T::N2 * T::N1) : l / T::N1;
+        int64_t g = box_node<D>(b, t[0] * T::T0 + l0, t[1] * T::T1 + l1, t[2] * T::T2 + l2);
+        sv[i] = (R)vec[g * D + a];
+    }
+}
+
+template <int D>
+__device__ __forceinline__ int tnode(int l0, int l1, int l2)
+{
+    using T = Tile<D>;
+    return (D == 3) ? (l0 * T::N1 + l1) * T::N2 + l2 : l0 * T::N1 + l1;
+}
+
+// gather gd[a][b] = sum_i v_i,a dN_i/dx_b over the stencil (tensor-product order)
+template <int D, typename R>
+__device__ __forceinline__ void gather_grad(const R* sv, const int* lc, const R (*w)[3], const R (*dw)[3], R* gd)
+{
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) gd[k] = 0;
+    if (D == 3) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            R U0[3] = {0, 0, 0}, U1[3] = {0, 0, 0}, U2[3] = {0, 0, 0};
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                R T0[3] = {0, 0, 0}, T1[3] = {0, 0, 0};
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const R* s = sv + tnode<D>(lc[0] + i, lc[1] + j, lc[2] + k) * D;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        T0[a] += s[a] * w[2][k];
+                        T1[a] += s[a] * dw[2][k];
+                    }
+                }
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    U0[a] += T0[a] * w[1][j];
+                    U1[a] += T0[a] * dw[1][j];
+                    U2[a] += T1[a] * w[1][j];
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                gd[a * 3 + 0] += U0[a] * dw[0][i];
+                gd[a * 3 + 1] += U1[a] * w[0][i];
+                gd[a * 3 + 2] += U2[a] * w[0][i];
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            R U0[2] = {0, 0}, U1[2] = {0, 0};
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const R* s = sv + tnode<D>(lc[0] + i, lc[1] + j, 0) * D;
+#pragma unroll
+                for (int a = 0; a < 2; ++a) {
+                    U0[a] += s[a] * w[1][j];
+                    U1[a] += s[a] * dw[1][j];
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < 2; ++a) {
+                gd[a * 2 + 0] += U0[a] * dw[0][i];
+                gd[a * 2 + 1] += U1[a] * w[0][i];
+            }
+        }
+    }
+}
+
+// phase 2 (linear): acc[node] += sum_b s_b dN_node/dx_b
+template <int D, typename R>
+__device__ __forceinline__ void scatter_linear(const R* s, const R (*w)[3], const R (*dw)[3], R* acc)
+{
+    if (D == 3) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const R ax = s[0] * dw[0][i], bx = s[1] * w[0][i], cx = s[2] * w[0][i];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const R A = ax * w[1][j] + bx * dw[1][j];
+                const R B = cx * w[1][j];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) acc[(i * 3 + j) * 3 + k] += A * w[2][k] + B * dw[2][k];
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const R ax = s[0] * dw[0][i], bx = s[1] * w[0][i];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) acc[i * 3 + j] += ax * w[1][j] + bx * dw[1][j];
+        }
+    }
+}
+
+// phase 2 (quadratic): acc[node] += gradN^T Q gradN, Q symmetric (Sym<D> storage)
+template <int D, typename R>
+__device__ __forceinline__ void scatter_quadratic(const R* Q, const R (*w)[3], const R (*dw)[3], R* acc)
+{
+    if (D == 3) {
+        R y2[3], yy[3], dy2[3], z2[3], zz[3], dz2[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            y2[k] = w[1][k] * w[1][k];
+            yy[k] = w[1][k] * dw[1][k];
+            dy2[k] = dw[1][k] * dw[1][k];
+            z2[k] = w[2][k] * w[2][k];
+            zz[k] = w[2][k] * dw[2][k];
+            dz2[k] = dw[2][k] * dw[2][k];
+        }
+        const R q00 = Q[0], q11 = Q[1], q22 = Q[2], q01 = R(2) * Q[3], q02 = R(2) * Q[4], q12 = R(2) * Q[5];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const R pxx = dw[0][i] * dw[0][i], pxw = dw[0][i] * w[0][i], pww = w[0][i] * w[0][i];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const R C2 = q00 * pxx * y2[j] + q11 * pww * dy2[j] + q01 * pxw * yy[j];
+                const R C1 = q02 * pxw * y2[j] + q12 * pww * yy[j];
+                const R C0 = q22 * pww * y2[j];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) acc[(i * 3 + j) * 3 + k] += C2 * z2[k] + C1 * zz[k] + C0 * dz2[k];
+            }
+        }
+    } else {
+        const R q00 = Q[0], q11 = Q[1], q01 = R(2) * Q[2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const R pxx = dw[0][i] * dw[0][i], pxw = dw[0][i] * w[0][i], pww = w[0][i] * w[0][i];
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+                acc[i * 3 + j] += q00 * pxx * w[1][j] * w[1][j] + q11 * pww * dw[1][j] * dw[1][j] +
+                                  q01 * pxw * w[1][j] * dw[1][j];
+        }
+    }
+}
+
+// phase 3: node sums of the per-cell partials, one RED per (node, component)
+template <int D, typename R>
+__device__ __forceinline__ void flush_tile(const BoxDev& b, const int* t, const R* acc, double* __restrict__ out)
+{
+    using T = Tile<D>;
+    for (int idx = threadIdx.x; idx < T::NN * D; idx += T::NT) {
+        const int a = idx % D, l = idx / D;
+        const int l2 = (D == 3) ? l % T::N2 : 0;
+        const int l1 = (D == 3) ? (l / T::N2) % T::N1 : l % T::N1;
+        const int l0 = (D == 3) ? l / (T::N2 * T::N1) : l / T::N1;
+        R s = 0;
+        bool any = false;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const int c0 = l0 - i;
+            if (c0 < 0 || c0 >= T::T0) continue;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const int c1 = l1 - j;
+                if (c1 < 0 || c1 >= T::T1) continue;
+#pragma unroll
+                for (int k = 0; k < T::K3; ++k) {
+                    const int c2 = l2 - k;
+                    if (D == 3 && (c2 < 0 || c2 >= T::T2)) continue;
+                    const int c = (D == 3) ? (c0 * T::T1 + c1) * T::T2 + c2 : c0 * T::T1 + c1;
+                    s += acc[(c * D + a) * T::NS + (i * 3 + j) * T::K3 + k];
+                    any = true;
+                }
+            }
+        }
+        if (any && s != R(0)) {
+            int64_t g = box_node<D>(b, t[0] * T::T0 + l0, t[1] * T::T1 + l1, t[2] * T::T2 + l2);
+            atomicAdd(&out[g * D + a], (double)s);
+        }
+    }
+}
+
+// =============================================================================================
+// a5: HVP  y += sum_p V0 dP(F_p(u); gd F^n) F^nT grad N  =  sum_p G_p grad N with
+//     G = gd S' + c' Ah gd^T Ah + l' (Ah : gd) Ah   (derivation from PAPER.md:188, 208)
+// =============================================================================================
+template <int D, typename R>
+__global__ void __launch_bounds__(Tile<D>::NT)
+k_hvp(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, const int* __restrict__ cell_start,
+      BoxDev b, const double* __restrict__ din, double* __restrict__ yout)
+{
+    using T = Tile<D>;
+    using CLY = ChunkLayout<D>;
+    using L = PL<D>;
+    using C = CL<D>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    R* sv = reinterpret_cast<R*>(smem_raw);
+    R* sp = sv + T::NN * D;
+    const int tile = blockIdx.x;
+    const int pbeg = cell_start[(int64_t)tile * T::NC], pend = cell_start[(int64_t)(tile + 1) * T::NC];
+    if (pbeg == pend) return;
+    int t[3];
+    tile_coords<D>(b, tile, t);
+    stage_nodes<D, R>(b, t, din, sv);
+    __syncthreads();
+    const R inv_dx = (R)b.inv_dx;
+    for (int cb = pbeg; cb < pend; cb += T::NT) {
+        const int ce = min(cb + T::NT, pend);
+        const int q = threadIdx.x;
+        const int p = cb + q;
+        if (p < ce) {
+            R w[3][3], dw[3][3], f;
+            int lc[3] = {0, 0, 0};
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const int tt = a == 0 ? T::T0 : (a == 1 ? T::T1 : T::T2);
+                lc[a] = base_of<R>(P[(L::X + a) * cap + p], b.o[a], b.inv_dx, &f) - b.lo[a] - t[a] * tt;
+                bspline<R>(f, inv_dx, w[a], dw[a]);
+            }
+            R gd[D * D];
+            gather_grad<D, R>(sv, lc, w, dw, gd);
+            R S[Sym<D>::N], A[D * D];
+#pragma unroll
+            for (int k = 0; k < Sym<D>::N; ++k) S[k] = cache[(C::S + k) * cap + p];
+#pragma unroll
+            for (int k = 0; k < D * D; ++k) A[k] = cache[(C::A + k) * cap + p];
+            const R cc = cache[C::C * cap + p], ll = cache[C::L * cap + p];
+            // M2 = A gd^T ; tr = A : gd
+            R M2[D * D], tr = 0;
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int bb = 0; bb < D; ++bb) {
+                    R s = 0;
+#pragma unroll
+                    for (int k = 0; k < D; ++k) s += A[a * D + k] * gd[bb * D + k];
+                    M2[a * D + bb] = s;
+                    tr += A[a * D + bb] * gd[a * D + bb];
+                }
+            const R ltr = ll * tr;
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int bb = 0; bb < D; ++bb) {
+                    R s1 = 0, s2 = 0;
+#pragma unroll
+                    for (int k = 0; k < D; ++k) {
+                        s1 += gd[a * D + k] * S[sym_idx<D>(k, bb)];
+                        s2 += M2[a * D + k] * A[k * D + bb];
+                    }
+                    sp[(CLY::G + a * D + bb) * T::NT + q] = s1 + cc * s2 + ltr * A[a * D + bb];
+                }
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    sp[(CLY::W + a * 3 + k) * T::NT + q] = w[a][k];
+                    sp[(CLY::DW + a * 3 + k) * T::NT + q] = dw[a][k];
+                }
+        }
+        __syncthreads();
+        const int cell = threadIdx.x / D, comp = threadIdx.x % D;
+        const int64_t key = (int64_t)tile * T::NC + cell;
+        const int s0 = max(cell_start[key], cb), s1 = min(cell_start[key + 1], ce);
+        R acc[T::NS];
+#pragma unroll
+        for (int k = 0; k < T::NS; ++k) acc[k] = 0;
+        for (int pp = s0; pp < s1; ++pp) {
+            const int qq = pp - cb;
+            R w[3][3], dw[3][3], s[D];
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    w[a][k] = sp[(CLY::W + a * 3 + k) * T::NT + qq];
+                    dw[a][k] = sp[(CLY::DW + a * 3 + k) * T::NT + qq];
+                }
+#pragma unroll
+            for (int bb = 0; bb < D; ++bb) s[bb] = sp[(CLY::G + comp * D + bb) * T::NT + qq];
+            scatter_linear<D, R>(s, w, dw, acc);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < T::NS; ++k) sp[(cell * D + comp) * T::NS + k] = acc[k];
+        __syncthreads();
+        flush_tile<D, R>(b, t, sp, yout);
+        __syncthreads();
+    }
+}
+
+// =============================================================================================
+// a4: gradient + energy + Newton cache + Jacobi diagonal (tiled)
+//   M = I + grad u, F(u) = M F^n, J = det M det F^n,  Ah = M^{-T},  S = F^n F^nT
+//   G_grad = V0 P(F(u)) F^nT = M S' - c' Ah ;  diag_a += gradN^T (S' + (c' + l') Ah_a Ah_a^T) gradN
+//   Psi = mu/2 (tr(M S M^T) - d) - mu ln J + lam/2 ln^2 J
+// partials per CTA: {sum V0 Psi, sum V0 |Psi|, inverted}
+// =============================================================================================
+template <int D> struct GradLayout {
+    static constexpr int W = 0, DW = 3 * D, G = 6 * D, S = G + D * D, A = S + Sym<D>::N, CL = A + D * D,
+                         NF = CL + 1;
+};
+
+template <int D, typename R>
+__global__ void __launch_bounds__(Tile<D>::NT)
+k_grad(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int* __restrict__ mat,
+       const int* __restrict__ cell_start, BoxDev b, MatTable mt, const double* __restrict__ uin,
+       double* __restrict__ gout, double* __restrict__ dout, double* __restrict__ partials)
+{
+    using T = Tile<D>;
+    using GL = GradLayout<D>;
+    using L = PL<D>;
+    using C = CL<D>;
+    using Rd = double;  // gradient / energy arithmetic in fp64 (R14)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Rd* sv = reinterpret_cast<Rd*>(smem_raw);
+    Rd* sp = sv + T::NN * D;
+    const int tile = blockIdx.x;
+    const int pbeg = cell_start[(int64_t)tile * T::NC], pend = cell_start[(int64_t)(tile + 1) * T::NC];
+    double red[3] = {0.0, 0.0, 0.0};
+    if (pbeg == pend) {
+        if (threadIdx.x == 0) {
+            partials[blockIdx.x * 3 + 0] = 0.0;
+            partials[blockIdx.x * 3 + 1] = 0.0;
+            partials[blockIdx.x * 3 + 2] = 0.0;
+        }
+        return;
+    }
+    int t[3];
+    tile_coords<D>(b, tile, t);
+    stage_nodes<D, Rd>(b, t, uin, sv);
+    __syncthreads();
+    for (int cb = pbeg; cb < pend; cb += T::NT) {
+        const int ce = min(cb + T::NT, pend);
+        const int q = threadIdx.x;
+        const int p = cb + q;
+        if (p < ce) {
+            Rd w[3][3], dw[3][3], f;
+            int lc[3] = {0, 0, 0};
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const int tt = a == 0 ? T::T0 : (a == 1 ? T::T1 : T::T2);
+                lc[a] = base_of<Rd>((Rd)P[(L::X + a) * cap + p], b.o[a], b.inv_dx, &f) - b.lo[a] - t[a] * tt;
+                bspline<Rd>(f, b.inv_dx, w[a], dw[a]);
+            }
+            Rd Mx[D * D];
+            gather_grad<D, Rd>(sv, lc, w, dw, Mx);
+#pragma unroll
+            for (int a = 0; a < D; ++a) Mx[a * D + a] += 1.0;
+            Rd Fn[D * D];
+#pragma unroll
+            for (int k = 0; k < D * D; ++k) Fn[k] = (Rd)P[(L::F + k) * cap + p];
+            const Rd V0 = (Rd)P[L::VOL * cap + p];
+            const int mid = mat[p];
+            const Rd mu = mt.mu[mid], lam = mt.lam[mid];
+            Rd S[Sym<D>::N];
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int bb = a; bb < D; ++bb) {
+                    Rd s = 0;
+#pragma unroll
+                    for (int k = 0; k < D; ++k) s += Fn[a * D + k] * Fn[bb * D + k];
+                    S[sym_idx<D>(a, bb)] = V0 * mu * s;  // S' = V0 mu F^n F^nT
+                }
+            const Rd detM = det<D, Rd>(Mx), detFn = det<D, Rd>(Fn);
+            Rd Ah[D * D];
+            cofactor<D, Rd>(Mx, Ah);
+            const Rd invdet = 1.0 / detM;
+#pragma unroll
+            for (int k = 0; k < D * D; ++k) Ah[k] *= invdet;
+            const bool ok = detM > 0.0 && detFn > 0.0;
+            const Rd lnJ = ok ? log(detM) + log(detFn) : 0.0;
+            const Rd cc = V0 * (mu - lam * lnJ), ll = V0 * lam;
+            // tr(M S' M^T) (S' carries V0 mu)
+            Rd trMSM = 0;
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int bb = 0; bb < D; ++bb) {
+                    Rd s = 0;
+#pragma unroll
+                    for (int k = 0; k < D; ++k) s += Mx[a * D + k] * S[sym_idx<D>(k, bb)];
+                    trMSM += s * Mx[a * D + bb];
+                    sp[(GL::G + a * D + bb) * T::NT + q] = s - cc * Ah[a * D + bb];
+                }
+            const Rd psiV = 0.5 * (trMSM - V0 * mu * D) - V0 * mu * lnJ + 0.5 * V0 * lam * lnJ * lnJ;
+            red[0] += psiV;
+            red[1] += fabs(psiV);
+            if (!ok) red[2] += 1.0;
+#pragma unroll
+            for (int k = 0; k < Sym<D>::N; ++k) {
+                sp[(GL::S + k) * T::NT + q] = S[k];
+                cache[(C::S + k) * cap + p] = (R)S[k];
+            }
+#pragma unroll
+            for (int k = 0; k < D * D; ++k) {
+                sp[(GL::A + k) * T::NT + q] = Ah[k];
+                cache[(C::A + k) * cap + p] = (R)Ah[k];
+            }
+            cache[C::C * cap + p] = (R)cc;
+            cache[C::L * cap + p] = (R)ll;
+            sp[GL::CL * T::NT + q] = cc + ll;
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    sp[(GL::W + a * 3 + k) * T::NT + q] = w[a][k];
+                    sp[(GL::DW + a * 3 + k) * T::NT + q] = dw[a][k];
+                }
+        }
+        __syncthreads();
+        const int cell = threadIdx.x / D, comp = threadIdx.x % D;
+        const int64_t key = (int64_t)tile * T::NC + cell;
+        const int s0 = max(cell_start[key], cb), s1 = min(cell_start[key + 1], ce);
+        Rd acc[T::NS], accd[T::NS];
+#pragma unroll
+        for (int k = 0; k < T::NS; ++k) acc[k] = accd[k] = 0;
+        for (int pp = s0; pp < s1; ++pp) {
+            const int qq = pp - cb;
+            Rd w[3][3], dw[3][3], s[D], Q[Sym<D>::N], Ar[D];
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    w[a][k] = sp[(GL::W + a * 3 + k) * T::NT + qq];
+                    dw[a][k] = sp[(GL::DW + a * 3 + k) * T::NT + qq];
+                }
+#pragma unroll
+            for (int bb = 0; bb < D; ++bb) {
+                s[bb] = sp[(GL::G + comp * D + bb) * T::NT + qq];
+                Ar[bb] = sp[(GL::A + comp * D + bb) * T::NT + qq];
+            }
+            const Rd clv = sp[GL::CL * T::NT + qq];
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int bb = a; bb < D; ++bb)
+                    Q[sym_idx<D>(a, bb)] = sp[(GL::S + sym_idx<D>(a, bb)) * T::NT + qq] + clv * Ar[a] * Ar[bb];
+            scatter_linear<D, Rd>(s, w, dw, acc);
+            scatter_quadratic<D, Rd>(Q, w, dw, accd);
+        }
+        __syncthreads();
+        Rd* accs = sp;                                  // aliases the chunk buffer
+        Rd* accs2 = sp + T::NC * D * T::NS;
+#pragma unroll
+        for (int k = 0; k < T::NS; ++k) {
+            accs[(cell * D + comp) * T::NS + k] = acc[k];
+            accs2[(cell * D + comp) * T::NS + k] = accd[k];
+        }
+        __syncthreads();
+        flush_tile<D, Rd>(b, t, accs, gout);
+        flush_tile<D, Rd>(b, t, accs2, dout);
+        __syncthreads();
+    }
+    block_reduce_store<3>(red, partials);
+}
+
+// node terms of the gradient / diagonal / energy:
+//   g += m/dt^2 (u - dt v^n) - m grav ;  diag += m/dt^2 ;
+//   E_node = m/(2dt^2)|u - dt v^n|^2 - u . m grav ;  |g_free|^2
+// partials per block: {E_node, |E_node terms|, |g_free|^2}
+template <int D>
+__global__ void k_grad_nodes(int64_t nn, const double* __restrict__ m, const double* __restrict__ vn,
+                             const double* __restrict__ u, const uint8_t* __restrict__ fmask, double dt,
+                             double g0, double g1, double g2, double* __restrict__ g, double* __restrict__ dg,
+                             double* __restrict__ partials)
+{
+    double red[3] = {0.0, 0.0, 0.0};
+    const double grav[3] = {g0, g1, g2};
+    const double idt2 = 1.0 / (dt * dt);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
+        const double mi = m[i];
+        double q = 0.0, wf = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const double r = u[i * D + a] - dt * vn[i * D + a];
+            const double fe = mi * grav[a];
+            q += r * r;
+            wf += u[i * D + a] * fe;
+            const double gv = g[i * D + a] + mi * idt2 * r - fe;
+            g[i * D + a] = gv;
+            dg[i * D + a] += mi * idt2;
+            if (fmask[i * D + a]) red[2] += gv * gv;
+        }
+        const double e = 0.5 * mi * idt2 * q;
+        red[0] += e - wf;
+        red[1] += e + fabs(wf);
+    }
+    block_reduce_store<3>(red, partials);
+}
+
+// =============================================================================================
+// a7: energy only (line search): sum_p V0 Psi(F_p(u)), per particle, u gathered from global
+// partials per block: {sum V0 Psi, sum V0|Psi|, inverted}
+// =============================================================================================
+template <int D, typename R>
+__global__ void k_energy(const R* __restrict__ P, int64_t cap, int64_t n, const int* __restrict__ mat, BoxDev b,
+                         MatTable mt, const double* __restrict__ u, double* __restrict__ partials)
+{
+    using L = PL<D>;
+    double red[3] = {0.0, 0.0, 0.0};
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        double w[3][3], dw[3][3], f;
+        int c[3] = {0, 0, 0};
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            c[a] = base_of<double>((double)P[(L::X + a) * cap + p], b.o[a], b.inv_dx, &f) - b.lo[a];
+            bspline<double>(f, b.inv_dx, w[a], dw[a]);
+        }
+        double Mx[D * D];
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) Mx[k] = 0.0;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+                for (int k = 0; k < Tile<D>::K3; ++k) {
+                    double gN[3];
+                    if (D == 3) {
+                        gN[0] = dw[0][i] * w[1][j] * w[2][k];
+                        gN[1] = w[0][i] * dw[1][j] * w[2][k];
+                        gN[2] = w[0][i] * w[1][j] * dw[2][k];
+                    } else {
+                        gN[0] = dw[0][i] * w[1][j];
+                        gN[1] = w[0][i] * dw[1][j];
+                    }
+                    const double* uu = u + box_node<D>(b, c[0] + i, c[1] + j, c[2] + k) * D;
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+#pragma unroll
+                        for (int bb = 0; bb < D; ++bb) Mx[a * D + bb] += uu[a] * gN[bb];
+                }
+#pragma unroll
+        for (int a = 0; a < D; ++a) Mx[a * D + a] += 1.0;
+        double Fn[D * D];
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) Fn[k] = (double)P[(L::F + k) * cap + p];
+        const double V0 = (double)P[L::VOL * cap + p];
+        const int mid = mat[p];
+        const double mu = mt.mu[mid], lam = mt.lam[mid];
+        const double detM = det<D, double>(Mx), detFn = det<D, double>(Fn);
+        if (!(detM > 0.0 && detFn > 0.0)) {
+            red[2] += 1.0;
+            continue;
+        }
+        const double lnJ = log(detM) + log(detFn);
+        double tr = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int bb = 0; bb < D; ++bb) {
+                double s = 0.0;
+#pragma unroll
+                for (int k = 0; k < D; ++k) s += Mx[a * D + k] * Fn[k * D + bb];
+                tr += s * s;  // |M F^n|_F^2 = tr(M S M^T)
+            }
+        const double psiV = V0 * (0.5 * mu * (tr - D) - mu * lnJ + 0.5 * lam * lnJ * lnJ);
+        red[0] += psiV;
+        red[1] += fabs(psiV);
+    }
+    block_reduce_store<3>(red, partials);
+}
+
+// =============================================================================================
+// a8: G2P + F update + advection, per particle
+// =============================================================================================
+template <int D, typename R>
+__global__ void k_g2p(R* __restrict__ P, int64_t cap, int64_t n, const int* __restrict__ pid, BoxDev b,
+                      const double* __restrict__ vg, double dt, ErrLatch* err)
+{
+    using L = PL<D>;
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    R w[3][3], dw[3][3], f[3];
+    int c[3] = {0, 0, 0};
+    const R inv_dx = (R)b.inv_dx, dx = (R)b.dx;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        c[a] = base_of<R>(P[(L::X + a) * cap + p], b.o[a], b.inv_dx, &f[a]) - b.lo[a];
+        bspline<R>(f[a], inv_dx, w[a], dw[a]);
+    }
+    R vp[D], Bp[D * D], gv[D * D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) vp[a] = 0;
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) Bp[k] = gv[k] = 0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int k = 0; k < Tile<D>::K3; ++k) {
+                R N, gN[3], off[3];
+                off[0] = dx * (R(i) - f[0]);
+                off[1] = dx * (R(j) - f[1]);
+                if (D == 3) {
+                    off[2] = dx * (R(k) - f[2]);
+                    N = w[0][i] * w[1][j] * w[2][k];
+                    gN[0] = dw[0][i] * w[1][j] * w[2][k];
+                    gN[1] = w[0][i] * dw[1][j] * w[2][k];
+                    gN[2] = w[0][i] * w[1][j] * dw[2][k];
+                } else {
+                    N = w[0][i] * w[1][j];
+                    gN[0] = dw[0][i] * w[1][j];
+                    gN[1] = w[0][i] * dw[1][j];
+                }
+                const double* vv = vg + box_node<D>(b, c[0] + i, c[1] + j, c[2] + k) * D;
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    const R va = (R)vv[a];
+                    vp[a] += N * va;
+#pragma unroll
+                    for (int bb = 0; bb < D; ++bb) {
+                        Bp[a * D + bb] += N * va * off[bb];
+                        gv[a * D + bb] += va * gN[bb];
+                    }
+                }
+            }
+    R F[D * D], Fn[D * D];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) F[k] = P[(L::F + k) * cap + p];
+    const R rdt = (R)dt;
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int bb = 0; bb < D; ++bb) {
+            R s = F[a * D + bb];
+#pragma unroll
+            for (int k = 0; k < D; ++k) s += rdt * gv[a * D + k] * F[k * D + bb];
+            Fn[a * D + bb] = s;
+        }
+    if (!(det<D, R>(Fn) > R(0))) latch_error(err, 3 /*INVERTED_F*/, pid[p]);
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) {
+        P[(L::F + k) * cap + p] = Fn[k];
+        P[(L::B + k) * cap + p] = Bp[k];
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        const R xn = P[(L::X + a) * cap + p] + rdt * vp[a];
+        P[(L::X + a) * cap + p] = xn;
+        P[(L::V + a) * cap + p] = vp[a];
+        R ff;
+        const int bn = base_of<R>(xn, b.o[a], b.inv_dx, &ff);
+        if (bn < 0 || bn + 2 > b.gdims[a] - 1) latch_error(err, 2 /*OUT_OF_DOMAIN*/, pid[p]);
+    }
+}
+
+// =============================================================================================
+// node-level kernels: masks, Newton / PCG vector operations (a3, a6)
+// =============================================================================================
+// fmask = active & !dirichlet ; Newton initial guess (R5)
+template <int D>
+__global__ void k_newton_init(int64_t nn, const uint8_t* __restrict__ act, const uint8_t* __restrict__ dmask,
+                              const double* __restrict__ dval, const double* __restrict__ vn, double dt, int guess,
+                              uint8_t* __restrict__ fmask, double* __restrict__ u)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nn) return;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        const bool dir = (dmask[i] >> a) & 1;
+        const bool fr = act[i] && !dir;
+        fmask[i * D + a] = fr;
+        u[i * D + a] = fr ? (guess == 1 ? 0.0 : dt * vn[i * D + a]) : ((act[i] && dir) ? dt * dval[i * D + a] : 0.0);
+    }
+}
+
+struct CGScalars {
+    double rz, pq, alpha, beta, rr, gn, tol2, E0, Eabs0;
+    int done, it, negcurv_first, fixed;
+};
+
+// r = -g (free), z = r/diag, p = z, x = 0, y = 0 ; partials {rz, rr}
+template <int D>
+__global__ void k_cg_init(int64_t ndof, const uint8_t* __restrict__ fm, const double* __restrict__ g,
+                          double* __restrict__ dg, double* __restrict__ r, double* __restrict__ z,
+                          double* __restrict__ p, double* __restrict__ x, double* __restrict__ y,
+                          double* __restrict__ partials)
+{
+    double red[2] = {0.0, 0.0};
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ndof; k += (int64_t)gridDim.x * blockDim.x) {
+        const bool f = fm[k];
+        if (!f) dg[k] = 1.0;
+        const double rk = f ? -g[k] : 0.0;
+        const double zk = rk / dg[k];
+        r[k] = rk;
+        z[k] = zk;
+        p[k] = zk;
+        x[k] = 0.0;
+        y[k] = 0.0;
+        if (f) {
+            red[0] += rk * zk;
+            red[1] += rk * rk;
+        }
+    }
+    block_reduce_store<2>(red, partials);
+}
+
+__global__ void k_cg_init_fin(const double* partials, int nb, CGScalars* s, double gn, double cg_rtol, int fixed)
+{
+    double v[2];
+    final_sum<2>(partials, nb, v);
+    if (threadIdx.x == 0) {
+        s->rz = v[0];
+        s->rr = v[1];
+        s->gn = gn;
+        s->tol2 = cg_rtol * cg_rtol * gn * gn;
+        s->it = 0;
+        s->negcurv_first = 0;
+        s->fixed = fixed;
+        s->done = (!fixed && v[1] <= s->tol2) ? 1 : 0;
+        s->alpha = s->beta = 0.0;
+    }
+}
+
+// q = y + m/dt^2 p on free DOFs, 0 elsewhere (in place in y) ; partial p.q
+template <int D>
+__global__ void k_cg_q(int64_t nn, const uint8_t* __restrict__ fm, const double* __restrict__ m, double idt2,
+                       const double* __restrict__ p, double* __restrict__ y, const CGScalars* s,
+                       double* __restrict__ partials)
+{
+    double red[1] = {0.0};
+    if (!s->done) {
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
+            const double mi = m[i] * idt2;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const int64_t k = i * D + a;
+                const double q = fm[k] ? y[k] + mi * p[k] : 0.0;
+                y[k] = q;
+                red[0] += p[k] * q;
+            }
+        }
+    }
+    block_reduce_store<1>(red, partials);
+}
+
+__global__ void k_cg_alpha(const double* partials, int nb, CGScalars* s)
+{
+    if (s->done) return;
+    double v[1];
+    final_sum<1>(partials, nb, v);
+    if (threadIdx.x == 0) {
+        s->pq = v[0];
+        if (!(v[0] > 0.0)) {
+            s->alpha = 0.0;
+            if (!s->fixed) {
+                if (s->it == 0) s->negcurv_first = 1;
+                s->done = 2;  // negative curvature: stop (R7)
+            }
+        } else {
+            s->alpha = s->rz / v[0];
+        }
+    }
+}
+
+// x += alpha p ; r -= alpha q ; z = r/diag ; partials {r.z, r.r}
+__global__ void k_cg_update(int64_t ndof, const uint8_t* __restrict__ fm, const double* __restrict__ p,
+                            const double* __restrict__ q, const double* __restrict__ dg, double* __restrict__ x,
+                            double* __restrict__ r, double* __restrict__ z, const CGScalars* s,
+                            double* __restrict__ partials)
+{
+    double red[2] = {0.0, 0.0};
+    if (!s->done) {
+        const double al = s->alpha;
+        for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ndof; k += (int64_t)gridDim.x * blockDim.x) {
+            const double xk = x[k] + al * p[k];
+            const double rk = r[k] - al * q[k];
+            const double zk = fm[k] ? rk / dg[k] : 0.0;
+            x[k] = xk;
+            r[k] = rk;
+            z[k] = zk;
+            if (fm[k]) {
+                red[0] += rk * zk;
+                red[1] += rk * rk;
+            }
+        }
+    }
+    block_reduce_store<2>(red, partials);
+}
+
+__global__ void k_cg_beta(const double* partials, int nb, CGScalars* s)
+{
+    if (s->done) return;
+    double v[2];
+    final_sum<2>(partials, nb, v);
+    if (threadIdx.x == 0) {
+        s->beta = (s->rz > 0.0) ? v[0] / s->rz : 0.0;
+        s->rz = v[0];
+        s->rr = v[1];
+        s->it += 1;
+        if (!s->fixed && v[1] <= s->tol2) s->done = 1;
+    }
+}
+
+// p = z + beta p ; y = 0
+__global__ void k_cg_p(int64_t ndof, const double* __restrict__ z, double* __restrict__ p, double* __restrict__ y,
+                       const CGScalars* s)
+{
+    if (s->done) return;
+    const double be = s->beta;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ndof; k += (int64_t)gridDim.x * blockDim.x) {
+        p[k] = z[k] + be * p[k];
+        y[k] = 0.0;
+    }
+}
+
+// ut = u + alpha x on free DOFs
+__global__ void k_axpy_free(int64_t ndof, const uint8_t* __restrict__ fm, const double* __restrict__ u, double alpha,
+                            const double* __restrict__ x, double* __restrict__ ut)
+{
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ndof; k += (int64_t)gridDim.x * blockDim.x)
+        ut[k] = fm[k] ? u[k] + alpha * x[k] : u[k];
+}
+
+template <int NV>
+__global__ void k_final_sum(const double* partials, int nb, double* out)
+{
+    final_sum<NV>(partials, nb, out);
+}
+
+// v^{n+1} = u / dt on active nodes ("v = (x - x^n)/dT")
+template <int D>
+__global__ void k_vnew(int64_t nn, const uint8_t* __restrict__ act, const double* __restrict__ u, double inv_dt,
+                       double* __restrict__ v)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nn) return;
+#pragma unroll
+    for (int a = 0; a < D; ++a) v[i * D + a] = act[i] ? u[i * D + a] * inv_dt : 0.0;
+}
+
+// =============================================================================================
+// dense <-> box node vectors
+// =============================================================================================
+template <int D, typename T>
+__global__ void k_box_to_dense(BoxDev b, int ncomp, const T* __restrict__ src, T* __restrict__ dst)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= b.nnodes) return;
+    int i2 = (D == 3) ? (int)(i % b.nn[2]) : 0;
+    int i1 = (D == 3) ? (int)((i / b.nn[2]) % b.nn[1]) : (int)(i % b.nn[1]);
+    int i0 = (D == 3) ? (int)(i / ((int64_t)b.nn[2] * b.nn[1])) : (int)(i / b.nn[1]);
+    int g0 = b.lo[0] + i0, g1 = b.lo[1] + i1, g2 = (D == 3) ? b.lo[2] + i2 : 0;
+    if (g0 >= b.gdims[0] || g1 >= b.gdims[1] || (D == 3 && g2 >= b.gdims[2])) return;
+    int64_t g = (D == 3) ? ((int64_t)g0 * b.gdims[1] + g1) * b.gdims[2] + g2 : (int64_t)g0 * b.gdims[1] + g1;
+    for (int a = 0; a < ncomp; ++a) dst[g * ncomp + a] = src[i * ncomp + a];
+}
+
+template <int D, typename T>
+__global__ void k_dense_to_box(BoxDev b, int ncomp, const T* __restrict__ src, T* __restrict__ dst)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= b.nnodes) return;
+    int i2 = (D == 3) ? (int)(i % b.nn[2]) : 0;
+    int i1 = (D == 3) ? (int)((i / b.nn[2]) % b.nn[1]) : (int)(i % b.nn[1]);
+    int i0 = (D == 3) ? (int)(i / ((int64_t)b.nn[2] * b.nn[1])) : (int)(i / b.nn[1]);
+    int g0 = b.lo[0] + i0, g1 = b.lo[1] + i1, g2 = (D == 3) ? b.lo[2] + i2 : 0;
+    bool in = !(g0 >= b.gdims[0] || g1 >= b.gdims[1] || (D == 3 && g2 >= b.gdims[2]));
+    int64_t g = (D == 3) ? ((int64_t)g0 * b.gdims[1] + g1) * b.gdims[2] + g2 : (int64_t)g0 * b.gdims[1] + g1;
+    for (int a = 0; a < ncomp; ++a) dst[i * ncomp + a] = in ? src[g * ncomp + a] : T(0);
+}
+
+// Dirichlet list (global node index, mask, values) -> box arrays
+template <int D>
+__global__ void k_scatter_dirichlet(BoxDev b, int64_t n, const int64_t* __restrict__ gidx,
+                                    const uint8_t* __restrict__ mask, const double* __restrict__ val,
+                                    uint8_t* __restrict__ dmask, double* __restrict__ dval)
+{
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int64_t g = gidx[k];
+    int g2 = (D == 3) ? (int)(g % b.gdims[2]) : 0;
+    int g1 = (D == 3) ? (int)((g / b.gdims[2]) % b.gdims[1]) : (int)(g % b.gdims[1]);
+    int g0 = (D == 3) ? (int)(g / ((int64_t)b.gdims[2] * b.gdims[1])) : (int)(g / b.gdims[1]);
+    int i0 = g0 - b.lo[0], i1 = g1 - b.lo[1], i2 = (D == 3) ? g2 - b.lo[2] : 0;
+    if (i0 < 0 || i1 < 0 || i2 < 0 || i0 >= b.nn[0] || i1 >= b.nn[1] || (D == 3 && i2 >= b.nn[2])) return;
+    int64_t i = box_node<D>(b, i0, i1, i2);
+    dmask[i] |= mask[k];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+        if ((mask[k] >> a) & 1) dval[i * D + a] = val[k * D + a];
+}
+
+// unsort: dst[pid[i]] = src[i] for every real field
+template <typename R>
+__global__ void k_unsort_field(const R* __restrict__ src, int64_t n, const int* __restrict__ pid, int ncomp_stride,
+                               int comp, double* __restrict__ dst)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    dst[(int64_t)pid[i] * ncomp_stride + comp] = (double)src[i];
+}
+
+template <typename R>
+__global__ void k_sort_field(const double* __restrict__ src, int64_t n, const int* __restrict__ pid, int ncomp_stride,
+                             int comp, R* __restrict__ dst)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    dst[i] = (R)src[(int64_t)pid[i] * ncomp_stride + comp];
+}
+
+
+template <int D>
+__global__ void k_fext(int64_t nn, const double* m, double g0, double g1, double g2, double* out)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nn) return;
+    const double gg[3] = {g0, g1, g2};
+    for (int a = 0; a < D; ++a) out[i * D + a] = m[i] * gg[a];
+}
+
+template <int D>
+__global__ void k_add_mass(int64_t nn, const double* m, double idt2, const double* d, double* y)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nn) return;
+    for (int a = 0; a < D; ++a) y[i * D + a] += m[i] * idt2 * d[i * D + a];
+}
+
+// node part of E_h for the line search: {E_node, |E_node terms|}
+template <int D>
+__global__ void k_energy_nodes(int64_t nn, const double* __restrict__ m, const double* __restrict__ vn,
+                               const double* __restrict__ uu, double dt, double g0, double g1, double g2,
+                               double* __restrict__ partials)
+{
+    double red[2] = {0.0, 0.0};
+    const double grav[3] = {g0, g1, g2};
+    const double idt2 = 1.0 / (dt * dt);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
+        double q = 0.0, wf = 0.0;
+        for (int a = 0; a < D; ++a) {
+            const double rr = uu[i * D + a] - dt * vn[i * D + a];
+            q += rr * rr;
+            wf += uu[i * D + a] * m[i] * grav[a];
+        }
+        const double e = 0.5 * m[i] * idt2 * q;
+        red[0] += e - wf;
+        red[1] += e + fabs(wf);
+    }
+    block_reduce_store<2>(red, partials);
+}
+
+}  // namespace osmpm

@@ -1,0 +1,221 @@
+// transmit.cuh -- coarse<->fine transmission operators (§3.2.2-3.2.3):
+//   Pi_{S->B}  mass-weighted projection, Eq. spatial_projection
+//   I_{B->S}   shape-function interpolation, Eq. interp_BtoS
+//   T_m        linear temporal interpolation, Eq. temporal_interp
+#pragma once
+#include "subdomain.cuh"
+
+namespace osmpm {
+
+// coarse quadratic stencil of a point: 3^D (global coarse node index or -1 outside the dense box, N)
+template <int D>
+__device__ __forceinline__ void coarse_stencil(const double* xp, const double* o, double inv_dx, const int* gd,
+                                               int64_t* idx, double* N)
+{
+    int base[3] = {0, 0, 0};
+    double w[3][3], dw[3][3];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        double X = (xp[a] - o[a]) * inv_dx;
+        double b = floor(X - 0.5);
+        base[a] = (int)b;
+        bspline<double>(X - b, inv_dx, w[a], dw[a]);
+    }
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int k = 0; k < Tile<D>::K3; ++k) {
+                int k0 = base[0] + i, k1 = base[1] + j, k2 = (D == 3) ? base[2] + k : 0;
+                bool in = k0 >= 0 && k0 < gd[0] && k1 >= 0 && k1 < gd[1] && (D == 2 || (k2 >= 0 && k2 < gd[2]));
+                idx[c] = in ? ((D == 3) ? ((int64_t)k0 * gd[1] + k1) * gd[2] + k2 : (int64_t)k0 * gd[1] + k1) : -1;
+                N[c] = (D == 3) ? w[0][i] * w[1][j] * w[2][k] : w[0][i] * w[1][j];
+                ++c;
+            }
+}
+
+struct GridGeo {
+    double o[3];
+    double dx, inv_dx;
+    int gd[3];
+};
+
+// Pi numerator / denominator: every ACTIVE fine box node scatters m_j [v_j, 1] N_B,I(x_j)
+template <int D>
+__global__ void k_project(BoxDev fb, const uint8_t* __restrict__ act, const double* __restrict__ m,
+                          const double* __restrict__ v, GridGeo cg, double* __restrict__ num, double* __restrict__ den)
+{
+    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= fb.nnodes || !act[j]) return;
+    int i2 = (D == 3) ? (int)(j % fb.nn[2]) : 0;
+    int i1 = (D == 3) ? (int)((j / fb.nn[2]) % fb.nn[1]) : (int)(j % fb.nn[1]);
+    int i0 = (D == 3) ? (int)(j / ((int64_t)fb.nn[2] * fb.nn[1])) : (int)(j / fb.nn[1]);
+    const int gi[3] = {fb.lo[0] + i0, fb.lo[1] + i1, fb.lo[2] + i2};
+    double xj[3];
+#pragma unroll
+    for (int a = 0; a < D; ++a) xj[a] = fb.o[a] + fb.dx * (double)gi[a];
+    int64_t idx[27];
+    double N[27];
+    coarse_stencil<D>(xj, cg.o, cg.inv_dx, cg.gd, idx, N);
+    const double mj = m[j];
+#pragma unroll
+    for (int s = 0; s < Tile<D>::NS; ++s) {
+        if (idx[s] < 0) continue;
+        const double wgt = mj * N[s];
+        atomicAdd(&den[idx[s]], wgt);
+#pragma unroll
+        for (int a = 0; a < D; ++a) atomicAdd(&num[idx[s] * D + a], wgt * v[j * D + a]);
+    }
+}
+
+template <int D>
+__global__ void k_project_out(int64_t nt, const int64_t* __restrict__ targets, const double* __restrict__ num,
+                              const double* __restrict__ den, double eps, double* __restrict__ out)
+{
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    const int64_t I = targets ? targets[t] : t;
+#pragma unroll
+    for (int a = 0; a < D; ++a) out[t * D + a] = num[I * D + a] / (den[I] + eps);
+}
+
+// I + T: v_j = (1 - alpha) sum_I v0_I N_I(x_j) + alpha sum_I v1_I N_I(x_j); the coarse fields live
+// on the coarse subdomain's box (nodes outside the box carry zero velocity)
+template <int D>
+__global__ void k_interp(int64_t nt, const int64_t* __restrict__ targets, GridGeo fg, BoxDev cb,
+                         const double* __restrict__ v0, const double* __restrict__ v1, double alpha,
+                         double* __restrict__ out)
+{
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    const int64_t j = targets ? targets[t] : t;
+    int g2 = (D == 3) ? (int)(j % fg.gd[2]) : 0;
+    int g1 = (D == 3) ? (int)((j / fg.gd[2]) % fg.gd[1]) : (int)(j % fg.gd[1]);
+    int g0 = (D == 3) ? (int)(j / ((int64_t)fg.gd[2] * fg.gd[1])) : (int)(j / fg.gd[1]);
+    const int gi[3] = {g0, g1, g2};
+    double xj[3];
+#pragma unroll
+    for (int a = 0; a < D; ++a) xj[a] = fg.o[a] + fg.dx * (double)gi[a];
+    int64_t idx[27];
+    double N[27];
+    coarse_stencil<D>(xj, cb.o, cb.inv_dx, cb.gdims, idx, N);
+    double I0[3] = {0, 0, 0}, I1[3] = {0, 0, 0};
+#pragma unroll
+    for (int s = 0; s < Tile<D>::NS; ++s) {
+        if (idx[s] < 0) continue;
+        const int64_t I = idx[s];
+        int k2 = (D == 3) ? (int)(I % cb.gdims[2]) : 0;
+        int k1 = (D == 3) ? (int)((I / cb.gdims[2]) % cb.gdims[1]) : (int)(I % cb.gdims[1]);
+        int k0 = (D == 3) ? (int)(I / ((int64_t)cb.gdims[2] * cb.gdims[1])) : (int)(I / cb.gdims[1]);
+        int l0 = k0 - cb.lo[0], l1 = k1 - cb.lo[1], l2 = (D == 3) ? k2 - cb.lo[2] : 0;
+        if (l0 < 0 || l1 < 0 || l2 < 0 || l0 >= cb.nn[0] || l1 >= cb.nn[1] || (D == 3 && l2 >= cb.nn[2])) continue;
+        const int64_t bi = box_node<D>(cb, l0, l1, l2);
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            I0[a] += v0[bi * D + a] * N[s];
+            if (v1) I1[a] += v1[bi * D + a] * N[s];
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) out[t * D + a] = (1.0 - alpha) * I0[a] + alpha * I1[a];
+}
+
+template <int D, typename R>
+static GridGeo geo_of(const Sub<D, R>* s)
+{
+    GridGeo g{};
+    for (int a = 0; a < 3; ++a) {
+        g.o[a] = s->origin[a];
+        g.gd[a] = (int)s->gdims[a];
+    }
+    g.dx = s->dx;
+    g.inv_dx = 1.0 / s->dx;
+    return g;
+}
+
+// Pi over ALL coarse dense nodes: num (nnB*D), den (nnB) device buffers of the coarse side
+template <int D, typename R>
+osmpm_status project_accumulate(Sub<D, R>* fine, Sub<D, R>* coarse, bool use_solved, DBuf<double>& num,
+                                DBuf<double>& den)
+{
+    cudaStream_t st = fine->st();
+    const int64_t nnb = coarse->dense_nodes();
+    OSMPM_TRY(num.need(nnb * D));
+    OSMPM_TRY(den.need(nnb));
+    OSMPM_CU(cudaMemsetAsync(num.p, 0, nnb * D * sizeof(double), st));
+    OSMPM_CU(cudaMemsetAsync(den.p, 0, nnb * sizeof(double), st));
+    const double* v = use_solved ? fine->vnew.p : fine->vn.p;
+    if (fine->ctx->prof.on) fine->ctx->prof.begin("transmit", st);
+    k_project<D><<<nblk_all(fine->box.nnodes, 256), 256, 0, st>>>(fine->box, fine->act.p, fine->m.p, v, geo_of(coarse),
+                                                                  num.p, den.p);
+    OSMPM_LAUNCH_CHECK();
+    if (fine->ctx->prof.on) fine->ctx->prof.end("transmit", st);
+    return OSMPM_OK;
+}
+
+template <int D, typename R>
+osmpm_status transmit_impl(Sub<D, R>* src, Sub<D, R>* dst, osmpm_direction dir, double alpha, double eps,
+                           int64_t nt, const int64_t* targets, double* out, osmpm_memspace sp)
+{
+    cudaStream_t st = src->st();
+    if (!src->have_grid) {
+        set_error("transmit: source subdomain has no grid (call osmpm_p2g)");
+        return OSMPM_E_STATE;
+    }
+    if (alpha < 0.0 || alpha > 1.0) {
+        set_error("transmit: alpha = %g outside [0, 1] (m > M, SPEC.md:330)", alpha);
+        return OSMPM_E_INVALID_ARG;
+    }
+    const bool need_solved = alpha > 0.0;
+    if (need_solved && !src->have_vnew) {
+        set_error("transmit: alpha > 0 needs the source's solved grid velocity");
+        return OSMPM_E_STATE;
+    }
+    if (!targets && nt != dst->dense_nodes()) {
+        set_error("transmit: targets == NULL requires n_targets == dst node count (%lld)",
+                  (long long)dst->dense_nodes());
+        return OSMPM_E_INVALID_ARG;
+    }
+    DBuf<int64_t> tg;
+    const int64_t* tptr = targets;
+    if (targets && sp == OSMPM_HOST) {
+        OSMPM_TRY(tg.need(nt));
+        OSMPM_CU(cudaMemcpyAsync(tg.p, targets, nt * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        tptr = tg.p;
+    }
+    DBuf<double> ob;
+    double* optr = out;
+    if (sp == OSMPM_HOST) {
+        OSMPM_TRY(ob.need(nt * D));
+        optr = ob.p;
+    }
+    if (dir == OSMPM_FINE_TO_COARSE) {
+        if (alpha != 0.0 && alpha != 1.0) {
+            set_error("transmit FINE_TO_COARSE: alpha selects v^n (0) or v^{n+1} (1)");
+            return OSMPM_E_INVALID_ARG;
+        }
+        DBuf<double> num, den;
+        OSMPM_TRY(project_accumulate(src, dst, alpha == 1.0, num, den));
+        if (nt > 0) {
+            k_project_out<D><<<nblk_all(nt, 256), 256, 0, st>>>(nt, tptr, num.p, den.p, eps, optr);
+            OSMPM_LAUNCH_CHECK();
+        }
+    } else {
+        if (nt > 0) {
+            if (src->ctx->prof.on) src->ctx->prof.begin("transmit", st);
+            k_interp<D><<<nblk_all(nt, 256), 256, 0, st>>>(nt, tptr, geo_of(dst), src->box, src->vn.p,
+                                                           need_solved ? src->vnew.p : nullptr, alpha, optr);
+            OSMPM_LAUNCH_CHECK();
+            if (src->ctx->prof.on) src->ctx->prof.end("transmit", st);
+        }
+    }
+    if (sp == OSMPM_HOST) {
+        OSMPM_CU(cudaMemcpyAsync(out, optr, nt * D * sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    OSMPM_CU(cudaStreamSynchronize(st));
+    return OSMPM_OK;
+}
+
+}  // namespace osmpm

@@ -1,0 +1,217 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on identical seeded
+inputs, element by element (tolerance rel L∞ <= 1e-11 per kernel output in fp64,
+<= 1e-8 on Newton-converged solutions, <= 1e-4 for the fp32 variant; north_star)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_helpers import make_sub, random_u, rel_linf
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-11
+
+FIXTURES = {
+    # several tiles per axis and ragged tails (3D tiles are 4^3 cells, 2D tiles 8^2 cells)
+    "3d": dict(dim=3, cells=(10, 9, 7), seed=101),
+    "2d": dict(dim=2, cells=(21, 17, 1), seed=102),
+    "3d_dense": dict(dim=3, cells=(6, 5, 9), seed=103, ppa=3),
+}
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2605_09097_b200 import osmpm
+    c = osmpm.Context(0)
+    yield c
+    c.close()
+
+
+def _scene(name):
+    return synth.random_fixture(**FIXTURES[name])
+
+
+@pytest.mark.parametrize("name", list(FIXTURES))
+def test_p2g_parity(ctx, name):
+    sc = _scene(name)
+    ref = oracle.p2g(sc)
+    sub = make_sub(ctx, sc)
+    sub.p2g()
+    out = sub.read_grid()
+    np.testing.assert_array_equal(out["active"], ref.active)
+    assert rel_linf(out["m"], ref.m) <= TOL
+    assert rel_linf(out["p"], ref.p) <= TOL
+    assert rel_linf(out["v"], ref.v) <= TOL
+    assert rel_linf(out["fext"], ref.fext) <= TOL
+    assert rel_linf(out["fsig"], ref.fsig) <= TOL
+
+
+@pytest.mark.parametrize("name", list(FIXTURES))
+def test_gradient_hvp_diag_parity(ctx, name):
+    sc = _scene(name)
+    d = sc.grid.dim
+    ref = oracle.p2g(sc)
+    sub = make_sub(ctx, sc)
+    sub.p2g()
+    u = random_u(ref.active, d, 2e-3 * sc.grid.dx, 7)
+    g, E = sub.newton_gradient(u)
+    g_ref = oracle.gradient(sc, ref, u)
+    E_ref, _ = oracle.energy(sc, ref, u)
+    assert rel_linf(g, g_ref) <= TOL
+    assert abs(E - E_ref) <= TOL * abs(E_ref)
+    dg = sub.newton_diag()
+    assert rel_linf(dg, oracle.diag(sc, ref, u)) <= TOL
+    rng = np.random.default_rng(8)
+    for trial in range(2):
+        dv = rng.normal(size=u.shape) * sc.grid.dx
+        y = sub.newton_hvp(dv)
+        assert rel_linf(y, oracle.hvp(sc, ref, u, dv)) <= TOL
+
+
+@pytest.mark.parametrize("name", ["3d", "2d"])
+def test_g2p_parity(ctx, name):
+    sc = _scene(name)
+    d = sc.grid.dim
+    ref = oracle.p2g(sc)
+    sub = make_sub(ctx, sc)
+    sub.p2g()
+    rng = np.random.default_rng(9)
+    vg = np.zeros((ref.m.shape[0], d))
+    vg[ref.active.astype(bool)] = rng.normal(size=(int(ref.active.sum()), d))
+    sub.set_grid_velocity(vg)
+    sub.g2p()
+    sub.sync()
+    out = sub.read_particles()
+    pref = oracle.g2p(sc, vg)
+    for k, r in (("x", pref.x), ("v", pref.v), ("F", pref.F), ("B", pref.B)):
+        assert rel_linf(out[k], r) <= TOL, k
+
+
+@pytest.mark.parametrize("name", ["3d", "2d"])
+def test_implicit_solve_parity_converged(ctx, name):
+    from paper_2605_09097_b200 import osmpm
+    sc = synth.random_fixture(**{**FIXTURES[name], "cells": (5, 4, 4) if name == "3d" else (9, 8, 1)})
+    ref = oracle.p2g(sc)
+    kw = dict(newton_rtol=1e-12, cg_rtol=1e-12, max_cg=4000, max_newton=50)
+    u_ref, st_ref = oracle.implicit_solve(sc, ref, oracle.default_settings(**kw))
+    sub = make_sub(ctx, sc)
+    sub.p2g()
+    st = sub.implicit_solve(osmpm.newton_settings(**kw))
+    assert st.status == 0 and st_ref.status == 0
+    v = sub.read_grid_velocity()
+    act = ref.active.astype(bool)
+    v_ref = np.where(act[:, None], u_ref / sc.dt, 0.0)
+    assert rel_linf(v, v_ref) <= 1e-8
+
+
+def test_implicit_solve_parity_fixed_iterations(ctx):
+    from paper_2605_09097_b200 import osmpm
+    sc = synth.random_fixture(dim=3, cells=(5, 5, 4), seed=104)
+    ref = oracle.p2g(sc)
+    kw = dict(max_newton=3, max_cg=20, fixed_iters=1)
+    u_ref, st_ref = oracle.implicit_solve(sc, ref, oracle.default_settings(**kw))
+    sub = make_sub(ctx, sc)
+    sub.p2g()
+    st = sub.implicit_solve(osmpm.newton_settings(**kw))
+    assert st.newton_iters == 3 and st.cg_iters == 60
+    v = sub.read_grid_velocity()
+    act = ref.active.astype(bool)
+    assert rel_linf(v, np.where(act[:, None], u_ref / sc.dt, 0.0)) <= 1e-9
+
+
+def test_dirichlet_parity(ctx):
+    from paper_2605_09097_b200 import osmpm
+    sc = synth.random_fixture(dim=2, cells=(10, 8, 1), seed=105)
+    ref = oracle.p2g(sc)
+    d = 2
+    nn = ref.m.shape[0]
+    rng = np.random.default_rng(3)
+    act = np.flatnonzero(ref.active)
+    sel = rng.choice(act, size=len(act) // 5, replace=False)
+    masks = rng.integers(1, 4, size=sel.size).astype(np.uint8)
+    vel = rng.normal(size=(sel.size, d))
+    dm = np.zeros((nn, d), np.uint8)
+    dv = np.zeros((nn, d))
+    for i, mk, vv in zip(sel, masks, vel):
+        for a in range(d):
+            if (mk >> a) & 1:
+                dm[i, a] = 1
+                dv[i, a] = vv[a]
+    kw = dict(newton_rtol=1e-12, cg_rtol=1e-12, max_cg=4000)
+    u_ref, _ = oracle.implicit_solve(sc, ref, oracle.default_settings(**kw), dirichlet_mask=dm, dirichlet_v=dv)
+    sub = make_sub(ctx, sc)
+    sub.set_dirichlet(sel, masks, vel)
+    sub.p2g()
+    sub.implicit_solve(osmpm.newton_settings(**kw))
+    v = sub.read_grid_velocity()
+    assert rel_linf(v, np.where(ref.active[:, None].astype(bool), u_ref / sc.dt, 0.0)) <= 1e-8
+
+
+def test_transmit_parity(ctx):
+    from paper_2605_09097_b200 import osmpm
+    # fine subdomain inside a coarse one, r = 4
+    fine = synth.random_fixture(dim=3, cells=(8, 8, 6), seed=106, dx=0.025)
+    coarse = synth.random_fixture(dim=3, cells=(6, 6, 5), seed=107, dx=0.1)
+    coarse.particles.x -= 0.1  # cover the fine block
+    coarse.grid = synth.grid_around(coarse.particles.x, 0.1, 4, 3)
+    rf = oracle.p2g(fine)
+    rc = oracle.p2g(coarse)
+    sf = make_sub(ctx, fine)
+    scs = make_sub(ctx, coarse)
+    sf.p2g()
+    scs.p2g()
+    nb = rc.m.shape[0]
+    # Pi of the fine v^n onto every coarse node
+    out = osmpm.transmit(sf, scs, osmpm.FINE_TO_COARSE, alpha=0.0, eps_tol=1e-12)
+    vb_ref, num, den = oracle.project(fine.grid, rf, coarse.grid, eps_tol=1e-12)
+    assert rel_linf(out, vb_ref) <= TOL
+    # I + T with the coarse v^n and a set v^{n+1}
+    rng = np.random.default_rng(4)
+    v1 = np.zeros((nb, 3))
+    v1[rc.active.astype(bool)] = rng.normal(size=(int(rc.active.sum()), 3))
+    scs.set_grid_velocity(v1)
+    targets = np.flatnonzero(rf.active)
+    for alpha in (0.0, 0.25, 1.0):
+        o = osmpm.transmit(scs, sf, osmpm.COARSE_TO_FINE, alpha=alpha, targets=targets)
+        r = oracle.interp(coarse.grid, rc.v, v1, alpha, fine.grid, targets)
+        assert rel_linf(o, r) <= TOL
+
+
+def test_empty_and_single_particle(ctx):
+    sc = synth.random_fixture(dim=3, cells=(1, 1, 1), ppa=1, seed=108)
+    sub = make_sub(ctx, sc)
+    sub.p2g()
+    ref = oracle.p2g(sc)
+    assert rel_linf(sub.read_grid()["m"], ref.m) <= TOL
+    empty = synth.random_fixture(dim=2, cells=(2, 2, 1), seed=109)
+    empty.particles = empty.particles.subset(np.zeros(empty.particles.n, bool))
+    sub = make_sub(ctx, empty)
+    sub.p2g()
+    assert np.abs(sub.read_grid()["m"]).max() == 0.0
+
+
+def test_out_of_domain_is_reported(ctx):
+    from paper_2605_09097_b200 import osmpm
+    sc = synth.random_fixture(dim=2, cells=(3, 3, 1), seed=110)
+    sc.particles.x[5, 0] = sc.grid.origin[0] + 0.4 * sc.grid.dx  # base = -1
+    with pytest.raises(osmpm.OsmpmError) as ei:
+        make_sub(ctx, sc)
+    assert ei.value.code == 2 and "particle 5" in str(ei.value)
+
+
+def test_fp32_variant_within_1e_4(ctx):
+    from paper_2605_09097_b200 import osmpm
+    sc = _scene("3d")
+    d = 3
+    ref = oracle.p2g(sc)
+    sub = make_sub(ctx, sc, precision=osmpm.F32)
+    sub.p2g()
+    out = sub.read_grid()
+    assert rel_linf(out["m"], ref.m) <= 1e-4
+    assert rel_linf(out["p"], ref.p) <= 1e-4
+    u = random_u(ref.active, d, 2e-3 * sc.grid.dx, 7)
+    g, E = sub.newton_gradient(u)
+    assert rel_linf(g, oracle.gradient(sc, ref, u)) <= 1e-4
+    dv = np.random.default_rng(8).normal(size=u.shape) * sc.grid.dx
+    assert rel_linf(sub.newton_hvp(dv), oracle.hvp(sc, ref, u, dv)) <= 1e-4
