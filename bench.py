@@ -1,0 +1,365 @@
+"""bench.py -- one OS-MPM fine implicit sub-step on the C5 workload (BASELINE.json configs[4]).
+
+A step = everything a fine sub-step of Alg. 1 does on 16,777,216 particles:
+  sort + APIC P2G (mass, momentum, stress)            -> osmpm_p2g
+  Pi_{S->B} onto the dx = 1/128 overlap grid          -> osmpm_transmit(FINE_TO_COARSE)
+  I_{B->S} + T_m (alpha = 1/2) onto the fine receivers -> osmpm_transmit(COARSE_TO_FINE) -> Dirichlet
+  backward-Euler Newton: exactly 10 Newton x 50 PCG HVPs, line search -> osmpm_implicit_solve
+  G2P + F update + advection                          -> osmpm_g2p
+Metric: particle-substeps/s = N_particles / step time (BASELINE.json `metric`).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--precision f64|f32]
+Prints ONE JSON line on rank 0.  See DESIGN.md §7 for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "implicit MPM particle-substeps/sec (C5 fine sub-step: P2G + Pi + I/T + 10 Newton x 50 PCG HVPs + G2P)"
+UNIT = "particle-substeps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="osmpm", choices=["osmpm", "reference"])
+    ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--cells", type=int, default=128, help="cube side in cells (128 -> 16.7M particles)")
+    ap.add_argument("--newton", type=int, default=10)
+    ap.add_argument("--cg", type=int, default=50)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-cells", type=int, default=14, help="oracle sample cube side (cells)")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------------------
+# workload
+# ------------------------------------------------------------------------------------------------
+
+def build_workload(cells):
+    import synth
+    fine = synth.c5_stress(n_cells=cells)
+    cgrid, cvel = synth.c5_coarse_field(fine.grid, n_cells=cells)
+    # passive coarse subdomain: 1 particle per coarse cell carrying the smooth field
+    # (its P2G gives v_B^n; v_B^{n+1} is the field shifted in time)
+    side = cells * fine.grid.dx
+    lo = 0.5 - side / 2
+    xb, vol = synth.lattice([lo] * 3, [lo + side] * 3, cgrid.dx, 1)
+    cpart = synth.make_particles(xb, vol, 1000.0)
+    idx = np.clip(np.round((xb - np.asarray(cgrid.origin)) / cgrid.dx).astype(int), 0, cgrid.dims[0] - 1)
+    cpart.v = np.ascontiguousarray(cvel[idx[:, 0], idx[:, 1], idx[:, 2]])
+    coarse = synth.Scene(cgrid, cpart, [(1.0e5, 0.3)], 4e-3, (0.0, 0.0, 0.0))
+    # fine receivers: fine nodes of the material footprint outside the cube shrunk by 2 cells
+    k0 = int(round((0.5 - side / 2) / fine.grid.dx))
+    n_nodes_side = cells + 3
+    kk = np.arange(k0 - 1, k0 - 1 + n_nodes_side)
+    K = np.stack(np.meshgrid(kk, kk, kk, indexing="ij"), -1).reshape(-1, 3)
+    inner = np.all((K >= k0 + 2) & (K <= k0 + cells - 2), axis=1)
+    R = K[~inner]
+    gd = fine.grid.dims
+    recv = (R[:, 0] * gd[1] + R[:, 1]) * gd[2] + R[:, 2]
+    return fine, coarse, cvel, np.ascontiguousarray(recv.astype(np.int64))
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+# ------------------------------------------------------------------------------------------------
+
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = max(smax, float(f[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------------
+# roofline accounting: algorithmic bytes of one HVP launch
+# ------------------------------------------------------------------------------------------------
+
+def hvp_algorithmic_bytes(n_particles, n_active_nodes, word):
+    # per particle: x (3) + Newton cache S' (6) + Ah (9) + c' + l' (2) = 20 words of the particle
+    # precision; per active node: read d (3) + write y (3) fp64 words
+    return n_particles * 20 * word + n_active_nodes * 6 * 8
+
+
+def load_traffic(prec):
+    path = os.path.join(ROOT, "profiles", f"ncu_hvp_{prec}.json")
+    if os.path.exists(path):
+        try:
+            return json.load(open(path)).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU oracle baseline (bounded sample)
+# ------------------------------------------------------------------------------------------------
+
+def oracle_substep_rate(cells, newton, cg):
+    """Time the fp64 oracle, as it stands, on one full fine sub-step of a `cells`^3 C5 cube."""
+    import oracle
+    import synth
+    sc = synth.c5_stress(n_cells=cells, full_box=False)
+    t0 = time.perf_counter()
+    gs = oracle.p2g(sc)
+    u, st = oracle.implicit_solve(sc, gs, oracle.default_settings(max_newton=newton, max_cg=cg, fixed_iters=1),
+                                  raise_on_error=False)
+    act = gs.active.astype(bool)
+    oracle.g2p(sc, np.where(act[:, None], u / sc.dt, 0.0))
+    dt = time.perf_counter() - t0
+    return sc.particles.n / dt, dt, sc.particles.n
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    cells = args.cpu_cells
+    for _ in range(args.warmup):
+        oracle_substep_rate(max(4, cells // 2), 1, 2)
+    times = []
+    n = 0
+    for _ in range(args.steps):
+        rate, dt, n = oracle_substep_rate(cells, args.newton, args.cg)
+        times.append(dt)
+    t = max(statistics.median(times), 1e-12)
+    value = n / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C5 sample: {cells}^3-cell cube, {n} particles, one fine sub-step "
+                               f"({args.newton} Newton x {args.cg} PCG)", "cells": cells},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{cells}^3-cell C5 cube ({n} particles), full sub-step per timed step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist = tdist
+    else:
+        torch.cuda.set_device(local_rank)
+    from paper_2605_09097_b200 import osmpm
+
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream(dev)
+    ctx = osmpm.Context(local_rank, stream.cuda_stream)
+    prec = osmpm.F64 if args.precision == "f64" else osmpm.F32
+    word = 8 if args.precision == "f64" else 4
+
+    fine, coarse, cvel, recv = build_workload(args.cells)
+    n = fine.particles.n
+    sub = osmpm.Subdomain(ctx, fine.grid, fine.dt, fine.particles, fine.materials, fine.gravity, precision=prec)
+    csub = osmpm.Subdomain(ctx, coarse.grid, coarse.dt, coarse.particles, coarse.materials, coarse.gravity,
+                           precision=prec)
+    csub.p2g()
+    cg = csub.read_grid(device=dev)
+    # v_B^{n+1}: the smooth field advanced (scaled) in time -> distinct endpoint for T_m
+    csub.set_grid_velocity((cg["v"] * 1.01).contiguous())
+    recv_d = torch.from_numpy(recv).to(dev)
+    settings = osmpm.newton_settings(max_newton=args.newton, max_cg=args.cg, fixed_iters=1)
+    mask_all = torch.full((recv.shape[0],), 7, dtype=torch.uint8, device=dev)
+
+    def step():
+        sub.p2g()
+        vb = osmpm.transmit(sub, csub, osmpm.FINE_TO_COARSE, alpha=0.0, eps_tol=1e-12, device=dev)
+        vS = osmpm.transmit(csub, sub, osmpm.COARSE_TO_FINE, alpha=0.5, targets=recv_d, device=dev)
+        sub.set_dirichlet_device(recv_d, mask_all, vS)
+        sub.implicit_solve(settings)
+        sub.g2p()
+        return vb
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    sub.p2g()  # (untimed) grid of the current state, for the active-node count of the roofline
+    _, _, box_dims = sub.info()
+    g = sub.read_grid(device=dev)
+    n_active = int(g["active"].sum().item())
+    del g
+
+    clocks = ClockSampler(local_rank)
+    ctx.profile(True)
+    ctx.profile_reset()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    l0 = ctx.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ck = clocks.stop()
+    launches_timed = ctx.launch_count() - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    hv_n, hv_ms = ctx.kernel_time("hvp")
+    fam = {f: ctx.kernel_time(f) for f in ("hvp", "grad", "energy", "p2g", "g2p", "sort", "cg", "transmit")}
+    ctx.profile(False)
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+
+    # end-to-end through the public API with pinned host buffers (H2D inputs, D2H result)
+    e2e = None
+    if not args.no_e2e:
+        pin = {k: torch.from_numpy(np.ascontiguousarray(getattr(fine.particles, k))).pin_memory()
+               for k in ("x", "v", "F", "B")}
+        outx = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+        outv = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+        h2d = sum(v.numel() * 8 for v in pin.values())
+        d2h = (outx.numel() + outv.numel()) * 8
+
+        def e2e_step():
+            sub.set_particles(pin["x"], pin["v"], pin["F"], pin["B"])
+            step()
+            sub.read_particles_into(x=outx, v=outv)
+
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        f1.record(stream)
+        torch.cuda.synchronize(dev)
+        te = torch.tensor([f0.elapsed_time(f1) / args.steps], device=dev, dtype=torch.float64)
+        if dist:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * n / (float(te.item()) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": float(te.item())}
+
+    if rank != 0:
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peak, peak_kind = peaks()
+    hvp_bytes = hvp_algorithmic_bytes(n, n_active, word)
+    hvp_avg_ms = hv_ms / max(hv_n, 1)
+    achieved = hvp_bytes / (hvp_avg_ms * 1e-3) / 1e9
+    traffic = load_traffic(args.precision)
+    cpu = None
+    if not args.no_cpu_baseline:
+        rate, dt, ncpu = oracle_substep_rate(args.cpu_cells, args.newton, args.cg)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"one fine sub-step ({args.newton} Newton x {args.cg} PCG) of a {args.cpu_cells}^3-cell C5 "
+                         f"cube ({ncpu} particles), {dt:.1f} s single-threaded"}
+    line = {
+        "metric": METRIC, "value": world * n / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+        "config": {"workload": "C5 (BASELINE.json configs[4]): random-density neo-Hookean cube, 128^3 cells at "
+                               "dx=1/512, 8 ppc, one fine implicit sub-step (10 Newton x 50 PCG) with "
+                               "coarse<->fine transmission to the dx=1/128 overlap grid",
+                   "particles_per_gpu": n, "cells": args.cells, "newton": args.newton, "cg": args.cg,
+                   "active_nodes": n_active, "box_nodes": int(np.prod(box_dims)), "receivers": int(recv.shape[0]),
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "working set (>3 GB) far larger than the 126 MB L2; no flush needed"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "k_hvp", "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": hvp_bytes, "avg_launch_ms": hvp_avg_ms,
+                     "launches": hv_n},
+        "kernel_ms_per_step": {f: v[1] / args.steps for f, v in fam.items()},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches_timed,
+        "clocks": ck,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

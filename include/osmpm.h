@@ -145,6 +145,8 @@ void osmpm_ctx_destroy(osmpm_ctx* ctx);
 osmpm_status osmpm_profile_enable(osmpm_ctx* ctx, int enable);
 osmpm_status osmpm_profile_reset(osmpm_ctx* ctx);
 osmpm_status osmpm_kernel_time(osmpm_ctx* ctx, const char* family, int64_t* launches, double* ms);
+/* Number of CUDA kernels the library has launched on this ctx since creation (all families). */
+osmpm_status osmpm_launch_count(osmpm_ctx* ctx, int64_t* launches);
 
 /* ----------------------------------------------------------------------------------------------
  * Subdomain (§3.1: each subdomain owns a grid (dx, dt) and its particles)

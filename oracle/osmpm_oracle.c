@@ -354,14 +354,16 @@ int orc_energy(const orc_grid* g, int64_t np, const double* x, const double* F, 
     int64_t nn = n_nodes(g);
     double e = 0.0, ea = 0.0;
     for (int64_t i = 0; i < nn; ++i) {
-        double q = 0.0, w = 0.0;
+        double q = 0.0, w = 0.0, qa = 0.0;
         for (int a = 0; a < d; ++a) {
             double r = u[i * d + a] - dt * vn[i * d + a];
             q += r * r;
             w += u[i * d + a] * fext[i * d + a];
+            qa += u[i * d + a] * u[i * d + a] + dt * dt * vn[i * d + a] * vn[i * d + a];
         }
         e += mi[i] / (2.0 * dt * dt) * q - w;
-        ea += mi[i] / (2.0 * dt * dt) * q + fabs(w);
+        /* round-off scale of the inertia term |u - dt v|^2 is |u|^2 + |dt v|^2 (R8) */
+        ea += mi[i] / (2.0 * dt * dt) * qa + fabs(w);
     }
     int64_t idx[27];
     double N[27], gN[81], xip[81], Fu[9];
@@ -542,15 +544,29 @@ int orc_implicit_solve(const orc_grid* g, int64_t np, const double* x, const dou
         if (free_mask[k]) u[k] = (st->guess == 1) ? 0.0 : dt * vn[k];
     double g0 = 0.0;
     int converged = 0;
+    /* natural force scale f_s = || m_i (|v_i^n| / dt + |g|) || over the free DOFs: the Newton test is
+     * relative to max(|g^(0)|, f_s) so that a state already at equilibrium counts as converged
+     * (R6) */
+    double fs = 0.0;
+    for (int64_t k = 0; k < nd; ++k)
+        if (free_mask[k]) {
+            double t = mi[k / d] * fabs(vn[k]) / dt + fabs(fext[k]);
+            fs += t * t;
+        }
+    fs = sqrt(fs);
+    double gref = 0.0;
     for (int it = 0; it < st->max_newton; ++it) {
         rc = orc_gradient(g, np, x, F, V0, mat, E, nu, dt, mi, vn, fext, u, gr);
         if (rc) goto done;
         for (int64_t k = 0; k < nd; ++k)
             if (!free_mask[k]) gr[k] = 0.0;
         double gn = sqrt(dot_free(nd, free_mask, gr, gr));
-        if (it == 0) g0 = gn;
+        if (it == 0) {
+            g0 = gn;
+            gref = g0 > fs ? g0 : fs;
+        }
         stats->grad_norm = gn;
-        if (!st->fixed_iters && (gn <= st->newton_rtol * g0 || gn <= st->newton_atol)) {
+        if (!st->fixed_iters && (gn <= st->newton_rtol * gref || gn <= st->newton_atol)) {
             converged = 1;
             break;
         }
@@ -622,7 +638,7 @@ int orc_implicit_solve(const orc_grid* g, int64_t np, const double* x, const dou
             if (!free_mask[k]) gr[k] = 0.0;
         double gn = sqrt(dot_free(nd, free_mask, gr, gr));
         stats->grad_norm = gn;
-        if (!(gn <= st->newton_rtol * g0 || gn <= st->newton_atol)) rc = ORC_NEWTON_NC;
+        if (!(gn <= st->newton_rtol * gref || gn <= st->newton_atol)) rc = ORC_NEWTON_NC;
     }
 done:
     stats->grad_norm0 = g0;

@@ -143,6 +143,13 @@ osmpm_status osmpm_kernel_time(osmpm_ctx* ctx, const char* family, int64_t* laun
     return ctx->prof.query(family, launches, ms);
 }
 
+osmpm_status osmpm_launch_count(osmpm_ctx* ctx, int64_t* launches)
+{
+    CHECK_ARG(ctx && launches, "NULL argument");
+    *launches = ctx->launches;
+    return OSMPM_OK;
+}
+
 osmpm_status osmpm_subdomain_create(osmpm_ctx* ctx, const osmpm_grid_desc* grid, double dt,
                                     const osmpm_particles_view* particles, const osmpm_material* mats,
                                     int32_t n_mats, const double gravity[3], osmpm_precision prec,

@@ -11,24 +11,34 @@ namespace osmpm {
 // quadratic stencil ("cell" b covers nodes b..b+2).  Cells are grouped into tiles of T0 x T1 x T2
 // cells; a tile owns the (T0+2)(T1+2)(T2+2) nodes its particles touch.  One CTA per tile.
 // ---------------------------------------------------------------------------------------------
+// Inside a tile, cells are ordered LAYER-MAJOR along the last axis (z in 3D, y in 2D): a layer
+// is the LC = T0 (x T1) cells with one last-axis index; the tiled kernels walk the layers in order.
 template <int D> struct Tile;
 template <> struct Tile<3> {
     static constexpr int T0 = 4, T1 = 4, T2 = 4;
     static constexpr int NC = T0 * T1 * T2;                   // cells per tile
+    static constexpr int LC = T0 * T1;                        // cells per layer
+    static constexpr int NL = T2;                             // layers per tile
     static constexpr int N0 = T0 + 2, N1 = T1 + 2, N2 = T2 + 2;
     static constexpr int NN = N0 * N1 * N2;                   // nodes per tile
     static constexpr int NS = 27;                             // stencil nodes
     static constexpr int K3 = 3;
-    static constexpr int NT = NC * 3;                         // threads: (cell, component)
+    static constexpr int ITEMS = LC * 3 * 3;                  // scatter items (cell, comp, i)
+    static constexpr int NACC = 9;                            // accumulators per item (j, k)
+    static constexpr int NT = 144;                            // threads per CTA (= ITEMS)
 };
 template <> struct Tile<2> {
-    static constexpr int T0 = 8, T1 = 8, T2 = 1;
+    static constexpr int T0 = 16, T1 = 4, T2 = 1;
     static constexpr int NC = T0 * T1;
+    static constexpr int LC = T0;
+    static constexpr int NL = T1;
     static constexpr int N0 = T0 + 2, N1 = T1 + 2, N2 = 1;
     static constexpr int NN = N0 * N1;
     static constexpr int NS = 9;
     static constexpr int K3 = 1;
-    static constexpr int NT = NC * 2;
+    static constexpr int ITEMS = LC * 2 * 3;
+    static constexpr int NACC = 3;                            // accumulators per item (j)
+    static constexpr int NT = 96;                             // threads per CTA (= ITEMS)
 };
 
 // Node box of the current step (all integers are global node / cell indices).
@@ -59,7 +69,8 @@ __device__ __forceinline__ uint32_t cell_key(const BoxDev& b, int c0, int c1, in
     int t0 = c0 / T::T0, t1 = c1 / T::T1, t2 = (D == 3) ? c2 / T::T2 : 0;
     int l0 = c0 - t0 * T::T0, l1 = c1 - t1 * T::T1, l2 = (D == 3) ? c2 - t2 * T::T2 : 0;
     uint32_t tile = (D == 3) ? ((uint32_t)t0 * b.nt[1] + t1) * b.nt[2] + t2 : (uint32_t)t0 * b.nt[1] + t1;
-    uint32_t loc = (D == 3) ? (l0 * T::T1 + l1) * T::T2 + l2 : l0 * T::T1 + l1;
+    // layer-major: the last axis is slowest inside the tile
+    uint32_t loc = (D == 3) ? (l2 * T::T0 + l0) * T::T1 + l1 : l1 * T::T0 + l0;
     return tile * T::NC + loc;
 }
 

@@ -215,524 +215,49 @@ __global__ void k_bmass(const R* __restrict__ P, int64_t cap, int64_t n, const u
             }
 }
 
-// =============================================================================================
-// tiled particle-loop scatter machinery (HVP, gradient, diagonal)
-//   phase 0: stage the tile's (T+2)^D nodes of the input vector in shared memory
-//   phase 1: per particle (thread per particle): weights, gather, per-particle source -> smem
-//   phase 2: per (cell, component) thread: register accumulation of its cell's particles'
-//            contributions to the 3^D stencil nodes (tensor-product evaluation)
-//   phase 3: per (node, component): sum the <= 3^D cell partials, one fp64 RED per node
-// =============================================================================================
-template <int D> struct ChunkLayout {
-    // per-particle smem fields (field-major with stride NT): w[D][3], dw[D][3], G[D][D]
-    static constexpr int W = 0, DW = 3 * D, G = 6 * D, NF = 6 * D + D * D;
-};
-
-template <int D>
-__device__ __forceinline__ void tile_coords(const BoxDev& b, int tile, int* t)
-{
-    if (D == 3) {
-        t[2] = tile % b.nt[2];
-        t[1] = (tile / b.nt[2]) % b.nt[1];
-        t[0] = tile / (b.nt[2] * b.nt[1]);
-    } else {
-        t[2] = 0;
-        t[1] = tile % b.nt[1];
-        t[0] = tile / b.nt[1];
-    }
-}
-
-// phase 0: sv[l*D + a] = vec[global node of tile-local node l][a]
-template <int D, typename R>
-__device__ __forceinline__ void stage_nodes(const BoxDev& b, const int* t, const double* __restrict__ vec, R* sv)
-{
-    using T = Tile<D>;
-    for (int i = threadIdx.x; i < T::NN * D; i += T::NT) {
-        int a = i % D, l = i / D;
-        int l2 = (D == 3) ? l % T::N2 : 0;
-        int l1 = (D == 3) ? (l / T::N2) % T::N1 : l % T::N1;
-        int l0 = (D == 3) ? l / (T::N2 * T::N1) : l / T::N1;
-        int64_t g = box_node<D>(b, t[0] * T::T0 + l0, t[1] * T::T1 + l1, t[2] * T::T2 + l2);
-        sv[i] = (R)vec[g * D + a];
-    }
-}
-
-template <int D>
-__device__ __forceinline__ int tnode(int l0, int l1, int l2)
-{
-    using T = Tile<D>;
-    return (D == 3) ? (l0 * T::N1 + l1) * T::N2 + l2 : l0 * T::N1 + l1;
-}
-
-// gather gd[a][b] = sum_i v_i,a dN_i/dx_b over the stencil (tensor-product order)
-template <int D, typename R>
-__device__ __forceinline__ void gather_grad(const R* sv, const int* lc, const R (*w)[3], const R (*dw)[3], R* gd)
-{
-#pragma unroll
-    for (int k = 0; k < D * D; ++k) gd[k] = 0;
-    if (D == 3) {
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            R U0[3] = {0, 0, 0}, U1[3] = {0, 0, 0}, U2[3] = {0, 0, 0};
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                R T0[3] = {0, 0, 0}, T1[3] = {0, 0, 0};
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    const R* s = sv + tnode<D>(lc[0] + i, lc[1] + j, lc[2] + k) * D;
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) {
-                        T0[a] += s[a] * w[2][k];
-                        T1[a] += s[a] * dw[2][k];
-                    }
-                }
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    U0[a] += T0[a] * w[1][j];
-                    U1[a] += T0[a] * dw[1][j];
-                    U2[a] += T1[a] * w[1][j];
-                }
-            }
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                gd[a * 3 + 0] += U0[a] * dw[0][i];
-                gd[a * 3 + 1] += U1[a] * w[0][i];
-                gd[a * 3 + 2] += U2[a] * w[0][i];
-            }
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            R U0[2] = {0, 0}, U1[2] = {0, 0};
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                const R* s = sv + tnode<D>(lc[0] + i, lc[1] + j, 0) * D;
-#pragma unroll
-                for (int a = 0; a < 2; ++a) {
-                    U0[a] += s[a] * w[1][j];
-                    U1[a] += s[a] * dw[1][j];
-                }
-            }
-#pragma unroll
-            for (int a = 0; a < 2; ++a) {
-                gd[a * 2 + 0] += U0[a] * dw[0][i];
-                gd[a * 2 + 1] += U1[a] * w[0][i];
-            }
-        }
-    }
-}
-
-// phase 2 (linear): acc[node] += sum_b s_b dN_node/dx_b
-template <int D, typename R>
-__device__ __forceinline__ void scatter_linear(const R* s, const R (*w)[3], const R (*dw)[3], R* acc)
-{
-    if (D == 3) {
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            const R ax = s[0] * dw[0][i], bx = s[1] * w[0][i], cx = s[2] * w[0][i];
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                const R A = ax * w[1][j] + bx * dw[1][j];
-                const R B = cx * w[1][j];
-#pragma unroll
-                for (int k = 0; k < 3; ++k) acc[(i * 3 + j) * 3 + k] += A * w[2][k] + B * dw[2][k];
-            }
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            const R ax = s[0] * dw[0][i], bx = s[1] * w[0][i];
-#pragma unroll
-            for (int j = 0; j < 3; ++j) acc[i * 3 + j] += ax * w[1][j] + bx * dw[1][j];
-        }
-    }
-}
-
-// phase 2 (quadratic): acc[node] += gradN^T Q gradN, Q symmetric (Sym<D> storage)
-template <int D, typename R>
-__device__ __forceinline__ void scatter_quadratic(const R* Q, const R (*w)[3], const R (*dw)[3], R* acc)
-{
-    if (D == 3) {
-        R y2[3], yy[3], dy2[3], z2[3], zz[3], dz2[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            y2[k] = w[1][k] * w[1][k];
-            yy[k] = w[1][k] * dw[1][k];
-            dy2[k] = dw[1][k] * dw[1][k];
-            z2[k] = w[2][k] * w[2][k];
-            zz[k] = w[2][k] * dw[2][k];
-            dz2[k] = dw[2][k] * dw[2][k];
-        }
-        const R q00 = Q[0], q11 = Q[1], q22 = Q[2], q01 = R(2) * Q[3], q02 = R(2) * Q[4], q12 = R(2) * Q[5];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            const R pxx = dw[0][i] * dw[0][i], pxw = dw[0][i] * w[0][i], pww = w[0][i] * w[0][i];
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                const R C2 = q00 * pxx * y2[j] + q11 * pww * dy2[j] + q01 * pxw * yy[j];
-                const R C1 = q02 * pxw * y2[j] + q12 * pww * yy[j];
-                const R C0 = q22 * pww * y2[j];
-#pragma unroll
-                for (int k = 0; k < 3; ++k) acc[(i * 3 + j) * 3 + k] += C2 * z2[k] + C1 * zz[k] + C0 * dz2[k];
-            }
-        }
-    } else {
-        const R q00 = Q[0], q11 = Q[1], q01 = R(2) * Q[2];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            const R pxx = dw[0][i] * dw[0][i], pxw = dw[0][i] * w[0][i], pww = w[0][i] * w[0][i];
-#pragma unroll
-            for (int j = 0; j < 3; ++j)
-                acc[i * 3 + j] += q00 * pxx * w[1][j] * w[1][j] + q11 * pww * dw[1][j] * dw[1][j] +
-                                  q01 * pxw * w[1][j] * dw[1][j];
-        }
-    }
-}
-
-// phase 3: node sums of the per-cell partials, one RED per (node, component)
-template <int D, typename R>
-__device__ __forceinline__ void flush_tile(const BoxDev& b, const int* t, const R* acc, double* __restrict__ out)
-{
-    using T = Tile<D>;
-    for (int idx = threadIdx.x; idx < T::NN * D; idx += T::NT) {
-        const int a = idx % D, l = idx / D;
-        const int l2 = (D == 3) ? l % T::N2 : 0;
-        const int l1 = (D == 3) ? (l / T::N2) % T::N1 : l % T::N1;
-        const int l0 = (D == 3) ? l / (T::N2 * T::N1) : l / T::N1;
-        R s = 0;
-        bool any = false;
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            const int c0 = l0 - i;
-            if (c0 < 0 || c0 >= T::T0) continue;
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                const int c1 = l1 - j;
-                if (c1 < 0 || c1 >= T::T1) continue;
-#pragma unroll
-                for (int k = 0; k < T::K3; ++k) {
-                    const int c2 = l2 - k;
-                    if (D == 3 && (c2 < 0 || c2 >= T::T2)) continue;
-                    const int c = (D == 3) ? (c0 * T::T1 + c1) * T::T2 + c2 : c0 * T::T1 + c1;
-                    s += acc[(c * D + a) * T::NS + (i * 3 + j) * T::K3 + k];
-                    any = true;
-                }
-            }
-        }
-        if (any && s != R(0)) {
-            int64_t g = box_node<D>(b, t[0] * T::T0 + l0, t[1] * T::T1 + l1, t[2] * T::T2 + l2);
-            atomicAdd(&out[g * D + a], (double)s);
-        }
-    }
-}
-
-// =============================================================================================
-// a5: HVP  y += sum_p V0 dP(F_p(u); gd F^n) F^nT grad N  =  sum_p G_p grad N with
-//     G = gd S' + c' Ah gd^T Ah + l' (Ah : gd) Ah   (derivation from PAPER.md:188, 208)
-// =============================================================================================
-template <int D, typename R>
-__global__ void __launch_bounds__(Tile<D>::NT)
-k_hvp(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, const int* __restrict__ cell_start,
-      BoxDev b, const double* __restrict__ din, double* __restrict__ yout)
-{
-    using T = Tile<D>;
-    using CLY = ChunkLayout<D>;
-    using L = PL<D>;
-    using C = CL<D>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    R* sv = reinterpret_cast<R*>(smem_raw);
-    R* sp = sv + T::NN * D;
-    const int tile = blockIdx.x;
-    const int pbeg = cell_start[(int64_t)tile * T::NC], pend = cell_start[(int64_t)(tile + 1) * T::NC];
-    if (pbeg == pend) return;
-    int t[3];
-    tile_coords<D>(b, tile, t);
-    stage_nodes<D, R>(b, t, din, sv);
-    __syncthreads();
-    const R inv_dx = (R)b.inv_dx;
-    for (int cb = pbeg; cb < pend; cb += T::NT) {
-        const int ce = min(cb + T::NT, pend);
-        const int q = threadIdx.x;
-        const int p = cb + q;
-        if (p < ce) {
-            R w[3][3], dw[3][3], f;
-            int lc[3] = {0, 0, 0};
-#pragma unroll
-            for (int a = 0; a < D; ++a) {
-                const int tt = a == 0 ? T::T0 : (a == 1 ? T::T1 : T::T2);
-                lc[a] = base_of<R>(P[(L::X + a) * cap + p], b.o[a], b.inv_dx, &f) - b.lo[a] - t[a] * tt;
-                bspline<R>(f, inv_dx, w[a], dw[a]);
-            }
-            R gd[D * D];
-            gather_grad<D, R>(sv, lc, w, dw, gd);
-            R S[Sym<D>::N], A[D * D];
-#pragma unroll
-            for (int k = 0; k < Sym<D>::N; ++k) S[k] = cache[(C::S + k) * cap + p];
-#pragma unroll
-            for (int k = 0; k < D * D; ++k) A[k] = cache[(C::A + k) * cap + p];
-            const R cc = cache[C::C * cap + p], ll = cache[C::L * cap + p];
-            // M2 = A gd^T ; tr = A : gd
-            R M2[D * D], tr = 0;
-#pragma unroll
-            for (int a = 0; a < D; ++a)
-#pragma unroll
-                for (int bb = 0; bb < D; ++bb) {
-                    R s = 0;
-#pragma unroll
-                    for (int k = 0; k < D; ++k) s += A[a * D + k] * gd[bb * D + k];
-                    M2[a * D + bb] = s;
-                    tr += A[a * D + bb] * gd[a * D + bb];
-                }
-            const R ltr = ll * tr;
-#pragma unroll
-            for (int a = 0; a < D; ++a)
-#pragma unroll
-                for (int bb = 0; bb < D; ++bb) {
-                    R s1 = 0, s2 = 0;
-#pragma unroll
-                    for (int k = 0; k < D; ++k) {
-                        s1 += gd[a * D + k] * S[sym_idx<D>(k, bb)];
-                        s2 += M2[a * D + k] * A[k * D + bb];
-                    }
-                    sp[(CLY::G + a * D + bb) * T::NT + q] = s1 + cc * s2 + ltr * A[a * D + bb];
-                }
-#pragma unroll
-            for (int a = 0; a < D; ++a)
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    sp[(CLY::W + a * 3 + k) * T::NT + q] = w[a][k];
-                    sp[(CLY::DW + a * 3 + k) * T::NT + q] = dw[a][k];
-                }
-        }
-        __syncthreads();
-        const int cell = threadIdx.x / D, comp = threadIdx.x % D;
-        const int64_t key = (int64_t)tile * T::NC + cell;
-        const int s0 = max(cell_start[key], cb), s1 = min(cell_start[key + 1], ce);
-        R acc[T::NS];
-#pragma unroll
-        for (int k = 0; k < T::NS; ++k) acc[k] = 0;
-        for (int pp = s0; pp < s1; ++pp) {
-            const int qq = pp - cb;
-            R w[3][3], dw[3][3], s[D];
-#pragma unroll
-            for (int a = 0; a < D; ++a)
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    w[a][k] = sp[(CLY::W + a * 3 + k) * T::NT + qq];
-                    dw[a][k] = sp[(CLY::DW + a * 3 + k) * T::NT + qq];
-                }
-#pragma unroll
-            for (int bb = 0; bb < D; ++bb) s[bb] = sp[(CLY::G + comp * D + bb) * T::NT + qq];
-            scatter_linear<D, R>(s, w, dw, acc);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < T::NS; ++k) sp[(cell * D + comp) * T::NS + k] = acc[k];
-        __syncthreads();
-        flush_tile<D, R>(b, t, sp, yout);
-        __syncthreads();
-    }
-}
-
-// =============================================================================================
-// a4: gradient + energy + Newton cache + Jacobi diagonal (tiled)
-//   M = I + grad u, F(u) = M F^n, J = det M det F^n,  Ah = M^{-T},  S = F^n F^nT
-//   G_grad = V0 P(F(u)) F^nT = M S' - c' Ah ;  diag_a += gradN^T (S' + (c' + l') Ah_a Ah_a^T) gradN
-//   Psi = mu/2 (tr(M S M^T) - d) - mu ln J + lam/2 ln^2 J
-// partials per CTA: {sum V0 Psi, sum V0 |Psi|, inverted}
-// =============================================================================================
-template <int D> struct GradLayout {
-    static constexpr int W = 0, DW = 3 * D, G = 6 * D, S = G + D * D, A = S + Sym<D>::N, CL = A + D * D,
-                         NF = CL + 1;
-};
-
-template <int D, typename R>
-__global__ void __launch_bounds__(Tile<D>::NT)
-k_grad(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int* __restrict__ mat,
-       const int* __restrict__ cell_start, BoxDev b, MatTable mt, const double* __restrict__ uin,
-       double* __restrict__ gout, double* __restrict__ dout, double* __restrict__ partials)
-{
-    using T = Tile<D>;
-    using GL = GradLayout<D>;
-    using L = PL<D>;
-    using C = CL<D>;
-    using Rd = double;  // gradient / energy arithmetic in fp64 (R14)
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Rd* sv = reinterpret_cast<Rd*>(smem_raw);
-    Rd* sp = sv + T::NN * D;
-    const int tile = blockIdx.x;
-    const int pbeg = cell_start[(int64_t)tile * T::NC], pend = cell_start[(int64_t)(tile + 1) * T::NC];
-    double red[3] = {0.0, 0.0, 0.0};
-    if (pbeg == pend) {
-        if (threadIdx.x == 0) {
-            partials[blockIdx.x * 3 + 0] = 0.0;
-            partials[blockIdx.x * 3 + 1] = 0.0;
-            partials[blockIdx.x * 3 + 2] = 0.0;
-        }
-        return;
-    }
-    int t[3];
-    tile_coords<D>(b, tile, t);
-    stage_nodes<D, Rd>(b, t, uin, sv);
-    __syncthreads();
-    for (int cb = pbeg; cb < pend; cb += T::NT) {
-        const int ce = min(cb + T::NT, pend);
-        const int q = threadIdx.x;
-        const int p = cb + q;
-        if (p < ce) {
-            Rd w[3][3], dw[3][3], f;
-            int lc[3] = {0, 0, 0};
-#pragma unroll
-            for (int a = 0; a < D; ++a) {
-                const int tt = a == 0 ? T::T0 : (a == 1 ? T::T1 : T::T2);
-                lc[a] = base_of<Rd>((Rd)P[(L::X + a) * cap + p], b.o[a], b.inv_dx, &f) - b.lo[a] - t[a] * tt;
-                bspline<Rd>(f, b.inv_dx, w[a], dw[a]);
-            }
-            Rd Mx[D * D];
-            gather_grad<D, Rd>(sv, lc, w, dw, Mx);
-#pragma unroll
-            for (int a = 0; a < D; ++a) Mx[a * D + a] += 1.0;
-            Rd Fn[D * D];
-#pragma unroll
-            for (int k = 0; k < D * D; ++k) Fn[k] = (Rd)P[(L::F + k) * cap + p];
-            const Rd V0 = (Rd)P[L::VOL * cap + p];
-            const int mid = mat[p];
-            const Rd mu = mt.mu[mid], lam = mt.lam[mid];
-            Rd S[Sym<D>::N];
-#pragma unroll
-            for (int a = 0; a < D; ++a)
-#pragma unroll
-                for (int bb = a; bb < D; ++bb) {
-                    Rd s = 0;
-#pragma unroll
-                    for (int k = 0; k < D; ++k) s += Fn[a * D + k] * Fn[bb * D + k];
-                    S[sym_idx<D>(a, bb)] = V0 * mu * s;  // S' = V0 mu F^n F^nT
-                }
-            const Rd detM = det<D, Rd>(Mx), detFn = det<D, Rd>(Fn);
-            Rd Ah[D * D];
-            cofactor<D, Rd>(Mx, Ah);
-            const Rd invdet = 1.0 / detM;
-#pragma unroll
-            for (int k = 0; k < D * D; ++k) Ah[k] *= invdet;
-            const bool ok = detM > 0.0 && detFn > 0.0;
-            const Rd lnJ = ok ? log(detM) + log(detFn) : 0.0;
-            const Rd cc = V0 * (mu - lam * lnJ), ll = V0 * lam;
-            // tr(M S' M^T) (S' carries V0 mu)
-            Rd trMSM = 0;
-#pragma unroll
-            for (int a = 0; a < D; ++a)
-#pragma unroll
-                for (int bb = 0; bb < D; ++bb) {
-                    Rd s = 0;
-#pragma unroll
-                    for (int k = 0; k < D; ++k) s += Mx[a * D + k] * S[sym_idx<D>(k, bb)];
-                    trMSM += s * Mx[a * D + bb];
-                    sp[(GL::G + a * D + bb) * T::NT + q] = s - cc * Ah[a * D + bb];
-                }
-            const Rd psiV = 0.5 * (trMSM - V0 * mu * D) - V0 * mu * lnJ + 0.5 * V0 * lam * lnJ * lnJ;
-            red[0] += psiV;
-            red[1] += fabs(psiV);
-            if (!ok) red[2] += 1.0;
-#pragma unroll
-            for (int k = 0; k < Sym<D>::N; ++k) {
-                sp[(GL::S + k) * T::NT + q] = S[k];
-                cache[(C::S + k) * cap + p] = (R)S[k];
-            }
-#pragma unroll
-            for (int k = 0; k < D * D; ++k) {
-                sp[(GL::A + k) * T::NT + q] = Ah[k];
-                cache[(C::A + k) * cap + p] = (R)Ah[k];
-            }
-            cache[C::C * cap + p] = (R)cc;
-            cache[C::L * cap + p] = (R)ll;
-            sp[GL::CL * T::NT + q] = cc + ll;
-#pragma unroll
-            for (int a = 0; a < D; ++a)
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    sp[(GL::W + a * 3 + k) * T::NT + q] = w[a][k];
-                    sp[(GL::DW + a * 3 + k) * T::NT + q] = dw[a][k];
-                }
-        }
-        __syncthreads();
-        const int cell = threadIdx.x / D, comp = threadIdx.x % D;
-        const int64_t key = (int64_t)tile * T::NC + cell;
-        const int s0 = max(cell_start[key], cb), s1 = min(cell_start[key + 1], ce);
-        Rd acc[T::NS], accd[T::NS];
-#pragma unroll
-        for (int k = 0; k < T::NS; ++k) acc[k] = accd[k] = 0;
-        for (int pp = s0; pp < s1; ++pp) {
-            const int qq = pp - cb;
-            Rd w[3][3], dw[3][3], s[D], Q[Sym<D>::N], Ar[D];
-#pragma unroll
-            for (int a = 0; a < D; ++a)
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    w[a][k] = sp[(GL::W + a * 3 + k) * T::NT + qq];
-                    dw[a][k] = sp[(GL::DW + a * 3 + k) * T::NT + qq];
-                }
-#pragma unroll
-            for (int bb = 0; bb < D; ++bb) {
-                s[bb] = sp[(GL::G + comp * D + bb) * T::NT + qq];
-                Ar[bb] = sp[(GL::A + comp * D + bb) * T::NT + qq];
-            }
-            const Rd clv = sp[GL::CL * T::NT + qq];
-#pragma unroll
-            for (int a = 0; a < D; ++a)
-#pragma unroll
-                for (int bb = a; bb < D; ++bb)
-                    Q[sym_idx<D>(a, bb)] = sp[(GL::S + sym_idx<D>(a, bb)) * T::NT + qq] + clv * Ar[a] * Ar[bb];
-            scatter_linear<D, Rd>(s, w, dw, acc);
-            scatter_quadratic<D, Rd>(Q, w, dw, accd);
-        }
-        __syncthreads();
-        Rd* accs = sp;                                  // aliases the chunk buffer
-        Rd* accs2 = sp + T::NC * D * T::NS;
-#pragma unroll
-        for (int k = 0; k < T::NS; ++k) {
-            accs[(cell * D + comp) * T::NS + k] = acc[k];
-            accs2[(cell * D + comp) * T::NS + k] = accd[k];
-        }
-        __syncthreads();
-        flush_tile<D, Rd>(b, t, accs, gout);
-        flush_tile<D, Rd>(b, t, accs2, dout);
-        __syncthreads();
-    }
-    block_reduce_store<3>(red, partials);
-}
+}  // namespace osmpm
+#include "tiled.cuh"
+namespace osmpm {
 
 // node terms of the gradient / diagonal / energy:
 //   g += m/dt^2 (u - dt v^n) - m grav ;  diag += m/dt^2 ;
 //   E_node = m/(2dt^2)|u - dt v^n|^2 - u . m grav ;  |g_free|^2
-// partials per block: {E_node, |E_node terms|, |g_free|^2}
+//   noise scale m/(2dt^2)(|u|^2 + |dt v^n|^2) + |u . m grav|  (R8)
+//   force scale |m (|v^n|/dt + |grav|)|^2 over free DOFs      (R6)
+// partials per block: {E_node, E_abs node terms, |g_free|^2, force scale^2}
 template <int D>
 __global__ void k_grad_nodes(int64_t nn, const double* __restrict__ m, const double* __restrict__ vn,
                              const double* __restrict__ u, const uint8_t* __restrict__ fmask, double dt,
                              double g0, double g1, double g2, double* __restrict__ g, double* __restrict__ dg,
                              double* __restrict__ partials)
 {
-    double red[3] = {0.0, 0.0, 0.0};
+    double red[4] = {0.0, 0.0, 0.0, 0.0};
     const double grav[3] = {g0, g1, g2};
     const double idt2 = 1.0 / (dt * dt);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
         const double mi = m[i];
-        double q = 0.0, wf = 0.0;
+        double q = 0.0, wf = 0.0, qa = 0.0;
 #pragma unroll
         for (int a = 0; a < D; ++a) {
-            const double r = u[i * D + a] - dt * vn[i * D + a];
+            const double ua = u[i * D + a], va = vn[i * D + a];
+            const double r = ua - dt * va;
             const double fe = mi * grav[a];
             q += r * r;
-            wf += u[i * D + a] * fe;
+            wf += ua * fe;
+            qa += ua * ua + dt * dt * va * va;
             const double gv = g[i * D + a] + mi * idt2 * r - fe;
             g[i * D + a] = gv;
             dg[i * D + a] += mi * idt2;
-            if (fmask[i * D + a]) red[2] += gv * gv;
+            if (fmask[i * D + a]) {
+                red[2] += gv * gv;
+                const double fs = mi * fabs(va) / dt + fabs(fe);
+                red[3] += fs * fs;
+            }
         }
-        const double e = 0.5 * mi * idt2 * q;
-        red[0] += e - wf;
-        red[1] += e + fabs(wf);
+        red[0] += 0.5 * mi * idt2 * q - wf;
+        red[1] += 0.5 * mi * idt2 * qa + fabs(wf);
     }
-    block_reduce_store<3>(red, partials);
+    block_reduce_store<4>(red, partials);
 }
 
 // =============================================================================================
@@ -1177,15 +702,16 @@ __global__ void k_energy_nodes(int64_t nn, const double* __restrict__ m, const d
     const double grav[3] = {g0, g1, g2};
     const double idt2 = 1.0 / (dt * dt);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
-        double q = 0.0, wf = 0.0;
+        double q = 0.0, wf = 0.0, qa = 0.0;
         for (int a = 0; a < D; ++a) {
-            const double rr = uu[i * D + a] - dt * vn[i * D + a];
+            const double ua = uu[i * D + a], va = vn[i * D + a];
+            const double rr = ua - dt * va;
             q += rr * rr;
-            wf += uu[i * D + a] * m[i] * grav[a];
+            wf += ua * m[i] * grav[a];
+            qa += ua * ua + dt * dt * va * va;
         }
-        const double e = 0.5 * m[i] * idt2 * q;
-        red[0] += e - wf;
-        red[1] += e + fabs(wf);
+        red[0] += 0.5 * m[i] * idt2 * q - wf;
+        red[1] += 0.5 * m[i] * idt2 * qa + fabs(wf);
     }
     block_reduce_store<2>(red, partials);
 }

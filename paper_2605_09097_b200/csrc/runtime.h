@@ -63,6 +63,7 @@ struct osmpm_ctx {
     bool own_stream = false;
     osmpm::Profiler prof;
     int num_sms = 148;
+    int64_t launches = 0;  // kernels launched through this ctx (bench gpu_launches)
 };
 
 struct osmpm_subdomain {

@@ -4,6 +4,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -89,6 +90,7 @@ struct Sub : public osmpm_subdomain {
     DBuf<double> m, mom, vn, fsig, mb, dval, u, g, dg, xs, r, z, p, y, ut, vnew, tmp;
     DBuf<uint8_t> act, dmask, fmask;
     DirList dir_user, dir_cpl;
+    DBuf<double> stage_io;  // persistent host-I/O staging buffer
 
     // ---- reductions / scalars ---------------------------------------------------------------
     DBuf<double> partA, partB, scal;
@@ -107,6 +109,7 @@ struct Sub : public osmpm_subdomain {
     }
 
     cudaStream_t st() const { return ctx->stream; }
+    void KC() const { ctx->launches++; }
 
     // =========================================================================================
     // creation
@@ -131,7 +134,9 @@ struct Sub : public osmpm_subdomain {
             mats.lam[k] = mt[k].E * mt[k].nu / ((1.0 + mt[k].nu) * (1.0 - 2.0 * mt[k].nu));
         }
         n = pv->n;
-        cap = std::max<int64_t>(n, 1);
+        // field stride: a multiple of 4 (16-B aligned fields for the TMA bulk copies) with >= 4
+        // elements of slack (bulk copies round their length up to 16 B)
+        cap = ((n + 4 + 3) / 4) * 4;
         OSMPM_CU(cudaMallocHost((void**)&h_scal, 64 * sizeof(double)));
         OSMPM_CU(cudaMallocHost((void**)&h_cgs, sizeof(CGScalars)));
         OSMPM_CU(cudaMallocHost((void**)&h_bounds, 8 * sizeof(int)));
@@ -271,7 +276,7 @@ struct Sub : public osmpm_subdomain {
         int init[8] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MIN, INT32_MIN, INT32_MIN, 0, 0};
         OSMPM_CU(cudaMemcpyAsync(bounds.p, init, sizeof(init), cudaMemcpyHostToDevice, st()));
         if (n > 0) {
-            k_bounds<D, R><<<nblk(n, 256), 256, 0, st()>>>(P.p, cap, n, b, bounds.p, pid.p, err.p);
+            KC(); k_bounds<D, R><<<nblk(n, 256), 256, 0, st()>>>(P.p, cap, n, b, bounds.p, pid.p, err.p);
             OSMPM_LAUNCH_CHECK();
         }
         OSMPM_CU(cudaMemcpyAsync(h_bounds, bounds.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, st()));
@@ -320,7 +325,7 @@ struct Sub : public osmpm_subdomain {
         OSMPM_TRY(cell_start.need(box.ncells + 1));
         auto& pf = ctx->prof;
         if (pf.on) pf.begin("sort", st());
-        k_keys<D, R><<<nblk_all(n, 256), 256, 0, st()>>>(P.p, cap, n, box, keys.p, vals.p);
+        KC(); k_keys<D, R><<<nblk_all(n, 256), 256, 0, st()>>>(P.p, cap, n, box, keys.p, vals.p);
         OSMPM_LAUNCH_CHECK();
         int nbits = 1;
         while ((int64_t(1) << nbits) < box.ncells) ++nbits;
@@ -329,7 +334,7 @@ struct Sub : public osmpm_subdomain {
         OSMPM_TRY(cub_tmp.need(bytes));
         OSMPM_CU(cub::DeviceRadixSort::SortPairs(cub_tmp.p, bytes, keys.p, keys2.p, vals.p, vals2.p, (int)n, 0,
                                                  nbits, st()));
-        k_permute<R><<<nblk_all(n, 256), 256, 0, st()>>>(P.p, P2.p, L::NF, cap, n, vals2.p, mat.p, mat2.p, bnd.p,
+        KC(); k_permute<R><<<nblk_all(n, 256), 256, 0, st()>>>(P.p, P2.p, L::NF, cap, n, vals2.p, mat.p, mat2.p, bnd.p,
                                                          bnd2.p, pid.p, pid2.p);
         OSMPM_LAUNCH_CHECK();
         std::swap(P.p, P2.p);
@@ -340,7 +345,7 @@ struct Sub : public osmpm_subdomain {
         std::swap(bnd.cap, bnd2.cap);
         std::swap(pid.p, pid2.p);
         std::swap(pid.cap, pid2.cap);
-        k_cell_start<<<nblk_all(n + 1, 256), 256, 0, st()>>>(keys2.p, n, box.ncells, cell_start.p);
+        KC(); k_cell_start<<<nblk_all(n + 1, 256), 256, 0, st()>>>(keys2.p, n, box.ncells, cell_start.p);
         OSMPM_LAUNCH_CHECK();
         if (pf.on) pf.end("sort", st());
         return OSMPM_OK;
@@ -377,10 +382,10 @@ struct Sub : public osmpm_subdomain {
         auto& pf = ctx->prof;
         if (pf.on) pf.begin("p2g", st());
         if (n > 0) {
-            k_p2g<D, R><<<nblk_all(n, 128), 128, 0, st()>>>(P.p, cap, n, mat.p, box, mats, m.p, mom.p, fsig.p);
+            KC(); k_p2g<D, R><<<nblk_all(n, 128), 128, 0, st()>>>(P.p, cap, n, mat.p, box, mats, m.p, mom.p, fsig.p);
             OSMPM_LAUNCH_CHECK();
         }
-        k_p2g_nodes<D><<<nblk_all(nn, 256), 256, 0, st()>>>(nn, m.p, mom.p, vn.p, act.p, mass_thr);
+        KC(); k_p2g_nodes<D><<<nblk_all(nn, 256), 256, 0, st()>>>(nn, m.p, mom.p, vn.p, act.p, mass_thr);
         OSMPM_LAUNCH_CHECK();
         if (pf.on) pf.end("p2g", st());
         have_grid = true;
@@ -393,7 +398,7 @@ struct Sub : public osmpm_subdomain {
     {
         OSMPM_CU(cudaMemsetAsync(mb.p, 0, box.nnodes * sizeof(double), st()));
         if (n > 0) {
-            k_bmass<D, R><<<nblk_all(n, 128), 128, 0, st()>>>(P.p, cap, n, bnd.p, box, mb.p);
+            KC(); k_bmass<D, R><<<nblk_all(n, 128), 128, 0, st()>>>(P.p, cap, n, bnd.p, box, mb.p);
             OSMPM_LAUNCH_CHECK();
         }
         return OSMPM_OK;
@@ -409,14 +414,16 @@ struct Sub : public osmpm_subdomain {
     {
         const size_t cnt = (size_t)dense_nodes() * nc;
         Tv* dptr = dst;
-        DBuf<Tv> stage;
+        DBuf<Tv> local;
+        DBuf<Tv>* stage = &local;
+        if constexpr (std::is_same<Tv, double>::value) stage = &stage_io;
         if (sp == OSMPM_HOST) {
-            OSMPM_TRY(stage.need(cnt));
-            dptr = stage.p;
+            OSMPM_TRY(stage->need(cnt));
+            dptr = stage->p;
         }
         OSMPM_CU(cudaMemsetAsync(dptr, 0, cnt * sizeof(Tv), st()));
         if (have_grid) {
-            k_box_to_dense<D, Tv><<<nblk_all(box.nnodes, 256), 256, 0, st()>>>(box, nc, src, dptr);
+            KC(); k_box_to_dense<D, Tv><<<nblk_all(box.nnodes, 256), 256, 0, st()>>>(box, nc, src, dptr);
             OSMPM_LAUNCH_CHECK();
         }
         if (sp == OSMPM_HOST) {
@@ -430,13 +437,13 @@ struct Sub : public osmpm_subdomain {
     {
         const size_t cnt = (size_t)dense_nodes() * nc;
         const double* sptr = src;
-        DBuf<double> stage;
+        DBuf<double>& stage = stage_io;
         if (sp == OSMPM_HOST) {
             OSMPM_TRY(stage.need(cnt));
             OSMPM_CU(cudaMemcpyAsync(stage.p, src, cnt * sizeof(double), cudaMemcpyHostToDevice, st()));
             sptr = stage.p;
         }
-        k_dense_to_box<D, double><<<nblk_all(box.nnodes, 256), 256, 0, st()>>>(box, nc, sptr, dst);
+        KC(); k_dense_to_box<D, double><<<nblk_all(box.nnodes, 256), 256, 0, st()>>>(box, nc, sptr, dst);
         OSMPM_LAUNCH_CHECK();
         if (sp == OSMPM_HOST) OSMPM_CU(cudaStreamSynchronize(st()));
         return OSMPM_OK;
@@ -464,7 +471,7 @@ struct Sub : public osmpm_subdomain {
         if (fe) {
             // f_ext = m g (PAPER.md:178 with partition of unity)
             OSMPM_TRY(tmp.need(nn * D));
-            k_fext<D><<<nblk_all(nn, 256), 256, 0, st()>>>(nn, m.p, grav[0], grav[1], grav[2], tmp.p);
+            KC(); k_fext<D><<<nblk_all(nn, 256), 256, 0, st()>>>(nn, m.p, grav[0], grav[1], grav[2], tmp.p);
             OSMPM_LAUNCH_CHECK();
             OSMPM_TRY(export_dense<double>(tmp.p, D, fe, sp));
         }
@@ -477,17 +484,8 @@ struct Sub : public osmpm_subdomain {
     // a4: gradient + energy at u (box vector) -> g (raw), dg (raw), scalars
     // scal[0..2] particle {E, |E|, inverted}; scal[3..5] node {E, |E|, |g_free|^2}
     // =========================================================================================
-    size_t grad_smem() const
-    {
-        using GL = GradLayout<D>;
-        size_t sp_n = std::max<size_t>((size_t)GL::NF * T::NT, (size_t)2 * T::NC * D * T::NS);
-        return (T::NN * D + sp_n) * sizeof(double);
-    }
-    size_t hvp_smem() const
-    {
-        size_t sp_n = std::max<size_t>((size_t)ChunkLayout<D>::NF * T::NT, (size_t)T::NC * D * T::NS);
-        return (T::NN * D + sp_n) * sizeof(R);
-    }
+    size_t grad_smem() const { return grad_smem_bytes<D>(); }
+    size_t hvp_smem() const { return hvp_smem_bytes<D, R>(); }
 
     osmpm_status grad_eval(const double* uu, bool need_fmask)
     {
@@ -504,16 +502,17 @@ struct Sub : public osmpm_subdomain {
             attr = true;
         }
         if (pf.on) pf.begin("grad", st());
-        k_grad<D, R><<<box.ntiles, T::NT, grad_smem(), st()>>>(P.p, cache.p, cap, mat.p, cell_start.p, box, mats,
+        KC(); k_grad<D, R><<<box.ntiles, T::NT, grad_smem(), st()>>>(P.p, cache.p, cap, mat.p, cell_start.p, box, mats,
                                                                uu, g.p, dg.p, partA.p);
         OSMPM_LAUNCH_CHECK();
         if (pf.on) pf.end("grad", st());
         const int nbn = nblk(nn, 256);
-        k_grad_nodes<D><<<nbn, 256, 0, st()>>>(nn, m.p, vn.p, uu, fmask.p, dt, grav[0], grav[1], grav[2], g.p, dg.p,
+        KC(); k_grad_nodes<D><<<nbn, 256, 0, st()>>>(nn, m.p, vn.p, uu, fmask.p, dt, grav[0], grav[1], grav[2], g.p, dg.p,
                                                 partB.p);
         OSMPM_LAUNCH_CHECK();
-        k_final_sum<3><<<1, 1024, 0, st()>>>(partA.p, box.ntiles, scal.p);
-        k_final_sum<3><<<1, 1024, 0, st()>>>(partB.p, nbn, scal.p + 3);
+        // scal[0..2] particles {E, E_abs, inverted}; scal[3..6] nodes {E, E_abs, |g_free|^2, f_scale^2}
+        KC(); k_final_sum<3><<<1, 1024, 0, st()>>>(partA.p, box.ntiles, scal.p);
+        KC(); k_final_sum<4><<<1, 1024, 0, st()>>>(partB.p, nbn, scal.p + 3);
         OSMPM_LAUNCH_CHECK();
         have_lin = true;
         return OSMPM_OK;
@@ -545,7 +544,7 @@ struct Sub : public osmpm_subdomain {
     {
         auto& pf = ctx->prof;
         if (pf.on) pf.begin("hvp", st());
-        k_hvp<D, R><<<box.ntiles, T::NT, hvp_smem(), st()>>>(P.p, cache.p, cap, cell_start.p, box, din, yout);
+        KC(); k_hvp<D, R><<<box.ntiles, T::NT, hvp_smem(), st()>>>(P.p, cache.p, cap, cell_start.p, box, din, yout);
         OSMPM_LAUNCH_CHECK();
         if (pf.on) pf.end("hvp", st());
         return OSMPM_OK;
@@ -562,7 +561,7 @@ struct Sub : public osmpm_subdomain {
         OSMPM_TRY(import_dense(din, D, p.p, sp));
         OSMPM_CU(cudaMemsetAsync(y.p, 0, nn * D * sizeof(double), st()));
         OSMPM_TRY(launch_hvp(p.p, y.p));
-        k_add_mass<D><<<nblk_all(nn, 256), 256, 0, st()>>>(nn, m.p, 1.0 / (dt * dt), p.p, y.p);
+        KC(); k_add_mass<D><<<nblk_all(nn, 256), 256, 0, st()>>>(nn, m.p, 1.0 / (dt * dt), p.p, y.p);
         OSMPM_LAUNCH_CHECK();
         return export_dense<double>(y.p, D, yout, sp);
     }
@@ -587,7 +586,7 @@ struct Sub : public osmpm_subdomain {
         OSMPM_CU(cudaMemsetAsync(dval.p, 0, nn * D * sizeof(double), st()));
         for (DirList* dl : {&dir_user, &dir_cpl})
             if (dl->n > 0) {
-                k_scatter_dirichlet<D><<<nblk_all(dl->n, 256), 256, 0, st()>>>(box, dl->n, dl->idx.p, dl->mask.p,
+                KC(); k_scatter_dirichlet<D><<<nblk_all(dl->n, 256), 256, 0, st()>>>(box, dl->n, dl->idx.p, dl->mask.p,
                                                                                dl->val.p, dmask.p, dval.p);
                 OSMPM_LAUNCH_CHECK();
             }
@@ -622,14 +621,15 @@ struct Sub : public osmpm_subdomain {
         auto& pf = ctx->prof;
         const int nbp = nblk(n, 256);
         if (pf.on) pf.begin("energy", st());
-        k_energy<D, R><<<nbp, 256, 0, st()>>>(P.p, cap, n, mat.p, box, mats, uu, partA.p);
+        KC(); k_energy<D, R><<<nbp, 256, 0, st()>>>(P.p, cap, n, mat.p, box, mats, uu, partA.p);
         OSMPM_LAUNCH_CHECK();
         if (pf.on) pf.end("energy", st());
         const int nbn = nblk(nn, 256);
-        k_energy_nodes<D><<<nbn, 256, 0, st()>>>(nn, m.p, vn.p, uu, dt, grav[0], grav[1], grav[2], partB.p);
+        KC(); k_energy_nodes<D><<<nbn, 256, 0, st()>>>(nn, m.p, vn.p, uu, dt, grav[0], grav[1], grav[2], partB.p);
         OSMPM_LAUNCH_CHECK();
-        k_final_sum<3><<<1, 1024, 0, st()>>>(partA.p, nbp, scal.p + 6);
-        k_final_sum<2><<<1, 1024, 0, st()>>>(partB.p, nbn, scal.p + 9);
+        // scal[8..10] particles {E, E_abs, inverted}; scal[11..12] nodes {E, E_abs}
+        KC(); k_final_sum<3><<<1, 1024, 0, st()>>>(partA.p, nbp, scal.p + 8);
+        KC(); k_final_sum<2><<<1, 1024, 0, st()>>>(partB.p, nbn, scal.p + 11);
         OSMPM_LAUNCH_CHECK();
         return OSMPM_OK;
     }
@@ -644,29 +644,33 @@ struct Sub : public osmpm_subdomain {
         std::memset(sts, 0, sizeof(*sts));
         const size_t nn = box.nnodes, ndof = nn * D;
         OSMPM_TRY(build_dirichlet());
-        k_newton_init<D><<<nblk_all(nn, 256), 256, 0, st()>>>(nn, act.p, dmask.p, dval.p, vn.p, dt, s->guess, fmask.p,
+        KC(); k_newton_init<D><<<nblk_all(nn, 256), 256, 0, st()>>>(nn, act.p, dmask.p, dval.p, vn.p, dt, s->guess, fmask.p,
                                                                u.p);
         OSMPM_LAUNCH_CHECK();
         const double idt2 = 1.0 / (dt * dt);
-        double g0 = 0.0;
+        double g0 = 0.0, gref = 0.0;
         bool converged = false;
         osmpm_status rc = OSMPM_OK;
         const int nbd = nblk(ndof, 256), nbn = nblk(nn, 256);
         const int chunk = s->fixed_iters ? s->max_cg : 8;
         for (int it = 0; it < s->max_newton; ++it) {
             OSMPM_TRY(grad_eval(u.p, true));
-            OSMPM_TRY(read_scal(6));
+            OSMPM_TRY(read_scal(7));
             const double gn = std::sqrt(h_scal[5]);
             const double E0 = h_scal[0] + h_scal[3], Ea0 = h_scal[1] + h_scal[4];
-            if (it == 0) g0 = gn;
+            if (it == 0) {
+                // Newton test relative to max(|g^(0)|, force scale) (R6)
+                g0 = gn;
+                gref = std::max(g0, std::sqrt(h_scal[6]));
+            }
             sts->grad_norm = gn;
-            if (!s->fixed_iters && (gn <= s->newton_rtol * g0 || gn <= s->newton_atol)) {
+            if (!s->fixed_iters && (gn <= s->newton_rtol * gref || gn <= s->newton_atol)) {
                 converged = true;
                 break;
             }
             // Jacobi PCG on H dx = -g (R6, R7)
-            k_cg_init<D><<<nbd, 256, 0, st()>>>(ndof, fmask.p, g.p, dg.p, r.p, z.p, p.p, xs.p, y.p, partB.p);
-            k_cg_init_fin<<<1, 1024, 0, st()>>>(partB.p, nbd, cgs.p, gn, s->cg_rtol, s->fixed_iters);
+            KC(); k_cg_init<D><<<nbd, 256, 0, st()>>>(ndof, fmask.p, g.p, dg.p, r.p, z.p, p.p, xs.p, y.p, partB.p);
+            KC(); k_cg_init_fin<<<1, 1024, 0, st()>>>(partB.p, nbd, cgs.p, gn, s->cg_rtol, s->fixed_iters);
             OSMPM_LAUNCH_CHECK();
             int done_it = 0;
             while (done_it < s->max_cg) {
@@ -674,11 +678,11 @@ struct Sub : public osmpm_subdomain {
                 for (int c = 0; c < cnt; ++c) {
                     OSMPM_TRY(launch_hvp(p.p, y.p));
                     if (ctx->prof.on) ctx->prof.begin("cg", st());
-                    k_cg_q<D><<<nbn, 256, 0, st()>>>(nn, fmask.p, m.p, idt2, p.p, y.p, cgs.p, partB.p);
-                    k_cg_alpha<<<1, 1024, 0, st()>>>(partB.p, nbn, cgs.p);
-                    k_cg_update<<<nbd, 256, 0, st()>>>(ndof, fmask.p, p.p, y.p, dg.p, xs.p, r.p, z.p, cgs.p, partB.p);
-                    k_cg_beta<<<1, 1024, 0, st()>>>(partB.p, nbd, cgs.p);
-                    k_cg_p<<<nbd, 256, 0, st()>>>(ndof, z.p, p.p, y.p, cgs.p);
+                    KC(); k_cg_q<D><<<nbn, 256, 0, st()>>>(nn, fmask.p, m.p, idt2, p.p, y.p, cgs.p, partB.p);
+                    KC(); k_cg_alpha<<<1, 1024, 0, st()>>>(partB.p, nbn, cgs.p);
+                    KC(); k_cg_update<<<nbd, 256, 0, st()>>>(ndof, fmask.p, p.p, y.p, dg.p, xs.p, r.p, z.p, cgs.p, partB.p);
+                    KC(); k_cg_beta<<<1, 1024, 0, st()>>>(partB.p, nbd, cgs.p);
+                    KC(); k_cg_p<<<nbd, 256, 0, st()>>>(ndof, z.p, p.p, y.p, cgs.p);
                     if (ctx->prof.on) ctx->prof.end("cg", st());
                     OSMPM_LAUNCH_CHECK();
                 }
@@ -696,12 +700,12 @@ struct Sub : public osmpm_subdomain {
             // backtracking line search (R8)
             double alpha = 1.0, Et = 0.0;
             for (;;) {
-                k_axpy_free<<<nbd, 256, 0, st()>>>(ndof, fmask.p, u.p, alpha, xs.p, ut.p);
+                KC(); k_axpy_free<<<nbd, 256, 0, st()>>>(ndof, fmask.p, u.p, alpha, xs.p, ut.p);
                 OSMPM_LAUNCH_CHECK();
                 OSMPM_TRY(energy_eval(ut.p));
-                OSMPM_TRY(read_scal(11));
-                const bool inv = h_scal[8] > 0;
-                Et = inv ? INFINITY : h_scal[6] + h_scal[9];
+                OSMPM_TRY(read_scal(13));
+                const bool inv = h_scal[10] > 0;
+                Et = inv ? INFINITY : h_scal[8] + h_scal[11];
                 if (Et < E0 || (std::isfinite(Et) && std::fabs(Et - E0) <= s->energy_noise_rtol * Ea0)) break;
                 alpha *= 0.5;
                 sts->ls_halvings++;
@@ -722,14 +726,14 @@ struct Sub : public osmpm_subdomain {
             OSMPM_TRY(read_scal(6));
             const double gn = std::sqrt(h_scal[5]);
             sts->grad_norm = gn;
-            if (!(gn <= s->newton_rtol * g0 || gn <= s->newton_atol)) {
+            if (!(gn <= s->newton_rtol * gref || gn <= s->newton_atol)) {
                 set_error("Newton did not converge in %d iterations (|g| = %g, |g0| = %g)", s->max_newton, gn, g0);
                 rc = OSMPM_E_NEWTON_NOT_CONVERGED;
             }
         }
         sts->grad_norm0 = g0;
         sts->status = rc;
-        k_vnew<D><<<nblk_all(nn, 256), 256, 0, st()>>>(nn, act.p, u.p, 1.0 / dt, vnew.p);
+        KC(); k_vnew<D><<<nblk_all(nn, 256), 256, 0, st()>>>(nn, act.p, u.p, 1.0 / dt, vnew.p);
         OSMPM_LAUNCH_CHECK();
         have_vnew = true;
         have_lin = false;  // the cache now refers to an intermediate point
@@ -766,7 +770,7 @@ struct Sub : public osmpm_subdomain {
         auto& pf = ctx->prof;
         if (pf.on) pf.begin("g2p", st());
         if (n > 0) {
-            k_g2p<D, R><<<nblk_all(n, 128), 128, 0, st()>>>(P.p, cap, n, pid.p, box, vnew.p, dt, err.p);
+            KC(); k_g2p<D, R><<<nblk_all(n, 128), 128, 0, st()>>>(P.p, cap, n, pid.p, box, vnew.p, dt, err.p);
             OSMPM_LAUNCH_CHECK();
         }
         if (pf.on) pf.end("g2p", st());
@@ -787,14 +791,15 @@ struct Sub : public osmpm_subdomain {
             if (!fl.dst || n == 0) continue;
             const size_t cnt = (size_t)n * fl.nc;
             double* d = fl.dst;
-            DBuf<double> stage;
+            DBuf<double>& stage = stage_io;
             if (sp == OSMPM_HOST) {
                 OSMPM_TRY(stage.need(cnt));
                 d = stage.p;
             }
-            for (int c = 0; c < fl.nc; ++c)
-                k_unsort_field<R><<<nblk_all(n, 256), 256, 0, st()>>>(P.p + (size_t)(fl.off + c) * cap, n, pid.p,
+            for (int c = 0; c < fl.nc; ++c) {
+                KC(); k_unsort_field<R><<<nblk_all(n, 256), 256, 0, st()>>>(P.p + (size_t)(fl.off + c) * cap, n, pid.p,
                                                                       fl.nc, c, d);
+            }
             OSMPM_LAUNCH_CHECK();
             if (sp == OSMPM_HOST) {
                 OSMPM_CU(cudaMemcpyAsync(fl.dst, d, cnt * sizeof(double), cudaMemcpyDeviceToHost, st()));
@@ -813,15 +818,16 @@ struct Sub : public osmpm_subdomain {
             if (!fl.src || n == 0) continue;
             const size_t cnt = (size_t)n * fl.nc;
             const double* s = fl.src;
-            DBuf<double> stage;
+            DBuf<double>& stage = stage_io;
             if (sp == OSMPM_HOST) {
                 OSMPM_TRY(stage.need(cnt));
                 OSMPM_CU(cudaMemcpyAsync(stage.p, fl.src, cnt * sizeof(double), cudaMemcpyHostToDevice, st()));
                 s = stage.p;
             }
-            for (int c = 0; c < fl.nc; ++c)
-                k_sort_field<R><<<nblk_all(n, 256), 256, 0, st()>>>(s, n, pid.p, fl.nc, c,
+            for (int c = 0; c < fl.nc; ++c) {
+                KC(); k_sort_field<R><<<nblk_all(n, 256), 256, 0, st()>>>(s, n, pid.p, fl.nc, c,
                                                                     P.p + (size_t)(fl.off + c) * cap);
+            }
             OSMPM_LAUNCH_CHECK();
             if (sp == OSMPM_HOST) OSMPM_CU(cudaStreamSynchronize(st()));
         }

@@ -148,6 +148,7 @@ osmpm_status project_accumulate(Sub<D, R>* fine, Sub<D, R>* coarse, bool use_sol
     OSMPM_CU(cudaMemsetAsync(den.p, 0, nnb * sizeof(double), st));
     const double* v = use_solved ? fine->vnew.p : fine->vn.p;
     if (fine->ctx->prof.on) fine->ctx->prof.begin("transmit", st);
+    fine->KC();
     k_project<D><<<nblk_all(fine->box.nnodes, 256), 256, 0, st>>>(fine->box, fine->act.p, fine->m.p, v, geo_of(coarse),
                                                                   num.p, den.p);
     OSMPM_LAUNCH_CHECK();
@@ -199,12 +200,14 @@ osmpm_status transmit_impl(Sub<D, R>* src, Sub<D, R>* dst, osmpm_direction dir, 
         DBuf<double> num, den;
         OSMPM_TRY(project_accumulate(src, dst, alpha == 1.0, num, den));
         if (nt > 0) {
+            src->KC();
             k_project_out<D><<<nblk_all(nt, 256), 256, 0, st>>>(nt, tptr, num.p, den.p, eps, optr);
             OSMPM_LAUNCH_CHECK();
         }
     } else {
         if (nt > 0) {
             if (src->ctx->prof.on) src->ctx->prof.begin("transmit", st);
+            src->KC();
             k_interp<D><<<nblk_all(nt, 256), 256, 0, st>>>(nt, tptr, geo_of(dst), src->box, src->vn.p,
                                                            need_solved ? src->vnew.p : nullptr, alpha, optr);
             OSMPM_LAUNCH_CHECK();

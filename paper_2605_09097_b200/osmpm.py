@@ -165,6 +165,11 @@ class Context:
         _check(lib().osmpm_kernel_time(self._h, family.encode(), C.byref(n), C.byref(ms)))
         return n.value, ms.value
 
+    def launch_count(self):
+        n = C.c_int64()
+        _check(lib().osmpm_launch_count(self._h, C.byref(n)))
+        return n.value
+
     def close(self):
         if self._h:
             lib().osmpm_ctx_destroy(self._h)
@@ -241,6 +246,11 @@ class Subdomain:
         _check(lib().osmpm_set_dirichlet(self._h, C.c_int64(node_idx.shape[0]), _ptr(node_idx, np.int64)[0],
                                          _ptr(comp_mask, np.uint8)[0], _ptr(vel)[0], C.c_int(HOST)))
 
+    def set_dirichlet_device(self, node_idx, comp_mask, vel):
+        """Dirichlet list from torch CUDA tensors (int64, uint8, float64 (n, d))."""
+        _check(lib().osmpm_set_dirichlet(self._h, C.c_int64(int(node_idx.shape[0])), _ptr(node_idx, np.int64)[0],
+                                         _ptr(comp_mask, np.uint8)[0], _ptr(vel)[0], C.c_int(DEVICE)))
+
     # --- hot path ------------------------------------------------------------------------------
     def p2g(self):
         _check(lib().osmpm_p2g(self._h))
@@ -305,6 +315,11 @@ class Subdomain:
         ps = [(_ptr(out[k])[0] if k in out else None) for k in ("x", "v", "F", "B")]
         _check(lib().osmpm_read_particles(self._h, *ps, C.c_int(HOST if device is None else DEVICE)))
         return out
+
+    def read_particles_into(self, x=None, v=None, F=None, B=None):
+        """Creation-order particle fields into caller buffers (numpy / pinned or CUDA torch tensors)."""
+        ps = [_ptr(a)[0] if a is not None else None for a in (x, v, F, B)]
+        _check(lib().osmpm_read_particles(self._h, *ps, C.c_int(_space(x, v, F, B))))
 
     def info(self):
         n = C.c_int64()

@@ -1,0 +1,86 @@
+"""Pins of the oracle's Schwarz frame (O11-O12): arbitration rules, exact reproduction of uniform
+translation for any M and resolution ratio, contraction of the interface residuals, parity mode
+(PAPER.md:294-301, 436-501)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import schwarz as S
+
+
+def _translating_pair(dim, c, M=4):
+    coarse, fine = synth.c1_cantilever(g=0.0) if dim == 2 else (None, None)
+    for sc in (coarse, fine):
+        sc.particles.v[:] = c
+        sc.gravity = (0.0, 0.0, 0.0)
+    fine.dt = coarse.dt / M
+    return coarse, fine
+
+
+def test_receivers_disjoint_and_tie_to_B():
+    coarse, fine = synth.c1_cantilever()
+    gsB = oracle.p2g(coarse)
+    gsS = oracle.p2g(fine)
+    hatB, hatS = S.receivers(coarse, fine, gsB, gsS, 1e-6)
+    assert hatB.sum() > 0 and hatS.sum() > 0
+    # every receiver is an active node of its own grid
+    assert np.all(gsB.active[hatB]) and np.all(gsS.active[hatS])
+    # coincident nodes are never receivers on both sides
+    xs, _ = S.node_positions(fine.grid)
+    cidx = S.coincident_coarse_index(coarse.grid, xs, 1e-9 * fine.grid.dx)
+    both = hatS & (cidx >= 0)
+    assert not np.any(hatB[cidx[both]])
+
+
+def test_arbitration_tie_goes_to_background():
+    # hand case: one coincident boundary node with equal masses on both grids -> B donates, S receives
+    coarse, fine = synth.c1_cantilever()
+    gsB = oracle.p2g(coarse)
+    gsS = oracle.p2g(fine)
+    gB, _ = S.gamma_set(coarse, gsB, 1e-6)
+    gS, _ = S.gamma_set(fine, gsS, 1e-6)
+    xs, _ = S.node_positions(fine.grid)
+    cidx = S.coincident_coarse_index(coarse.grid, xs, 1e-9 * fine.grid.dx)
+    amb = np.flatnonzero(gS & (cidx >= 0) & gB[np.maximum(cidx, 0)])
+    assert amb.size > 0
+    j = amb[0]
+    I = cidx[j]
+    gsS.m[j] = gsB.m[I]          # force a tie
+    hatB, hatS = S.receivers(coarse, fine, gsB, gsS, 1e-6)
+    assert not hatB[I]
+    gsS.m[j] = 2.0 * gsB.m[I]    # S heavier -> S donates, B receives (if eligible)
+    hatB2, hatS2 = S.receivers(coarse, fine, gsB, gsS, 1e-6)
+    assert not hatS2[j]
+
+
+@pytest.mark.parametrize("M", [1, 4])
+def test_uniform_translation_is_reproduced_exactly(M):
+    c = np.array([0.3, -0.2])
+    coarse, fine = _translating_pair(2, c, M)
+    x0c = coarse.particles.x.copy()
+    x0f = fine.particles.x.copy()
+    res = S.schwarz_step(coarse, fine, M, parity_fixed_k=2)
+    # exact up to the solver tolerance (Newton / PCG at 1e-12 relative)
+    for pt, x0 in ((res.coarse_particles, x0c), (res.fine_particles, x0f)):
+        np.testing.assert_allclose(pt.v, np.tile(c, (pt.n, 1)), rtol=0, atol=1e-10)
+        np.testing.assert_allclose(pt.x, x0 + coarse.dt * c, rtol=0, atol=1e-12)
+        np.testing.assert_allclose(pt.F, np.broadcast_to(np.eye(2), pt.F.shape), rtol=0, atol=1e-10)
+    assert res.r_B[-1] < 1e-10 and res.r_S[-1] < 1e-10
+
+
+def test_cantilever_frame_converges_with_contracting_residuals():
+    coarse, fine = synth.c1_cantilever()
+    # clamp: fine nodes with x <= 0 fixed in all components (R17)
+    gsS = oracle.p2g(fine)
+    xs, _ = S.node_positions(fine.grid)
+    mask = np.repeat((xs[:, 0] <= 1e-12)[:, None], 2, axis=1).astype(np.uint8)
+    user_S = S.UserBC(mask, np.zeros_like(xs))
+    res = S.schwarz_step(coarse, fine, 4, eps_conv=1e-5, k_max=30, user_S=user_S)
+    assert res.converged
+    assert res.iters >= 2
+    # the interface residuals contract (geometric convergence of the alternating method)
+    rB = np.array(res.r_B)
+    assert rB[-1] < rB[0]
+    # the beam sags (gravity) and the clamp holds
+    assert res.fine_particles.x[:, 1].mean() < fine.particles.x[:, 1].mean()
