@@ -1,30 +1,385 @@
-// coupler.cuh -- multiplicative Schwarz coupling of a coarse and a fine subdomain (§3.3-3.5,
-// Alg. 1).  Placeholder entry points; the driver is implemented in coupler_impl (next milestone).
+// coupler.cuh -- multiplicative Schwarz coupling of a coarse (B) and a fine (S) subdomain
+// (§3.2-3.5, Alg. 1 at PAPER.md:436-481).  The hot operators run on the GPU (P2G, implicit
+// solves, G2P, Pi, I, T); the once-per-frame receiver-set construction (boundary grid selection,
+// overlap arbitration, eligibility) is host logic over node flags read back from the device.
+// Readings of the paper: DESIGN.md R10-R16.
 #pragma once
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
 #include "transmit.cuh"
+
+struct osmpm_coupler {
+    osmpm_subdomain* coarse = nullptr;
+    osmpm_subdomain* fine = nullptr;
+    osmpm_schwarz_settings set{};
+    virtual ~osmpm_coupler() {}
+    virtual osmpm_status prepare() = 0;
+    virtual osmpm_status substep(int m, osmpm_solve_stats* st) = 0;
+    virtual osmpm_status step(osmpm_schwarz_report* rep) = 0;
+};
 
 namespace osmpm {
 
-inline osmpm_status coupler_create(osmpm_subdomain*, osmpm_subdomain*, const osmpm_schwarz_settings*, osmpm_coupler**)
+// v = (1 - alpha) a + alpha b  (T_m, Eq. temporal_interp)
+__global__ void k_lerp(int64_t n, const double* __restrict__ a, const double* __restrict__ b, double alpha,
+                       double* __restrict__ out)
 {
-    set_error("Schwarz coupler not built yet");
-    return OSMPM_E_STATE;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (1.0 - alpha) * a[i] + alpha * b[i];
 }
-inline void coupler_destroy(osmpm_coupler*) {}
-inline osmpm_status coupler_prepare(osmpm_coupler*)
+
+template <int D, typename R>
+struct Coupler : public osmpm_coupler {
+    Sub<D, R>* B = nullptr;
+    Sub<D, R>* S = nullptr;
+    std::vector<int64_t> recvB, recvS;           // receivers (dense node indices, ascending)
+    DBuf<int64_t> dB, dS;
+    DBuf<uint8_t> maskB, maskS;
+    DBuf<double> vGB, vGBnew, vSn, vSnp1, vSprev, vbc, num, den;
+    bool prepared = false;
+    double eps_tol = 0.0;
+    cudaStream_t st() const { return B->st(); }
+
+    // ------------------------------------------------------------------------------------------
+    // host helpers
+    // ------------------------------------------------------------------------------------------
+    template <typename T>
+    static osmpm_status d2h(std::vector<T>& h, const T* d, size_t n, cudaStream_t s)
+    {
+        h.resize(n);
+        if (n) OSMPM_CU(cudaMemcpyAsync(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+        return OSMPM_OK;
+    }
+
+    // box-local index of a dense node index (or -1 outside the box)
+    static int64_t box_of(const Sub<D, R>* s, int64_t g)
+    {
+        const BoxDev& b = s->box;
+        int64_t k[3] = {0, 0, 0};
+        if (D == 3) {
+            k[2] = g % s->gdims[2];
+            k[1] = (g / s->gdims[2]) % s->gdims[1];
+            k[0] = g / (s->gdims[2] * s->gdims[1]);
+        } else {
+            k[1] = g % s->gdims[1];
+            k[0] = g / s->gdims[1];
+        }
+        int64_t l[3];
+        for (int a = 0; a < 3; ++a) {
+            l[a] = (a < D) ? k[a] - b.lo[a] : 0;
+            if (a < D && (l[a] < 0 || l[a] >= b.nn[a])) return -1;
+        }
+        return (D == 3) ? (l[0] * b.nn[1] + l[1]) * b.nn[2] + l[2] : l[0] * b.nn[1] + l[1];
+    }
+
+    static int64_t dense_of_box(const Sub<D, R>* s, int64_t i, int64_t* k)
+    {
+        const BoxDev& b = s->box;
+        int64_t l[3] = {0, 0, 0};
+        if (D == 3) {
+            l[2] = i % b.nn[2];
+            l[1] = (i / b.nn[2]) % b.nn[1];
+            l[0] = i / ((int64_t)b.nn[2] * b.nn[1]);
+        } else {
+            l[1] = i % b.nn[1];
+            l[0] = i / b.nn[1];
+        }
+        for (int a = 0; a < 3; ++a) k[a] = (a < D) ? b.lo[a] + l[a] : 0;
+        for (int a = 0; a < D; ++a)
+            if (k[a] >= s->gdims[a]) return -1;
+        return (D == 3) ? (k[0] * s->gdims[1] + k[1]) * s->gdims[2] + k[2] : k[0] * s->gdims[1] + k[1];
+    }
+
+    static double bsw(double f, int o)
+    {
+        if (o == 0) return 0.5 * (1.5 - f) * (1.5 - f);
+        if (o == 1) return 0.75 - (f - 1.0) * (f - 1.0);
+        return 0.5 * (f - 0.5) * (f - 0.5);
+    }
+
+    // ------------------------------------------------------------------------------------------
+    // Step 0: store, P2G both, Gamma, arbitration, receivers, v_GammaB^(0)
+    // ------------------------------------------------------------------------------------------
+    osmpm_status prepare() override
+    {
+        OSMPM_TRY(S->checkpoint());
+        OSMPM_TRY(B->p2g());
+        OSMPM_TRY(S->p2g());
+        OSMPM_TRY(B->boundary_mass());
+        OSMPM_TRY(S->boundary_mass());
+        // Pi denominator of the step-0 fine grid (eligibility of coarse receivers, R13)
+        OSMPM_TRY(project_accumulate(S, B, false, num, den));
+        std::vector<double> mB, mbB, mS, mbS, denB;
+        std::vector<uint8_t> aB, aS;
+        OSMPM_TRY(d2h(mB, B->m.p, B->box.nnodes, st()));
+        OSMPM_TRY(d2h(mbB, B->mb.p, B->box.nnodes, st()));
+        OSMPM_TRY(d2h(aB, B->act.p, B->box.nnodes, st()));
+        OSMPM_TRY(d2h(mS, S->m.p, S->box.nnodes, st()));
+        OSMPM_TRY(d2h(mbS, S->mb.p, S->box.nnodes, st()));
+        OSMPM_TRY(d2h(aS, S->act.p, S->box.nnodes, st()));
+        OSMPM_TRY(d2h(denB, den.p, B->dense_nodes(), st()));
+        OSMPM_CU(cudaStreamSynchronize(st()));
+        const double tauB = set.tau_gamma_rel * B->median_mass, tauS = set.tau_gamma_rel * S->median_mass;
+        // Gamma_alpha = {active i : m^b_i > tau} (Eq. boundary_grid_set), as dense index -> box index
+        std::vector<char> hatB(B->box.nnodes, 0);
+        for (int64_t i = 0; i < B->box.nnodes; ++i) hatB[i] = aB[i] && mbB[i] > tauB;
+        std::vector<int64_t> gS;  // fine Gamma (box indices)
+        for (int64_t i = 0; i < S->box.nnodes; ++i)
+            if (aS[i] && mbS[i] > tauS) gS.push_back(i);
+        std::vector<char> hatS_keep(gS.size(), 1);
+        const double tol = 1e-9 * std::min(B->dx, S->dx);
+        for (size_t q = 0; q < gS.size(); ++q) {
+            int64_t k[3];
+            if (dense_of_box(S, gS[q], k) < 0) continue;
+            int64_t kk[3] = {0, 0, 0};
+            bool coincide = true;
+            for (int a = 0; a < D; ++a) {
+                const double x = S->origin[a] + S->dx * (double)k[a];
+                const double X = (x - B->origin[a]) / B->dx;
+                kk[a] = (int64_t)std::llround(X);
+                if (std::fabs(X - (double)kk[a]) * B->dx > tol || kk[a] < 0 || kk[a] >= B->gdims[a]) coincide = false;
+            }
+            if (!coincide) continue;
+            const int64_t gI = (D == 3) ? (kk[0] * B->gdims[1] + kk[1]) * B->gdims[2] + kk[2] : kk[0] * B->gdims[1] + kk[1];
+            const int64_t I = box_of(B, gI);
+            if (I < 0 || !hatB[I]) continue;
+            // ambiguous overlap node (Eq. overlap_donor): donor = larger nodal mass, ties -> B
+            if (mB[I] >= mS[gS[q]])
+                hatB[I] = 0;       // B donates: S receives
+            else
+                hatS_keep[q] = 0;  // S donates: B receives
+        }
+        // coarse receivers need fine support (R13)
+        recvB.clear();
+        for (int64_t i = 0; i < B->box.nnodes; ++i) {
+            if (!hatB[i]) continue;
+            int64_t k[3];
+            const int64_t g = dense_of_box(B, i, k);
+            if (g >= 0 && denB[g] > tauB) recvB.push_back(g);
+        }
+        std::sort(recvB.begin(), recvB.end());
+        // fine receivers need an active coarse stencil (R13)
+        recvS.clear();
+        for (size_t q = 0; q < gS.size(); ++q) {
+            if (!hatS_keep[q]) continue;
+            int64_t k[3];
+            const int64_t g = dense_of_box(S, gS[q], k);
+            if (g < 0) continue;
+            double f[3];
+            int64_t base[3] = {0, 0, 0};
+            for (int a = 0; a < D; ++a) {
+                const double x = S->origin[a] + S->dx * (double)k[a];
+                const double X = (x - B->origin[a]) / B->dx;
+                base[a] = (int64_t)std::floor(X - 0.5);
+                f[a] = X - (double)base[a];
+            }
+            bool ok = true;
+            for (int o0 = 0; o0 < 3 && ok; ++o0)
+                for (int o1 = 0; o1 < 3 && ok; ++o1)
+                    for (int o2 = 0; o2 < (D == 3 ? 3 : 1) && ok; ++o2) {
+                        const int off[3] = {o0, o1, o2};
+                        double w = 1.0;
+                        for (int a = 0; a < D; ++a) w *= bsw(f[a], off[a]);
+                        if (!(w > 0.0)) continue;
+                        int64_t kk[3] = {0, 0, 0};
+                        for (int a = 0; a < D; ++a) {
+                            kk[a] = base[a] + off[a];
+                            if (kk[a] < 0 || kk[a] >= B->gdims[a]) ok = false;
+                        }
+                        if (!ok) break;
+                        const int64_t gI =
+                            (D == 3) ? (kk[0] * B->gdims[1] + kk[1]) * B->gdims[2] + kk[2] : kk[0] * B->gdims[1] + kk[1];
+                        const int64_t I = box_of(B, gI);
+                        if (I < 0 || !aB[I]) ok = false;
+                    }
+            if (ok) recvS.push_back(g);
+        }
+        std::sort(recvS.begin(), recvS.end());
+        const int64_t nB = recvB.size(), nS = recvS.size();
+        OSMPM_TRY(dB.need(std::max<int64_t>(nB, 1)));
+        OSMPM_TRY(dS.need(std::max<int64_t>(nS, 1)));
+        OSMPM_TRY(maskB.need(std::max<int64_t>(nB, 1)));
+        OSMPM_TRY(maskS.need(std::max<int64_t>(nS, 1)));
+        for (DBuf<double>* bb : {&vGB, &vGBnew})
+            OSMPM_TRY(bb->need(std::max<int64_t>(nB, 1) * D));
+        for (DBuf<double>* bb : {&vSn, &vSnp1, &vSprev, &vbc})
+            OSMPM_TRY(bb->need(std::max<int64_t>(nS, 1) * D));
+        if (nB) OSMPM_CU(cudaMemcpyAsync(dB.p, recvB.data(), nB * sizeof(int64_t), cudaMemcpyHostToDevice, st()));
+        if (nS) OSMPM_CU(cudaMemcpyAsync(dS.p, recvS.data(), nS * sizeof(int64_t), cudaMemcpyHostToDevice, st()));
+        OSMPM_CU(cudaMemsetAsync(maskB.p, (1 << D) - 1, std::max<int64_t>(nB, 1), st()));
+        OSMPM_CU(cudaMemsetAsync(maskS.p, (1 << D) - 1, std::max<int64_t>(nS, 1), st()));
+        // v_GammaB^(0) = Pi(v_S^n) on the coarse receivers (R16)
+        eps_tol = set.eps_tol >= 0 ? set.eps_tol : 1e-12 * S->total_mass;
+        if (nB) {
+            B->KC();
+            k_project_out<D><<<nblk_all(nB, 256), 256, 0, st()>>>(nB, dB.p, num.p, den.p, eps_tol, vGB.p);
+            OSMPM_LAUNCH_CHECK();
+        }
+        // v_GammaS^(0) = I(v_B^n) (R15: r_S at k = 0 compares I(v_B^(1)) with I(v_B^n))
+        if (nS) {
+            B->KC();
+            k_interp<D><<<nblk_all(nS, 256), 256, 0, st()>>>(nS, dS.p, geo_of(S), B->box, B->vn.p, nullptr, 0.0,
+                                                             vSprev.p);
+            OSMPM_LAUNCH_CHECK();
+        }
+        // the coarse subdomain's Schwarz Dirichlet data for the first coarse solve
+        OSMPM_TRY(B->set_dirlist(B->dir_cpl, nB, dB.p, maskB.p, vGB.p, OSMPM_DEVICE));
+        OSMPM_CU(cudaStreamSynchronize(st()));
+        prepared = true;
+        return OSMPM_OK;
+    }
+
+    // endpoint interpolations for the current coarse solve (Eq. spatial_interp_n)
+    osmpm_status endpoints()
+    {
+        const int64_t nS = recvS.size();
+        if (!nS) return OSMPM_OK;
+        B->KC();
+        k_interp<D><<<nblk_all(nS, 256), 256, 0, st()>>>(nS, dS.p, geo_of(S), B->box, B->vn.p, nullptr, 0.0, vSn.p);
+        B->KC();
+        k_interp<D><<<nblk_all(nS, 256), 256, 0, st()>>>(nS, dS.p, geo_of(S), B->box, B->vnew.p, nullptr, 0.0,
+                                                         vSnp1.p);
+        OSMPM_LAUNCH_CHECK();
+        return OSMPM_OK;
+    }
+
+    // one fine sub-step m of Alg. 1 lines 459-463 (+ P2G of the current state first, R14)
+    osmpm_status substep(int m, osmpm_solve_stats* stats) override
+    {
+        if (!prepared) {
+            set_error("schwarz_substep before schwarz_prepare");
+            return OSMPM_E_STATE;
+        }
+        if (m < 1 || m > set.M) {
+            set_error("sub-step m = %d outside [1, M = %d] (SPEC.md:330)", m, set.M);
+            return OSMPM_E_INVALID_ARG;
+        }
+        if (m == 1) {
+            if (!B->have_vnew) {
+                set_error("schwarz_substep(1) needs the coarse subdomain's solve of this iteration");
+                return OSMPM_E_STATE;
+            }
+            OSMPM_TRY(endpoints());
+        }
+        if (!S->have_grid) OSMPM_TRY(S->p2g());
+        const int64_t nS = recvS.size();
+        const double alpha = (double)m / (double)set.M;  // Eq. temporal_interp
+        if (nS) {
+            B->KC();
+            k_lerp<<<nblk_all(nS * D, 256), 256, 0, st()>>>(nS * D, vSn.p, vSnp1.p, alpha, vbc.p);
+            OSMPM_LAUNCH_CHECK();
+        }
+        OSMPM_TRY(S->set_dirlist(S->dir_cpl, nS, dS.p, maskS.p, vbc.p, OSMPM_DEVICE));
+        OSMPM_TRY(S->implicit_solve(&set.fine, stats));
+        if (m == set.M) {
+            // v_GammaB^(k+1) = Pi(last sub-step's solved fine velocities) (R16)
+            OSMPM_TRY(project_accumulate(S, B, true, num, den));
+            const int64_t nB = recvB.size();
+            if (nB) {
+                B->KC();
+                k_project_out<D><<<nblk_all(nB, 256), 256, 0, st()>>>(nB, dB.p, num.p, den.p, eps_tol, vGBnew.p);
+                OSMPM_LAUNCH_CHECK();
+            }
+        }
+        return S->g2p();
+    }
+
+    static double rel_change(const std::vector<double>& nw, const std::vector<double>& old)
+    {
+        double a = 0.0, b = 0.0;
+        for (size_t i = 0; i < nw.size(); ++i) {
+            a += (nw[i] - old[i]) * (nw[i] - old[i]);
+            b += nw[i] * nw[i];
+        }
+        return b > 0.0 ? std::sqrt(a / b) : std::sqrt(a);
+    }
+
+    osmpm_status step(osmpm_schwarz_report* rep) override
+    {
+        osmpm_schwarz_report local{};
+        osmpm_schwarz_report* RP = rep ? rep : &local;
+        std::memset(RP, 0, sizeof(*RP));
+        OSMPM_TRY(prepare());
+        RP->n_recv_B = (int)recvB.size();
+        RP->n_recv_S = (int)recvS.size();
+        const int64_t nB = recvB.size(), nS = recvS.size();
+        const int n_iter = set.parity_fixed_k > 0 ? set.parity_fixed_k : set.k_max;
+        std::vector<double> hGB, hGBnew, hSnp1, hSprev;
+        for (int k = 0; k < n_iter; ++k) {
+            // Step 1: coarse solve with Dirichlet Gamma-hat_B <- v_GammaB^(k) (Eq. implicit_solve_coarse),
+            // restarting from the frozen step-0 coarse grid (R14)
+            OSMPM_TRY(B->set_dirlist(B->dir_cpl, nB, dB.p, maskB.p, vGB.p, OSMPM_DEVICE));
+            OSMPM_TRY(B->implicit_solve(&set.coarse, nullptr));
+            // Step 2: restore the fine particles (Alg. 1) and sub-cycle
+            OSMPM_TRY(S->restore());
+            OSMPM_TRY(S->p2g());
+            for (int m = 1; m <= set.M; ++m) {
+                OSMPM_TRY(substep(m, nullptr));
+                RP->fine_substeps++;
+            }
+            // Step 3: interface residuals (Eqs. convergence_residuals / criterion)
+            OSMPM_TRY(d2h(hGB, vGB.p, nB * D, st()));
+            OSMPM_TRY(d2h(hGBnew, vGBnew.p, nB * D, st()));
+            OSMPM_TRY(d2h(hSnp1, vSnp1.p, nS * D, st()));
+            OSMPM_TRY(d2h(hSprev, vSprev.p, nS * D, st()));
+            OSMPM_CU(cudaStreamSynchronize(st()));
+            const double rB = rel_change(hGBnew, hGB), rS = rel_change(hSnp1, hSprev);
+            if (k < 256) {
+                RP->r_B[k] = rB;
+                RP->r_S[k] = rS;
+            }
+            RP->iters = k + 1;
+            std::swap(vGB.p, vGBnew.p);
+            std::swap(vGB.cap, vGBnew.cap);
+            if (nS) OSMPM_CU(cudaMemcpyAsync(vSprev.p, vSnp1.p, nS * D * sizeof(double), cudaMemcpyDeviceToDevice, st()));
+            if (rB <= set.eps_conv && rS <= set.eps_conv) {
+                RP->converged = 1;
+                if (set.parity_fixed_k <= 0) break;
+            }
+        }
+        // Step 4: post-convergence coarse G2P + advection with v_B^(k*+1)
+        OSMPM_TRY(B->g2p());
+        OSMPM_TRY(B->sync());
+        OSMPM_TRY(S->sync());
+        B->dir_cpl.n = 0;
+        S->dir_cpl.n = 0;
+        prepared = false;
+        if (!RP->converged && set.parity_fixed_k <= 0) {
+            set_error("Schwarz iteration did not converge in k_max = %d iterations (r_B = %g, r_S = %g)", set.k_max,
+                      RP->r_B[std::min(RP->iters, 256) - 1], RP->r_S[std::min(RP->iters, 256) - 1]);
+            return OSMPM_E_SCHWARZ_NOT_CONVERGED;
+        }
+        return OSMPM_OK;
+    }
+};
+
+inline osmpm_status coupler_create(osmpm_subdomain* coarse, osmpm_subdomain* fine, const osmpm_schwarz_settings* s,
+                                   osmpm_coupler** out)
 {
-    set_error("Schwarz coupler not built yet");
-    return OSMPM_E_STATE;
+    osmpm_coupler* c = nullptr;
+#define MK(DD, RR)                                                                                  \
+    {                                                                                               \
+        auto* q = new Coupler<DD, RR>();                                                            \
+        q->B = static_cast<Sub<DD, RR>*>(coarse);                                                   \
+        q->S = static_cast<Sub<DD, RR>*>(fine);                                                     \
+        c = q;                                                                                      \
+    }
+    if (coarse->dim == 3 && coarse->prec == OSMPM_F64) MK(3, double)
+    else if (coarse->dim == 2 && coarse->prec == OSMPM_F64) MK(2, double)
+    else if (coarse->dim == 3) MK(3, float)
+    else MK(2, float)
+#undef MK
+    c->coarse = coarse;
+    c->fine = fine;
+    c->set = *s;
+    *out = c;
+    return OSMPM_OK;
 }
-inline osmpm_status coupler_substep(osmpm_coupler*, int32_t, osmpm_solve_stats*)
-{
-    set_error("Schwarz coupler not built yet");
-    return OSMPM_E_STATE;
-}
-inline osmpm_status coupler_step(osmpm_coupler*, osmpm_schwarz_report*)
-{
-    set_error("Schwarz coupler not built yet");
-    return OSMPM_E_STATE;
-}
+inline void coupler_destroy(osmpm_coupler* c) { delete c; }
+inline osmpm_status coupler_prepare(osmpm_coupler* c) { return c->prepare(); }
+inline osmpm_status coupler_substep(osmpm_coupler* c, int32_t m, osmpm_solve_stats* st) { return c->substep(m, st); }
+inline osmpm_status coupler_step(osmpm_coupler* c, osmpm_schwarz_report* r) { return c->step(r); }
 
 }  // namespace osmpm

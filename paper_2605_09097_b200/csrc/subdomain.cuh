@@ -204,6 +204,8 @@ struct Sub : public osmpm_subdomain {
             double med = (n % 2) ? ms[n / 2] : 0.5 * (ms[n / 2 - 1] + ms[n / 2]);
             mass_thr = 1e-12 * med;
             median_mass = med;
+            total_mass = 0.0;
+            for (double mm : ms) total_mass += mm;
         }
         OSMPM_CU(cudaMemcpy(P.p, h.data(), h.size() * sizeof(R), cudaMemcpyHostToDevice));
         OSMPM_CU(cudaMemcpy(mat.p, hm.data(), cap * sizeof(int), cudaMemcpyHostToDevice));
@@ -213,7 +215,7 @@ struct Sub : public osmpm_subdomain {
         OSMPM_TRY(compute_box());
         return check_err();
     }
-    double median_mass = 0;
+    double median_mass = 0, total_mass = 0;
 
     osmpm_status set_gravity(const double* gv) override
     {
@@ -649,6 +651,15 @@ struct Sub : public osmpm_subdomain {
         OSMPM_LAUNCH_CHECK();
         const double idt2 = 1.0 / (dt * dt);
         double g0 = 0.0, gref = 0.0;
+        // E(u) for the line search comes from the same energy kernel as the trial energies, so both
+        // sides of the comparison round alike (R8); later iterations reuse the accepted trial
+        double E0n = 0.0, Ea0n = 0.0;
+        if (s->max_newton > 0) {
+            OSMPM_TRY(energy_eval(u.p));
+            OSMPM_TRY(read_scal(13));
+            E0n = (h_scal[10] > 0) ? INFINITY : h_scal[8] + h_scal[11];
+            Ea0n = h_scal[9] + h_scal[12];
+        }
         bool converged = false;
         osmpm_status rc = OSMPM_OK;
         const int nbd = nblk(ndof, 256), nbn = nblk(nn, 256);
@@ -657,7 +668,7 @@ struct Sub : public osmpm_subdomain {
             OSMPM_TRY(grad_eval(u.p, true));
             OSMPM_TRY(read_scal(7));
             const double gn = std::sqrt(h_scal[5]);
-            const double E0 = h_scal[0] + h_scal[3], Ea0 = h_scal[1] + h_scal[4];
+            const double E0 = E0n, Ea0 = Ea0n;
             if (it == 0) {
                 // Newton test relative to max(|g^(0)|, force scale) (R6)
                 g0 = gn;
@@ -698,7 +709,7 @@ struct Sub : public osmpm_subdomain {
             sts->cg_iters += h_cgs->it + (h_cgs->done == 2 ? 1 : 0);
             if (h_cgs->negcurv_first) OSMPM_CU(cudaMemcpyAsync(xs.p, z.p, ndof * sizeof(double), cudaMemcpyDeviceToDevice, st()));
             // backtracking line search (R8)
-            double alpha = 1.0, Et = 0.0;
+            double alpha = 1.0, Et = 0.0, Eat = 0.0;
             for (;;) {
                 KC(); k_axpy_free<<<nbd, 256, 0, st()>>>(ndof, fmask.p, u.p, alpha, xs.p, ut.p);
                 OSMPM_LAUNCH_CHECK();
@@ -706,6 +717,7 @@ struct Sub : public osmpm_subdomain {
                 OSMPM_TRY(read_scal(13));
                 const bool inv = h_scal[10] > 0;
                 Et = inv ? INFINITY : h_scal[8] + h_scal[11];
+                Eat = h_scal[9] + h_scal[12];
                 if (Et < E0 || (std::isfinite(Et) && std::fabs(Et - E0) <= s->energy_noise_rtol * Ea0)) break;
                 alpha *= 0.5;
                 sts->ls_halvings++;
@@ -718,6 +730,8 @@ struct Sub : public osmpm_subdomain {
             if (rc != OSMPM_OK) break;
             std::swap(u.p, ut.p);
             std::swap(u.cap, ut.cap);
+            E0n = Et;
+            Ea0n = Eat;
             sts->energy = Et;
             sts->newton_iters = it + 1;
         }
