@@ -542,11 +542,45 @@ struct Sub : public osmpm_subdomain {
 
 
 
+    // HVP variant: warp-specialised persistent kernel (default) or the barrier-phased tiled kernel
+    // (OSMPM_HVP=tiled), kept for A/B measurements
+    int hvp_variant() const
+    {
+        static int v = -1;
+        if (v < 0) {
+            const char* e = getenv("OSMPM_HVP");
+            const std::string s = e ? e : "";
+            v = (s == "ws") ? 1 : (s == "tiled_nopf") ? 2 : 0;
+        }
+        return v;
+    }
+
     osmpm_status launch_hvp(const double* din, double* yout)
     {
         auto& pf = ctx->prof;
         if (pf.on) pf.begin("hvp", st());
-        KC(); k_hvp<D, R><<<box.ntiles, T::NT, hvp_smem(), st()>>>(P.p, cache.p, cap, cell_start.p, box, din, yout);
+        if (hvp_variant() == 1) {
+            using Lay = WSLayout<D, R>;
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_hvp_ws<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::BYTES);
+                attr = true;
+            }
+            const int grid = std::max(1, std::min(box.ntiles, ctx->num_sms));
+            KC(); k_hvp_ws<D, R><<<grid, WS<D>::NTHR, Lay::BYTES, st()>>>(P.p, cache.p, cap, cell_start.p, box, din,
+                                                                          yout);
+        } else if (hvp_variant() == 2) {
+            static bool attr2 = false;
+            if (!attr2) {
+                cudaFuncSetAttribute(k_hvp<D, R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)hvp_smem_bytes<D, R, false>());
+                attr2 = true;
+            }
+            KC(); k_hvp<D, R, false><<<box.ntiles, T::NT, hvp_smem_bytes<D, R, false>(), st()>>>(
+                P.p, cache.p, cap, cell_start.p, box, din, yout);
+        } else {
+            KC(); k_hvp<D, R><<<box.ntiles, T::NT, hvp_smem(), st()>>>(P.p, cache.p, cap, cell_start.p, box, din, yout);
+        }
         OSMPM_LAUNCH_CHECK();
         if (pf.on) pf.end("hvp", st());
         return OSMPM_OK;

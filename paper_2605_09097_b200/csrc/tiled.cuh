@@ -403,7 +403,7 @@ __device__ __forceinline__ void weights_at(const Rw* x, const BoxDev& b, const i
 // a5: HVP  y += sum_p V0 dP(F_p(u); gd F^n) F^nT grad N  =  sum_p G_p grad N with
 //     G = gd S' + c' Ah gd^T Ah + l' (Ah : gd) Ah   (derivation from PAPER.md:188, 208)
 // =============================================================================================
-template <int D> struct HvpOcc { static constexpr int MIN_BLOCKS = (D == 3) ? 3 : 4; };
+template <int D, bool PF> struct HvpOcc { static constexpr int MIN_BLOCKS = (D == 3) ? (PF ? 3 : 4) : 4; };
 
 // per-particle streamed inputs: x (D) and the Newton cache (CL<D>::NF fields)
 template <int D, typename R> struct HvpIn {
@@ -412,14 +412,14 @@ template <int D, typename R> struct HvpIn {
     static constexpr int PFS = Tile<D>::NT + 2 * UE;  // per-field capacity (alignment slack)
 };
 
-template <int D, typename R>
+template <int D, typename R, bool PF = true>
 constexpr size_t hvp_smem_bytes()
 {
     using T = Tile<D>;
     constexpr size_t rec = (size_t)HvpRec<D, R>::RS * T::NT;
     constexpr size_t recstg = rec > (size_t)Stage<D>::SIZE ? rec : (size_t)Stage<D>::SIZE;
-    return 16 + ((size_t)T::NN * SV<D>::S + T::NN * D + recstg + (size_t)HvpIn<D, R>::NF * HvpIn<D, R>::PFS) *
-                    sizeof(R);
+    return 16 + ((size_t)T::NN * SV<D>::S + T::NN * D + recstg +
+                 (PF ? (size_t)HvpIn<D, R>::NF * HvpIn<D, R>::PFS : 0)) * sizeof(R);
 }
 
 // issue the TMA bulk copies of the first min(NT, le - lb) particles of a layer
@@ -442,8 +442,8 @@ __device__ __forceinline__ int hvp_prefetch(const R* __restrict__ P, const R* __
     return lb0;
 }
 
-template <int D, typename R>
-__global__ void __launch_bounds__(Tile<D>::NT, HvpOcc<D>::MIN_BLOCKS)
+template <int D, typename R, bool PF = true>
+__global__ void __launch_bounds__(Tile<D>::NT, HvpOcc<D, PF>::MIN_BLOCKS)
 k_hvp(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, const int* __restrict__ cell_start,
       BoxDev b, const double* __restrict__ din, double* __restrict__ yout)
 {
@@ -456,7 +456,7 @@ k_hvp(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, const i
     R* sv = reinterpret_cast<R*>(smem_raw + 16);
     R* sy = sv + T::NN * SV<D>::S;
     R* pf = sy + T::NN * D;                 // streamed particle inputs (NF fields x PFS)
-    R* rec = pf + In::NF * In::PFS;         // per-particle records, aliased by the staging array
+    R* rec = pf + (PF ? In::NF * In::PFS : 0);  // per-particle records, aliased by the staging array
     R* stg = rec;
     const int tile = blockIdx.x;
     const int64_t kt = (int64_t)tile * T::NC;
@@ -468,7 +468,7 @@ k_hvp(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, const i
     int layer = 0;
     while (scs[layer * T::LC] == scs[(layer + 1) * T::LC]) ++layer;
     int lb0 = 0;
-    if (threadIdx.x == 0) {
+    if (PF && threadIdx.x == 0) {
         mbar_init(bar, 1);
         fence_async_smem();
         lb0 = hvp_prefetch<D, R>(P, cache, cap, scs[layer * T::LC], scs[(layer + 1) * T::LC], pf, bar);
@@ -493,7 +493,7 @@ k_hvp(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, const i
         for (int sb = lb; sb < le; sb += T::NT) {
             const int se = min(sb + T::NT, le);
             const int q = threadIdx.x, p = sb + q;
-            const bool from_pf = (sb == lb);
+            const bool from_pf = PF && (sb == lb);
             if (from_pf) mbar_wait(bar, parity);
             if (p < se) {
                 // streamed inputs: smem copy of the first NT particles, global beyond
