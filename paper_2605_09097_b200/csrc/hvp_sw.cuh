@@ -1,0 +1,313 @@
+// hvp_sw.cuh -- sliding-window tiled Hessian-vector product (a5), the default HVP.
+//
+// Same arithmetic as k_hvp (tiled.cuh):  y += sum_p G_p grad N_p,
+//   G_p = gd S' + c' Ah gd^T Ah + l' (Ah : gd) Ah,   gd = sum_j d_j grad N_j^T
+// (derived from PAPER.md:188 Eq. F_update and PAPER.md:208, K = d^2 Phi).
+//
+// One CTA per tile of cells, layers walked in order along the last axis.  Differences from k_hvp:
+//  * sliding window: a scatter item (cell, component a, x-offset i) keeps 3 node planes of
+//    accumulators (last-axis offsets kk = 0, 1, 2 relative to the current layer).  After layer L the
+//    kk = 0 plane (node plane L) has received every contribution it will ever get from this tile
+//    (layers L-2, L-1, L), so the item emits it and shifts the window.  There is no shared-memory
+//    node accumulator tile, no per-layer zeroing, and 3x fewer staged partials.
+//  * per emitted plane, the staged partials (one slot per contributing cell; slots of cells outside
+//    the tile are zeroed once and never written) are summed in a fixed order and written with one
+//    fp64 RED per node and component straight to global memory.
+//  * two CTA barriers per layer (records ready / plane staged) instead of six.
+//  * the node tile is stored with a padded row stride so that the four cells of a warp's lanes hit
+//    distinct bank groups in the tensor-product gather.
+// Particle inputs (x + Newton cache) are streamed with TMA bulk copies (cp.async.bulk + mbarrier),
+// the next non-empty layer in flight while the current one computes.
+#pragma once
+#include "tiled.cuh"
+
+namespace osmpm {
+
+template <int D> struct SW {
+    using T = Tile<D>;
+    // padded last-axis stride of the node tile (3D: 7 nodes -> 224-B rows, 4 cells of a warp at bank
+    // groups 0, 24, 16, 8); 2D unpadded
+    static constexpr int NZP = (D == 3) ? T::N2 + 1 : T::N1;
+    static constexpr int NNP = (D == 3) ? T::N0 * T::N1 * NZP : T::N0 * T::N1;
+    static constexpr int NLAT = (D == 3) ? T::N0 * T::N1 : T::N0;   // lateral nodes of a plane
+    static constexpr int NSLOT = (D == 3) ? 9 : 3;                  // contributing cells per node
+    static constexpr int NITEM = NLAT * D;                          // (lateral node, comp)
+    static constexpr int STG = NITEM * NSLOT;
+    static constexpr int NACC = T::NACC;                            // 3D: (j, kk); 2D: kk
+};
+
+template <int D>
+__device__ __forceinline__ int sw_node(int l0, int l1, int l2)
+{
+    using T = Tile<D>;
+    return (D == 3) ? (l0 * T::N1 + l1) * SW<D>::NZP + l2 : l0 * T::N1 + l1;
+}
+
+template <int D, typename R>
+constexpr size_t hvp_sw_smem_bytes()
+{
+    using T = Tile<D>;
+    return 16 + ((size_t)SW<D>::NNP * SV<D>::S + SW<D>::STG + (size_t)HvpIn<D, R>::NF * HvpIn<D, R>::PFS +
+                 (size_t)HvpRec<D, R>::RS * T::NT) *
+                    sizeof(R);
+}
+
+// gd[a][b] = sum_i d_i,a dN_i/dx_b from the padded node tile (tensor-product order, explicit FMA)
+template <int D, typename R>
+__device__ __forceinline__ void sw_gather(const R* sv, const int* lc, const R (*w)[3], const R (*dw)[3], R* gd)
+{
+    using V2 = typename Vec2<R>::type;
+    using T = Tile<D>;
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) gd[k] = R(0);
+    if (D == 3) {
+        const R* base = sv + sw_node<D>(lc[0], lc[1], lc[2]) * 4;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            R U0[3] = {0, 0, 0}, U1[3] = {0, 0, 0}, U2[3] = {0, 0, 0};
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                R T0[3] = {0, 0, 0}, T1[3] = {0, 0, 0};
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const R* sp = base + ((i * T::N1 + j) * SW<D>::NZP + k) * 4;
+                    const V2 v01 = *reinterpret_cast<const V2*>(sp);
+                    const R s[3] = {v01.x, v01.y, sp[2]};
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        T0[a] = fma(s[a], w[2][k], T0[a]);
+                        T1[a] = fma(s[a], dw[2][k], T1[a]);
+                    }
+                }
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    U0[a] = fma(T0[a], w[1][j], U0[a]);
+                    U1[a] = fma(T0[a], dw[1][j], U1[a]);
+                    U2[a] = fma(T1[a], w[1][j], U2[a]);
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                gd[a * 3 + 0] = fma(U0[a], dw[0][i], gd[a * 3 + 0]);
+                gd[a * 3 + 1] = fma(U1[a], w[0][i], gd[a * 3 + 1]);
+                gd[a * 3 + 2] = fma(U2[a], w[0][i], gd[a * 3 + 2]);
+            }
+        }
+    } else {
+        gather_grad<D, R>(sv, lc, w, dw, gd);
+    }
+}
+
+// item (cell, a, i): emit the completed kk = 0 plane into the staging slots, shift the window
+template <int D, typename R>
+__device__ __forceinline__ void sw_emit(int cellL, int a, int i, R* acc, R* stg)
+{
+    using T = Tile<D>;
+    if (D == 3) {
+        const int cx = cellL / T::T1, cy = cellL % T::T1;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const int nxy = (cx + i) * T::N1 + (cy + j);
+            stg[(nxy * 3 + a) * 9 + i * 3 + j] = acc[j * 3 + 0];
+            acc[j * 3 + 0] = acc[j * 3 + 1];
+            acc[j * 3 + 1] = acc[j * 3 + 2];
+            acc[j * 3 + 2] = R(0);
+        }
+    } else {
+        stg[((cellL + i) * 2 + a) * 3 + i] = acc[0];
+        acc[0] = acc[1];
+        acc[1] = acc[2];
+        acc[2] = R(0);
+    }
+}
+
+// fixed-order NSLOT-term sums of plane `plane` (tile-local last-axis node index) -> one RED each
+template <int D, typename R>
+__device__ __forceinline__ void sw_flush(const BoxDev& b, const int* t, int plane, const R* stg,
+                                         double* __restrict__ out)
+{
+    using T = Tile<D>;
+    for (int it = threadIdx.x; it < SW<D>::NITEM; it += T::NT) {
+        const R* p = stg + it * SW<D>::NSLOT;
+        R s = p[0];
+#pragma unroll
+        for (int k = 1; k < SW<D>::NSLOT; ++k) s += p[k];
+        if (s != R(0)) {
+            const int a = it % D, nxy = it / D;
+            int64_t g;
+            if (D == 3)
+                g = box_node<D>(b, t[0] * T::T0 + nxy / T::N1, t[1] * T::T1 + nxy % T::N1, t[2] * T::T2 + plane);
+            else
+                g = box_node<D>(b, t[0] * T::T0 + nxy, t[1] * T::T1 + plane, 0);
+            atomicAdd(&out[g * D + a], (double)s);
+        }
+    }
+}
+
+// TMA bulk copies of the first min(NT, le - lb) particles of a layer, one field per lane of warp 0
+// (NF <= 32 copies issued in parallel instead of a serial loop on one thread)
+template <int D, typename R>
+__device__ __forceinline__ void sw_prefetch(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, int lb,
+                                            int le, R* pf, uint64_t* bar, int lane)
+{
+    using In = HvpIn<D, R>;
+    static_assert(In::NF <= 32, "one field per lane");
+    const int lb0 = lb & ~(In::UE - 1);                       // 16-B aligned start
+    const int cnt = min(le, lb + Tile<D>::NT) - lb0;
+    const uint32_t bytes = (uint32_t)((cnt + In::UE - 1) & ~(In::UE - 1)) * sizeof(R);
+    fence_async_smem();
+    if (lane == 0) mbar_expect_tx(bar, bytes * In::NF);
+    __syncwarp();
+    if (lane < In::NF) {
+        const R* src = (lane < D) ? P + (int64_t)(PL<D>::X + lane) * cap + lb0 : cache + (int64_t)(lane - D) * cap + lb0;
+        bulk_g2s(pf + lane * In::PFS, src, bytes, bar);
+    }
+}
+
+template <int D, typename R>
+__global__ void __launch_bounds__(Tile<D>::NT, 3)
+k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, const int* __restrict__ cell_start,
+         BoxDev b, const double* __restrict__ din, double* __restrict__ yout)
+{
+    using T = Tile<D>;
+    using C = CL<D>;
+    using In = HvpIn<D, R>;
+    using S = SW<D>;
+    constexpr int RS = HvpRec<D, R>::RS;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+    R* sv = reinterpret_cast<R*>(smem_raw + 16);
+    R* stg = sv + S::NNP * SV<D>::S;
+    R* pf = stg + S::STG;
+    R* rec = pf + In::NF * In::PFS;
+    const int tile = blockIdx.x;
+    const int64_t kt = (int64_t)tile * T::NC;
+    __shared__ int scs[T::NC + 1];  // the tile's cell ranges
+    for (int i = threadIdx.x; i <= T::NC; i += T::NT) scs[i] = cell_start[kt + i];
+    __syncthreads();
+    if (scs[0] == scs[T::NC]) return;
+    auto layer_empty = [&](int l) { return scs[l * T::LC] == scs[(l + 1) * T::LC]; };
+    int first = 0;
+    while (layer_empty(first)) ++first;
+    if (threadIdx.x < 32) {
+        if (threadIdx.x == 0) mbar_init(bar, 1);
+        __syncwarp();
+        sw_prefetch<D, R>(P, cache, cap, scs[first * T::LC], scs[(first + 1) * T::LC], pf, bar, threadIdx.x);
+    }
+    int t[3];
+    tile_coords<D>(b, tile, t);
+    // node tile of d (padded rows) and the staging slots (zero once: slots of cells outside the
+    // tile are never written)
+    for (int idx = threadIdx.x; idx < T::NN * D; idx += T::NT) {
+        const int a = idx % D, l = idx / D;
+        int c[3];
+        tnode_coords<D>(l, c);
+        const int64_t g = box_node<D>(b, t[0] * T::T0 + c[0], t[1] * T::T1 + c[1], t[2] * T::T2 + c[2]);
+        sv[sw_node<D>(c[0], c[1], c[2]) * SV<D>::S + a] = (R)din[g * D + a];
+    }
+    for (int k = threadIdx.x; k < S::STG; k += T::NT) stg[k] = R(0);
+    __syncthreads();
+    const int it = threadIdx.x;
+    const int icell = it / (D * 3), icomp = (it / 3) % D, ii = it % 3;
+    uint32_t parity = 0;
+    R acc[S::NACC];
+#pragma unroll
+    for (int k = 0; k < S::NACC; ++k) acc[k] = R(0);
+    for (int layer = 0; layer < T::NL + 2; ++layer) {
+        if (layer < T::NL && !layer_empty(layer)) {
+            const int lb = scs[layer * T::LC], le = scs[(layer + 1) * T::LC];
+            int next = layer + 1;
+            while (next < T::NL && layer_empty(next)) ++next;
+            const int pf_base = lb & ~(In::UE - 1);
+            const int ks = scs[layer * T::LC + icell];
+            const int ke = scs[layer * T::LC + icell + 1];
+            for (int sb = lb; sb < le; sb += T::NT) {
+                const int se = min(sb + T::NT, le);
+                const int q = threadIdx.x, p = sb + q;
+                const bool from_pf = (sb == lb);
+                if (sb != lb) __syncthreads();  // previous chunk's records consumed
+                if (from_pf) mbar_wait(bar, parity);
+                if (p < se) {
+                    // streamed field f of particle p: the smem copy (first chunk) or global memory.
+                    // The Newton cache is read only after the gather (register pressure: the
+                    // weights and gather temporaries are dead by then).
+                    const R* s = pf + (p - pf_base);
+                    auto in = [&](int f) -> R {
+                        return from_pf ? s[f * In::PFS]
+                                       : (f < D ? P[(int64_t)(PL<D>::X + f) * cap + p] : cache[(int64_t)(f - D) * cap + p]);
+                    };
+                    R x[3];
+#pragma unroll
+                    for (int a = 0; a < D; ++a) x[a] = in(a);
+                    R w[3][3], dw[3][3];
+                    int lc[3] = {0, 0, 0};
+                    weights_at<D, R>(x, b, t, lc, w, dw);
+                    const RecPtr<R> r(rec, q, RS);
+                    store_weights<D, R>(r, w, dw);
+                    R gd[D * D];
+                    sw_gather<D, R>(sv, lc, w, dw, gd);
+                    R Sv[Sym<D>::N], A[D * D];
+#pragma unroll
+                    for (int k = 0; k < Sym<D>::N; ++k) Sv[k] = in(D + C::S + k);
+#pragma unroll
+                    for (int k = 0; k < D * D; ++k) A[k] = in(D + C::A + k);
+                    const R cc = in(D + C::C), ll = in(D + C::L);
+                    // M2 = A gd^T ; tr = A : gd
+                    R M2[D * D], tr = R(0);
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+#pragma unroll
+                        for (int bb = 0; bb < D; ++bb) {
+                            R s = R(0);
+#pragma unroll
+                            for (int k = 0; k < D; ++k) s = fma(A[a * D + k], gd[bb * D + k], s);
+                            M2[a * D + bb] = s;
+                            tr = fma(A[a * D + bb], gd[a * D + bb], tr);
+                        }
+                    const R ltr = ll * tr;
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+#pragma unroll
+                        for (int bb = 0; bb < D; ++bb) {
+                            R s1 = R(0), s2 = R(0);
+#pragma unroll
+                            for (int k = 0; k < D; ++k) {
+                                s1 = fma(gd[a * D + k], Sv[sym_idx<D>(k, bb)], s1);
+                                s2 = fma(M2[a * D + k], A[k * D + bb], s2);
+                            }
+                            *r.at(Rec<D>::G + a * D + bb) = fma(cc, s2, fma(ltr, A[a * D + bb], s1));
+                        }
+                }
+                __syncthreads();  // records ready; the streamed buffer is free
+                if (from_pf) {
+                    parity ^= 1u;
+                    if (threadIdx.x < 32 && next < T::NL)
+                        sw_prefetch<D, R>(P, cache, cap, scs[next * T::LC], scs[(next + 1) * T::LC], pf, bar,
+                                          threadIdx.x);
+                }
+                if (it < T::ITEMS) {
+                    const int p0 = max(ks, sb), p1 = min(ke, se);
+                    const int len = p1 - p0, rot = len > 0 ? (icell & 7) % len : 0;
+                    for (int k = 0; k < len; ++k) {
+                        const RecPtr<R> r(rec, rotated(p0, len, k, rot) - sb, RS);
+                        ItemW<D, R> W;
+                        W.load(r, ii);
+                        R s[D];
+#pragma unroll
+                        for (int bb = 0; bb < D; ++bb) s[bb] = *r.at(Rec<D>::G + icomp * D + bb);
+                        item_linear<D, R>(s, W, acc);
+                    }
+                }
+            }
+        }
+        // node plane `layer` is complete: stage it, then sum the slots and RED
+        if (it < T::ITEMS) sw_emit<D, R>(icell, icomp, ii, acc, stg);
+        __syncthreads();
+        sw_flush<D, R>(b, t, layer, stg, yout);
+        // the next emit must not overwrite slots still being summed: a non-empty next layer has its
+        // records barrier in between; otherwise synchronise here
+        if (layer + 1 >= T::NL || layer_empty(layer + 1)) __syncthreads();
+    }
+}
+
+}  // namespace osmpm

@@ -542,15 +542,15 @@ struct Sub : public osmpm_subdomain {
 
 
 
-    // HVP variant: warp-specialised persistent kernel (default) or the barrier-phased tiled kernel
-    // (OSMPM_HVP=tiled), kept for A/B measurements
+    // HVP variant: sliding-window tiled kernel (default, hvp_sw.cuh); OSMPM_HVP=tiled | tiled_nopf | ws
+    // select the earlier variants, kept for A/B measurements
     int hvp_variant() const
     {
         static int v = -1;
         if (v < 0) {
             const char* e = getenv("OSMPM_HVP");
             const std::string s = e ? e : "";
-            v = (s == "ws") ? 1 : (s == "tiled_nopf") ? 2 : 0;
+            v = (s == "ws") ? 1 : (s == "tiled_nopf") ? 2 : (s == "tiled") ? 0 : 3;
         }
         return v;
     }
@@ -578,8 +578,17 @@ struct Sub : public osmpm_subdomain {
             }
             KC(); k_hvp<D, R, false><<<box.ntiles, T::NT, hvp_smem_bytes<D, R, false>(), st()>>>(
                 P.p, cache.p, cap, cell_start.p, box, din, yout);
-        } else {
+        } else if (hvp_variant() == 0) {
             KC(); k_hvp<D, R><<<box.ntiles, T::NT, hvp_smem(), st()>>>(P.p, cache.p, cap, cell_start.p, box, din, yout);
+        } else {
+            static bool attr3 = false;
+            if (!attr3) {
+                cudaFuncSetAttribute(k_hvp_sw<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)hvp_sw_smem_bytes<D, R>());
+                attr3 = true;
+            }
+            KC(); k_hvp_sw<D, R><<<box.ntiles, T::NT, hvp_sw_smem_bytes<D, R>(), st()>>>(P.p, cache.p, cap,
+                                                                                         cell_start.p, box, din, yout);
         }
         OSMPM_LAUNCH_CHECK();
         if (pf.on) pf.end("hvp", st());

@@ -52,6 +52,7 @@ def main():
     data = [r for r in rows[hi + 1:end] if len(r) == len(h)]
     iS = h.index("Warp Stall Sampling (All Samples)")
     iE = h.index("Instructions Executed")
+    iW = h.index("L1 Wavefronts Shared") if "L1 Wavefronts Shared" in h else None
     amap = line_map(fsub)
 
     def f(x):
@@ -62,22 +63,28 @@ def main():
 
     st = collections.Counter()
     ex = collections.Counter()
+    wf = collections.Counter()
     a0 = int(data[0][0], 16)  # ncu reports absolute addresses; the function starts at the first
     for r in data:
         a = int(r[0], 16) - a0
         key = amap.get(a, ("?", 0))
         st[key] += f(r[iS])
         ex[key] += f(r[iE])
+        if iW is not None:
+            wf[key] += f(r[iW])
     ts = sum(st.values()) or 1
     te = sum(ex.values()) or 1
+    tw = sum(wf.values()) or 1
+    print(f"total shared wavefronts {sum(wf.values()):.4g}")
     src = {}
-    for k, _ in st.most_common(top):
+    order = wf if os.environ.get("SORT") == "smem" else st
+    for k, _ in order.most_common(top):
         fn, ln = k
         path = os.path.join(ROOT, "paper_2605_09097_b200", "csrc", fn)
         if fn not in src and os.path.exists(path):
             src[fn] = open(path).read().splitlines()
         text = src.get(fn, [""] * (ln + 1))[ln - 1].strip()[:80] if ln else ""
-        print(f"{st[k] / ts * 100:5.1f}% stall {ex[k] / te * 100:5.1f}% inst  {fn}:{ln}  {text}")
+        print(f"{st[k] / ts * 100:5.1f}% stall {ex[k] / te * 100:5.1f}% inst {wf[k] / tw * 100:5.1f}% smem  {fn}:{ln}  {text}")
 
 
 if __name__ == "__main__":
