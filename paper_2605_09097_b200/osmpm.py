@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 
 import numpy as np
 
@@ -152,6 +153,7 @@ class Context:
         s = None if stream is None else C.c_void_p(stream)
         _check(lib().osmpm_ctx_create(C.c_int(device), s, C.byref(self._h)))
         self.device = device
+        self._children = []  # weakrefs to subdomains / couplers: destroyed before the context
 
     def profile(self, enable=True):
         _check(lib().osmpm_profile_enable(self._h, C.c_int(1 if enable else 0)))
@@ -172,6 +174,11 @@ class Context:
 
     def close(self):
         if self._h:
+            # couplers before subdomains before the context they live on
+            kids = [k() for k in self._children]
+            for k in sorted((k for k in kids if k is not None), key=lambda o: not isinstance(o, Coupler)):
+                k.close()
+            self._children = []
             lib().osmpm_ctx_destroy(self._h)
             self._h = C.c_void_p()
 
@@ -197,6 +204,7 @@ class Subdomain:
 
     def __init__(self, ctx: Context, grid, dt, particles, materials, gravity=(0.0, 0.0, 0.0), precision=F64):
         self.ctx = ctx
+        ctx._children.append(weakref.ref(self))
         self.grid = grid
         self.dim = grid.dim
         self._h = C.c_void_p()
@@ -333,7 +341,8 @@ class Subdomain:
 
     def close(self):
         if self._h:
-            lib().osmpm_subdomain_destroy(self._h)
+            if self.ctx._h:
+                lib().osmpm_subdomain_destroy(self._h)
             self._h = C.c_void_p()
 
     def __del__(self):
@@ -368,6 +377,7 @@ class Coupler:
     def __init__(self, coarse: Subdomain, fine: Subdomain, settings: SchwarzSettings):
         self._h = C.c_void_p()
         self.coarse, self.fine = coarse, fine
+        fine.ctx._children.append(weakref.ref(self))
         _check(lib().osmpm_coupler_create(coarse._h, fine._h, C.byref(settings), C.byref(self._h)))
 
     def prepare(self):
@@ -385,7 +395,8 @@ class Coupler:
 
     def close(self):
         if self._h:
-            lib().osmpm_coupler_destroy(self._h)
+            if self.fine._h and self.coarse._h:
+                lib().osmpm_coupler_destroy(self._h)
             self._h = C.c_void_p()
 
     def __del__(self):
