@@ -8,8 +8,23 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libosmpm.so")
 SOURCES = ["capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+def _nccl_dir():
+    """The NCCL that torch loads (nvidia-nccl wheel); libosmpm links the same libnccl.so.2 so one copy
+    serves torch.distributed and the library's communicator."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec and spec.submodule_search_locations:
+        d = list(spec.submodule_search_locations)[0]
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    raise RuntimeError("nccl.h / libnccl.so.2 of the nvidia-nccl wheel not found")
+
+
+NCCL = _nccl_dir()
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17", "--expt-relaxed-constexpr",
-         "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include")]
+         "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"), "-I", os.path.join(NCCL, "include"),
+         "-L", os.path.join(NCCL, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(NCCL, "lib")]
 
 
 def _newest_source():

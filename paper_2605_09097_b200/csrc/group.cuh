@@ -1,0 +1,475 @@
+// group.cuh -- the hot path over a GROUP of x-slabs of one subdomain:
+//   a standalone subdomain is a group of one slab (no exchange at all);
+//   a distributed subdomain (dist.cuh) is one or more slabs per rank, ranks joined by NCCL.
+// Node arrays are kept CONSISTENT on owners and ghosts: after every particle scatter (P2G, gradient,
+// HVP) the ghost planes are reverse-added into their owner and the owner's sums copied back
+// (halo_sum).  Node-wise operations then run redundantly on ghosts, and only reductions (dots,
+// energies, norms) are restricted to owned nodes.  Reductions: the block partials of all local
+// slabs lie back to back, one fixed-order final sum per group, then ncclAllReduce across ranks.
+#pragma once
+#include "subdomain.cuh"
+
+namespace osmpm {
+
+// ---------------------------------------------------------------------------------------------
+// halo exchange of node fields
+// ---------------------------------------------------------------------------------------------
+template <int D, typename R> struct HField {
+    DBuf<double> Sub<D, R>::* f;
+    int nc;
+};
+
+// reverse-add ghost planes into their owners, then copy the owners' sums back to the ghosts
+template <int D, typename R>
+osmpm_status halo_sum(SlabGroup<D, R> G, std::initializer_list<HField<D, R>> fields)
+{
+    const int ns = G.ns;
+    const bool remote = G.multi();
+    if (ns == 1 && !remote) return OSMPM_OK;
+    const int64_t plane = G.s[0]->plane_nodes();
+    cudaStream_t st = G.st;
+    // local pairs: reverse add
+    for (int i = 0; i + 1 < ns; ++i) {
+        Sub<D, R>* a = G.s[i];
+        Sub<D, R>* b = G.s[i + 1];
+        for (const auto& hf : fields) {
+            const int64_t cnt = 2 * plane * hf.nc;
+            const double* src = (a->*hf.f).p + (a->box.nnodes - 2 * plane) * hf.nc;
+            a->KC();
+            k_add_vec<<<nblk_all(cnt, 256), 256, 0, st>>>(cnt, src, (b->*hf.f).p);
+            OSMPM_LAUNCH_CHECK();
+        }
+    }
+    if (remote) {
+        // last local slab -> right rank (its first slab), left rank -> first local slab
+        const GroupComm& gc = *G.gc;
+        int64_t tot = 0;
+        for (const auto& hf : fields) tot += 2 * plane * hf.nc;
+        OSMPM_TRY(G.gb->halo_tmp.need(tot));
+        Sub<D, R>* last = G.s[ns - 1];
+        Sub<D, R>* first = G.s[0];
+        OSMPM_NCCL(ncclGroupStart());
+        int64_t off = 0;
+        for (const auto& hf : fields) {
+            const int64_t cnt = 2 * plane * hf.nc;
+            if (gc.rank + 1 < gc.nranks)
+                OSMPM_NCCL(ncclSend((last->*hf.f).p + (last->box.nnodes - 2 * plane) * hf.nc, cnt, ncclDouble,
+                                    gc.rank + 1, gc.comm, st));
+            if (gc.rank > 0) OSMPM_NCCL(ncclRecv(G.gb->halo_tmp.p + off, cnt, ncclDouble, gc.rank - 1, gc.comm, st));
+            off += cnt;
+        }
+        OSMPM_NCCL(ncclGroupEnd());
+        if (gc.rank > 0) {
+            off = 0;
+            for (const auto& hf : fields) {
+                const int64_t cnt = 2 * plane * hf.nc;
+                first->KC();
+                k_add_vec<<<nblk_all(cnt, 256), 256, 0, st>>>(cnt, G.gb->halo_tmp.p + off, (first->*hf.f).p);
+                OSMPM_LAUNCH_CHECK();
+                off += cnt;
+            }
+        }
+    }
+    // forward copy of the owners' sums into the ghosts
+    for (int i = 0; i + 1 < ns; ++i) {
+        Sub<D, R>* a = G.s[i];
+        Sub<D, R>* b = G.s[i + 1];
+        for (const auto& hf : fields) {
+            const int64_t cnt = 2 * plane * hf.nc;
+            OSMPM_CU(cudaMemcpyAsync((a->*hf.f).p + (a->box.nnodes - 2 * plane) * hf.nc, (b->*hf.f).p,
+                                     cnt * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    if (remote) {
+        const GroupComm& gc = *G.gc;
+        Sub<D, R>* last = G.s[ns - 1];
+        Sub<D, R>* first = G.s[0];
+        OSMPM_NCCL(ncclGroupStart());
+        for (const auto& hf : fields) {
+            const int64_t cnt = 2 * plane * hf.nc;
+            if (gc.rank > 0) OSMPM_NCCL(ncclSend((first->*hf.f).p, cnt, ncclDouble, gc.rank - 1, gc.comm, st));
+            if (gc.rank + 1 < gc.nranks)
+                OSMPM_NCCL(ncclRecv((last->*hf.f).p + (last->box.nnodes - 2 * plane) * hf.nc, cnt, ncclDouble,
+                                    gc.rank + 1, gc.comm, st));
+        }
+        OSMPM_NCCL(ncclGroupEnd());
+    }
+    return OSMPM_OK;
+}
+
+// in-place sum of n doubles across ranks (no-op on one rank)
+template <int D, typename R>
+osmpm_status group_allreduce(SlabGroup<D, R> G, double* d, int n)
+{
+    if (!G.multi()) return OSMPM_OK;
+    OSMPM_NCCL(ncclAllReduce(d, d, n, ncclDouble, ncclSum, G.gc->comm, G.st));
+    return OSMPM_OK;
+}
+
+template <int D, typename R>
+osmpm_status read_gscal(SlabGroup<D, R> G, int cnt)
+{
+    OSMPM_CU(cudaMemcpyAsync(G.gb->h_scal, G.gb->scal.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, G.st));
+    OSMPM_CU(cudaStreamSynchronize(G.st));
+    return OSMPM_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// a1 + a2: P2G over the group
+// ---------------------------------------------------------------------------------------------
+template <int D, typename R>
+osmpm_status group_p2g(SlabGroup<D, R> G)
+{
+    int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, hi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
+    for (int i = 0; i < G.ns; ++i) {
+        int l[3], h[3];
+        OSMPM_TRY(G.s[i]->bounds_local(l, h));
+        OSMPM_TRY(G.s[i]->check_err());
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = std::min(lo[a], l[a]);
+            hi[a] = std::max(hi[a], h[a]);
+        }
+    }
+    if (G.multi()) {
+        // min of (lo, -hi) across ranks
+        int v[6];
+        for (int a = 0; a < 3; ++a) {
+            v[a] = lo[a];
+            v[3 + a] = (hi[a] == INT32_MIN) ? INT32_MAX : -hi[a];
+        }
+        OSMPM_CU(cudaMemcpyAsync(G.gb->gbounds.p, v, sizeof(v), cudaMemcpyHostToDevice, G.st));
+        OSMPM_NCCL(ncclAllReduce(G.gb->gbounds.p, G.gb->gbounds.p, 6, ncclInt32, ncclMin, G.gc->comm, G.st));
+        OSMPM_CU(cudaMemcpyAsync(v, G.gb->gbounds.p, sizeof(v), cudaMemcpyDeviceToHost, G.st));
+        OSMPM_CU(cudaStreamSynchronize(G.st));
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = v[a];
+            hi[a] = (v[3 + a] == INT32_MAX) ? INT32_MIN : -v[3 + a];
+        }
+    }
+    auto& pf = G.ctx->prof;
+    if (pf.on) pf.begin("p2g", G.st);
+    for (int i = 0; i < G.ns; ++i) {
+        G.s[i]->set_box(lo, hi);
+        OSMPM_TRY(G.s[i]->p2g_scatter());
+    }
+    OSMPM_TRY(halo_sum<D, R>(G, {{&Sub<D, R>::m, 1}, {&Sub<D, R>::mom, D}, {&Sub<D, R>::fsig, D}}));
+    for (int i = 0; i < G.ns; ++i) OSMPM_TRY(G.s[i]->p2g_nodes());
+    if (pf.on) pf.end("p2g", G.st);
+    return OSMPM_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// a4: gradient + energy at each slab's u -> g, dg (consistent), gb.scal[0..6]:
+//   particles {E, |E|, inverted}, nodes {E, |E|, |g_free|^2, f_scale^2}
+// ---------------------------------------------------------------------------------------------
+template <int D, typename R>
+osmpm_status group_grad(SlabGroup<D, R> G, bool need_fmask)
+{
+    GroupBufs& gb = *G.gb;
+    int64_t na = 0, nb = 0;
+    for (int i = 0; i < G.ns; ++i) {
+        na += G.s[i]->box.ntiles;
+        nb += G.s[i]->grad_blocks_nodes();
+    }
+    OSMPM_TRY(gb.partA.need((size_t)std::max<int64_t>(na, 1) * 3));
+    OSMPM_TRY(gb.partB.need((size_t)std::max<int64_t>(nb, 1) * 4));
+    auto& pf = G.ctx->prof;
+    if (pf.on) pf.begin("grad", G.st);
+    int64_t off = 0;
+    for (int i = 0; i < G.ns; ++i) {
+        Sub<D, R>* s = G.s[i];
+        OSMPM_TRY(s->grad_scatter(s->u.p, need_fmask, gb.partA.p + off * 3));
+        off += s->box.ntiles;
+    }
+    if (pf.on) pf.end("grad", G.st);
+    OSMPM_TRY(halo_sum<D, R>(G, {{&Sub<D, R>::g, D}, {&Sub<D, R>::dg, D}}));
+    off = 0;
+    for (int i = 0; i < G.ns; ++i) {
+        Sub<D, R>* s = G.s[i];
+        OSMPM_TRY(s->grad_nodes(s->u.p, gb.partB.p + off * 4));
+        off += s->grad_blocks_nodes();
+    }
+    G.s[0]->KC();
+    k_final_sum<3><<<1, 1024, 0, G.st>>>(gb.partA.p, (int)na, gb.scal.p);
+    G.s[0]->KC();
+    k_final_sum<4><<<1, 1024, 0, G.st>>>(gb.partB.p, (int)nb, gb.scal.p + 3);
+    OSMPM_LAUNCH_CHECK();
+    OSMPM_TRY(group_allreduce<D, R>(G, gb.scal.p, 7));
+    return read_gscal<D, R>(G, 7);
+}
+
+// line-search energy at each slab's `ut` (trial) or `u` -> gb.scal[8..12]
+template <int D, typename R>
+osmpm_status group_energy(SlabGroup<D, R> G, bool trial)
+{
+    GroupBufs& gb = *G.gb;
+    int64_t na = 0, nb = 0;
+    for (int i = 0; i < G.ns; ++i) {
+        na += G.s[i]->energy_blocks_particles();
+        nb += G.s[i]->grad_blocks_nodes();
+    }
+    OSMPM_TRY(gb.partA.need((size_t)std::max<int64_t>(na, 1) * 3));
+    OSMPM_TRY(gb.partB.need((size_t)std::max<int64_t>(nb, 1) * 4));
+    auto& pf = G.ctx->prof;
+    if (pf.on) pf.begin("energy", G.st);
+    int64_t oa = 0, ob = 0;
+    for (int i = 0; i < G.ns; ++i) {
+        Sub<D, R>* s = G.s[i];
+        OSMPM_TRY(s->energy_launch(trial ? s->ut.p : s->u.p, gb.partA.p + oa * 3, gb.partB.p + ob * 2));
+        oa += s->energy_blocks_particles();
+        ob += s->grad_blocks_nodes();
+    }
+    if (pf.on) pf.end("energy", G.st);
+    G.s[0]->KC();
+    k_final_sum<3><<<1, 1024, 0, G.st>>>(gb.partA.p, (int)na, gb.scal.p + 8);
+    G.s[0]->KC();
+    k_final_sum<2><<<1, 1024, 0, G.st>>>(gb.partB.p, (int)nb, gb.scal.p + 11);
+    OSMPM_LAUNCH_CHECK();
+    OSMPM_TRY(group_allreduce<D, R>(G, gb.scal.p + 8, 5));
+    return read_gscal<D, R>(G, 13);
+}
+
+// HVP of each slab's p into y (zeroed here), halo-summed, plus the mass term (osmpm_newton_hvp)
+template <int D, typename R>
+osmpm_status group_hvp(SlabGroup<D, R> G)
+{
+    for (int i = 0; i < G.ns; ++i) {
+        Sub<D, R>* s = G.s[i];
+        OSMPM_CU(cudaMemsetAsync(s->y.p, 0, s->box.nnodes * D * sizeof(double), G.st));
+        OSMPM_TRY(s->launch_hvp(s->p.p, s->y.p));
+    }
+    OSMPM_TRY(halo_sum<D, R>(G, {{&Sub<D, R>::y, D}}));
+    for (int i = 0; i < G.ns; ++i) {
+        Sub<D, R>* s = G.s[i];
+        const int64_t nn = s->box.nnodes;
+        s->KC();
+        k_add_mass<D><<<nblk_all(nn, 256), 256, 0, G.st>>>(nn, s->m.p, 1.0 / (s->dt * s->dt), s->p.p, s->y.p);
+        OSMPM_LAUNCH_CHECK();
+    }
+    return OSMPM_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// a3-a7: Newton-PCG with backtracking line search over the group (DESIGN.md
+// R5-R8).  CG scalars live on the device (gb.cgs); a CG iteration has no host synchronisation.
+// ---------------------------------------------------------------------------------------------
+template <int D, typename R>
+osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmpm_solve_stats* stats)
+{
+    GroupBufs& gb = *G.gb;
+    cudaStream_t st = G.st;
+    osmpm_solve_stats stl{};
+    osmpm_solve_stats* sts = stats ? stats : &stl;
+    std::memset(sts, 0, sizeof(*sts));
+    for (int i = 0; i < G.ns; ++i) OSMPM_TRY(G.s[i]->need_grid());
+    Sub<D, R>* s0 = G.s[0];
+    const double dt = s0->dt;
+    const double idt2 = 1.0 / (dt * dt);
+    int64_t nbn_tot = 0, nbd_tot = 0;
+    for (int i = 0; i < G.ns; ++i) {
+        Sub<D, R>* q = G.s[i];
+        const size_t nn = q->box.nnodes;
+        OSMPM_TRY(q->build_dirichlet());
+        q->KC();
+        k_newton_init<D><<<nblk_all(nn, 256), 256, 0, st>>>(nn, q->act.p, q->dmask.p, q->dval.p, q->vn.p, dt, s->guess,
+                                                           q->fmask.p, q->u.p);
+        OSMPM_LAUNCH_CHECK();
+        nbn_tot += nblk(nn, 256);
+        nbd_tot += nblk(nn * D, 256);
+    }
+    OSMPM_TRY(gb.partB.need((size_t)std::max<int64_t>(std::max(nbn_tot, nbd_tot), 1) * 4));
+    const bool remote = G.multi();
+    double g0 = 0.0, gref = 0.0;
+    // E(u) for the line search comes from the same energy kernels as the trial energies, so both
+    // sides of the comparison round alike (R8); later iterations reuse the accepted trial
+    double E0n = 0.0, Ea0n = 0.0;
+    if (s->max_newton > 0) {
+        OSMPM_TRY(group_energy<D, R>(G, false));
+        E0n = (gb.h_scal[10] > 0) ? INFINITY : gb.h_scal[8] + gb.h_scal[11];
+        Ea0n = gb.h_scal[9] + gb.h_scal[12];
+    }
+    bool converged = false;
+    osmpm_status rc = OSMPM_OK;
+    const int chunk = s->fixed_iters ? s->max_cg : 8;
+    auto& pf = G.ctx->prof;
+    // the reduction of the block partials of all slabs (offsets in units of blocks)
+    auto reduce = [&](int nv, int64_t nbtot, auto fused_kernel_launch, auto sum_kernel_launch) -> osmpm_status {
+        if (!remote) {
+            fused_kernel_launch(gb.partB.p, (int)nbtot);
+        } else {
+            s0->KC();
+            if (nv == 1)
+                k_final_sum_cg<1><<<1, 1024, 0, st>>>(gb.partB.p, (int)nbtot, gb.cgs.p, gb.gsum.p);
+            else
+                k_final_sum_cg<2><<<1, 1024, 0, st>>>(gb.partB.p, (int)nbtot, gb.cgs.p, gb.gsum.p);
+            OSMPM_NCCL(ncclAllReduce(gb.gsum.p, gb.gsum.p, nv, ncclDouble, ncclSum, G.gc->comm, st));
+            sum_kernel_launch(gb.gsum.p);
+        }
+        OSMPM_LAUNCH_CHECK();
+        return OSMPM_OK;
+    };
+    for (int it = 0; it < s->max_newton; ++it) {
+        OSMPM_TRY(group_grad<D, R>(G, true));
+        const double gn = std::sqrt(gb.h_scal[5]);
+        const double E0 = E0n, Ea0 = Ea0n;
+        if (it == 0) {
+            // Newton test relative to max(|g^(0)|, force scale) (R6)
+            g0 = gn;
+            gref = std::max(g0, std::sqrt(gb.h_scal[6]));
+        }
+        sts->grad_norm = gn;
+        if (!s->fixed_iters && (gn <= s->newton_rtol * gref || gn <= s->newton_atol)) {
+            converged = true;
+            break;
+        }
+        // Jacobi PCG on H dx = -g (R6, R7)
+        {
+            int64_t off = 0;
+            for (int i = 0; i < G.ns; ++i) {
+                Sub<D, R>* q = G.s[i];
+                const int64_t ndof = q->box.nnodes * D;
+                q->KC();
+                k_cg_init<D><<<nblk(ndof, 256), 256, 0, st>>>(ndof, q->nown * D, q->fmask.p, q->g.p, q->dg.p, q->r.p,
+                                                              q->z.p, q->p.p, q->xs.p, q->y.p, gb.partB.p + off * 2);
+                off += nblk(ndof, 256);
+            }
+            if (!remote) {
+                s0->KC();
+                k_cg_init_fin<<<1, 1024, 0, st>>>(gb.partB.p, (int)off, gb.cgs.p, gn, s->cg_rtol, s->fixed_iters);
+            } else {
+                s0->KC();
+                k_final_sum<2><<<1, 1024, 0, st>>>(gb.partB.p, (int)off, gb.gsum.p);
+                OSMPM_NCCL(ncclAllReduce(gb.gsum.p, gb.gsum.p, 2, ncclDouble, ncclSum, G.gc->comm, st));
+                s0->KC();
+                k_cg_init_fin_sum<<<1, 1, 0, st>>>(gb.gsum.p, gb.cgs.p, gn, s->cg_rtol, s->fixed_iters);
+            }
+            OSMPM_LAUNCH_CHECK();
+        }
+        int done_it = 0;
+        while (done_it < s->max_cg) {
+            const int cnt = std::min(chunk, s->max_cg - done_it);
+            for (int c = 0; c < cnt; ++c) {
+                for (int i = 0; i < G.ns; ++i) OSMPM_TRY(G.s[i]->launch_hvp(G.s[i]->p.p, G.s[i]->y.p));
+                if (pf.on) pf.begin("cg", st);
+                OSMPM_TRY(halo_sum<D, R>(G, {{&Sub<D, R>::y, D}}));
+                int64_t off = 0;
+                for (int i = 0; i < G.ns; ++i) {
+                    Sub<D, R>* q = G.s[i];
+                    const int64_t nn = q->box.nnodes;
+                    q->KC();
+                    k_cg_q<D><<<nblk(nn, 256), 256, 0, st>>>(nn, q->nown, q->fmask.p, q->m.p, idt2, q->p.p, q->y.p,
+                                                             gb.cgs.p, gb.partB.p + off);
+                    off += nblk(nn, 256);
+                }
+                OSMPM_TRY(reduce(
+                    1, off,
+                    [&](double* pp, int nb) {
+                        s0->KC();
+                        k_cg_alpha<<<1, 1024, 0, st>>>(pp, nb, gb.cgs.p);
+                    },
+                    [&](double* v) {
+                        s0->KC();
+                        k_cg_alpha_sum<<<1, 1, 0, st>>>(v, gb.cgs.p);
+                    }));
+                off = 0;
+                for (int i = 0; i < G.ns; ++i) {
+                    Sub<D, R>* q = G.s[i];
+                    const int64_t ndof = q->box.nnodes * D;
+                    q->KC();
+                    k_cg_update<<<nblk(ndof, 256), 256, 0, st>>>(ndof, q->nown * D, q->fmask.p, q->p.p, q->y.p,
+                                                                 q->dg.p, q->xs.p, q->r.p, q->z.p, gb.cgs.p,
+                                                                 gb.partB.p + off * 2);
+                    off += nblk(ndof, 256);
+                }
+                OSMPM_TRY(reduce(
+                    2, off,
+                    [&](double* pp, int nb) {
+                        s0->KC();
+                        k_cg_beta<<<1, 1024, 0, st>>>(pp, nb, gb.cgs.p);
+                    },
+                    [&](double* v) {
+                        s0->KC();
+                        k_cg_beta_sum<<<1, 1, 0, st>>>(v, gb.cgs.p);
+                    }));
+                for (int i = 0; i < G.ns; ++i) {
+                    Sub<D, R>* q = G.s[i];
+                    const int64_t ndof = q->box.nnodes * D;
+                    q->KC();
+                    k_cg_p<<<nblk(ndof, 256), 256, 0, st>>>(ndof, q->z.p, q->p.p, q->y.p, gb.cgs.p);
+                }
+                if (pf.on) pf.end("cg", st);
+                OSMPM_LAUNCH_CHECK();
+            }
+            done_it += cnt;
+            if (!s->fixed_iters) {
+                OSMPM_CU(cudaMemcpyAsync(gb.h_cgs, gb.cgs.p, sizeof(CGScalars), cudaMemcpyDeviceToHost, st));
+                OSMPM_CU(cudaStreamSynchronize(st));
+                if (gb.h_cgs->done) break;
+            }
+        }
+        OSMPM_CU(cudaMemcpyAsync(gb.h_cgs, gb.cgs.p, sizeof(CGScalars), cudaMemcpyDeviceToHost, st));
+        OSMPM_CU(cudaStreamSynchronize(st));
+        sts->cg_iters += gb.h_cgs->it + (gb.h_cgs->done == 2 ? 1 : 0);
+        if (gb.h_cgs->negcurv_first)
+            for (int i = 0; i < G.ns; ++i) {
+                Sub<D, R>* q = G.s[i];
+                OSMPM_CU(cudaMemcpyAsync(q->xs.p, q->z.p, q->box.nnodes * D * sizeof(double),
+                                         cudaMemcpyDeviceToDevice, st));
+            }
+        // backtracking line search (R8)
+        double alpha = 1.0, Et = 0.0, Eat = 0.0;
+        for (;;) {
+            for (int i = 0; i < G.ns; ++i) {
+                Sub<D, R>* q = G.s[i];
+                const int64_t ndof = q->box.nnodes * D;
+                q->KC();
+                k_axpy_free<<<nblk(ndof, 256), 256, 0, st>>>(ndof, q->fmask.p, q->u.p, alpha, q->xs.p, q->ut.p);
+            }
+            OSMPM_LAUNCH_CHECK();
+            OSMPM_TRY(group_energy<D, R>(G, true));
+            const bool inv = gb.h_scal[10] > 0;
+            Et = inv ? INFINITY : gb.h_scal[8] + gb.h_scal[11];
+            Eat = gb.h_scal[9] + gb.h_scal[12];
+            if (Et < E0 || (std::isfinite(Et) && std::fabs(Et - E0) <= s->energy_noise_rtol * Ea0)) break;
+            alpha *= 0.5;
+            sts->ls_halvings++;
+            if (alpha < s->ls_min_alpha) {
+                set_error("line search stagnated at Newton iteration %d (alpha < %g)", it, s->ls_min_alpha);
+                rc = OSMPM_E_LINESEARCH_STAGNATION;
+                break;
+            }
+        }
+        if (rc != OSMPM_OK) break;
+        for (int i = 0; i < G.ns; ++i) {
+            std::swap(G.s[i]->u.p, G.s[i]->ut.p);
+            std::swap(G.s[i]->u.cap, G.s[i]->ut.cap);
+        }
+        E0n = Et;
+        Ea0n = Eat;
+        sts->energy = Et;
+        sts->newton_iters = it + 1;
+    }
+    if (rc == OSMPM_OK && !s->fixed_iters && !converged) {
+        OSMPM_TRY(group_grad<D, R>(G, true));
+        const double gn = std::sqrt(gb.h_scal[5]);
+        sts->grad_norm = gn;
+        if (!(gn <= s->newton_rtol * gref || gn <= s->newton_atol)) {
+            set_error("Newton did not converge in %d iterations (|g| = %g, |g0| = %g)", s->max_newton, gn, g0);
+            rc = OSMPM_E_NEWTON_NOT_CONVERGED;
+        }
+    }
+    sts->grad_norm0 = g0;
+    sts->status = rc;
+    for (int i = 0; i < G.ns; ++i) {
+        Sub<D, R>* q = G.s[i];
+        const int64_t nn = q->box.nnodes;
+        q->KC();
+        k_vnew<D><<<nblk_all(nn, 256), 256, 0, st>>>(nn, q->act.p, q->u.p, 1.0 / dt, q->vnew.p);
+        OSMPM_LAUNCH_CHECK();
+        q->have_vnew = true;
+        q->have_lin = false;  // the cache now refers to an intermediate point
+    }
+    return rc;
+}
+
+}  // namespace osmpm

@@ -228,7 +228,7 @@ namespace osmpm {
 //   force scale |m (|v^n|/dt + |grav|)|^2 over free DOFs      (R6)
 // partials per block: {E_node, E_abs node terms, |g_free|^2, force scale^2}
 template <int D>
-__global__ void k_grad_nodes(int64_t nn, const double* __restrict__ m, const double* __restrict__ vn,
+__global__ void k_grad_nodes(int64_t nn, int64_t nown, const double* __restrict__ m, const double* __restrict__ vn,
                              const double* __restrict__ u, const uint8_t* __restrict__ fmask, double dt,
                              double g0, double g1, double g2, double* __restrict__ g, double* __restrict__ dg,
                              double* __restrict__ partials)
@@ -250,14 +250,16 @@ __global__ void k_grad_nodes(int64_t nn, const double* __restrict__ m, const dou
             const double gv = g[i * D + a] + mi * idt2 * r - fe;
             g[i * D + a] = gv;
             dg[i * D + a] += mi * idt2;
-            if (fmask[i * D + a]) {
+            if (fmask[i * D + a] && i < nown) {
                 red[2] += gv * gv;
                 const double fs = mi * fabs(va) / dt + fabs(fe);
                 red[3] += fs * fs;
             }
         }
-        red[0] += 0.5 * mi * idt2 * q - wf;
-        red[1] += 0.5 * mi * idt2 * qa + fabs(wf);
+        if (i < nown) {
+            red[0] += 0.5 * mi * idt2 * q - wf;
+            red[1] += 0.5 * mi * idt2 * qa + fabs(wf);
+        }
     }
     block_reduce_store<4>(red, partials);
 }
@@ -447,7 +449,7 @@ struct CGScalars {
 
 // r = -g (free), z = r/diag, p = z, x = 0, y = 0 ; partials {rz, rr}
 template <int D>
-__global__ void k_cg_init(int64_t ndof, const uint8_t* __restrict__ fm, const double* __restrict__ g,
+__global__ void k_cg_init(int64_t ndof, int64_t nown_dof, const uint8_t* __restrict__ fm, const double* __restrict__ g,
                           double* __restrict__ dg, double* __restrict__ r, double* __restrict__ z,
                           double* __restrict__ p, double* __restrict__ x, double* __restrict__ y,
                           double* __restrict__ partials)
@@ -463,7 +465,7 @@ __global__ void k_cg_init(int64_t ndof, const uint8_t* __restrict__ fm, const do
         p[k] = zk;
         x[k] = 0.0;
         y[k] = 0.0;
-        if (f) {
+        if (f && k < nown_dof) {
             red[0] += rk * zk;
             red[1] += rk * rk;
         }
@@ -471,11 +473,9 @@ __global__ void k_cg_init(int64_t ndof, const uint8_t* __restrict__ fm, const do
     block_reduce_store<2>(red, partials);
 }
 
-__global__ void k_cg_init_fin(const double* partials, int nb, CGScalars* s, double gn, double cg_rtol, int fixed)
+__device__ __forceinline__ void cg_init_fin(const double* v, CGScalars* s, double gn, double cg_rtol, int fixed)
 {
-    double v[2];
-    final_sum<2>(partials, nb, v);
-    if (threadIdx.x == 0) {
+    {
         s->rz = v[0];
         s->rr = v[1];
         s->gn = gn;
@@ -487,10 +487,21 @@ __global__ void k_cg_init_fin(const double* partials, int nb, CGScalars* s, doub
         s->alpha = s->beta = 0.0;
     }
 }
+__global__ void k_cg_init_fin(const double* partials, int nb, CGScalars* s, double gn, double cg_rtol, int fixed)
+{
+    double v[2];
+    final_sum<2>(partials, nb, v);
+    if (threadIdx.x == 0) cg_init_fin(v, s, gn, cg_rtol, fixed);
+}
+// group-reduced variant: v = {r.z, r.r} already summed over slabs and ranks
+__global__ void k_cg_init_fin_sum(const double* v, CGScalars* s, double gn, double cg_rtol, int fixed)
+{
+    cg_init_fin(v, s, gn, cg_rtol, fixed);
+}
 
 // q = y + m/dt^2 p on free DOFs, 0 elsewhere (in place in y) ; partial p.q
 template <int D>
-__global__ void k_cg_q(int64_t nn, const uint8_t* __restrict__ fm, const double* __restrict__ m, double idt2,
+__global__ void k_cg_q(int64_t nn, int64_t nown, const uint8_t* __restrict__ fm, const double* __restrict__ m, double idt2,
                        const double* __restrict__ p, double* __restrict__ y, const CGScalars* s,
                        double* __restrict__ partials)
 {
@@ -503,19 +514,16 @@ __global__ void k_cg_q(int64_t nn, const uint8_t* __restrict__ fm, const double*
                 const int64_t k = i * D + a;
                 const double q = fm[k] ? y[k] + mi * p[k] : 0.0;
                 y[k] = q;
-                red[0] += p[k] * q;
+                if (i < nown) red[0] += p[k] * q;
             }
         }
     }
     block_reduce_store<1>(red, partials);
 }
 
-__global__ void k_cg_alpha(const double* partials, int nb, CGScalars* s)
+__device__ __forceinline__ void cg_alpha(const double* v, CGScalars* s)
 {
-    if (s->done) return;
-    double v[1];
-    final_sum<1>(partials, nb, v);
-    if (threadIdx.x == 0) {
+    {
         s->pq = v[0];
         if (!(v[0] > 0.0)) {
             s->alpha = 0.0;
@@ -528,9 +536,20 @@ __global__ void k_cg_alpha(const double* partials, int nb, CGScalars* s)
         }
     }
 }
+__global__ void k_cg_alpha(const double* partials, int nb, CGScalars* s)
+{
+    if (s->done) return;
+    double v[1];
+    final_sum<1>(partials, nb, v);
+    if (threadIdx.x == 0) cg_alpha(v, s);
+}
+__global__ void k_cg_alpha_sum(const double* v, CGScalars* s)
+{
+    if (!s->done) cg_alpha(v, s);
+}
 
 // x += alpha p ; r -= alpha q ; z = r/diag ; partials {r.z, r.r}
-__global__ void k_cg_update(int64_t ndof, const uint8_t* __restrict__ fm, const double* __restrict__ p,
+__global__ void k_cg_update(int64_t ndof, int64_t nown_dof, const uint8_t* __restrict__ fm, const double* __restrict__ p,
                             const double* __restrict__ q, const double* __restrict__ dg, double* __restrict__ x,
                             double* __restrict__ r, double* __restrict__ z, const CGScalars* s,
                             double* __restrict__ partials)
@@ -545,7 +564,7 @@ __global__ void k_cg_update(int64_t ndof, const uint8_t* __restrict__ fm, const 
             x[k] = xk;
             r[k] = rk;
             z[k] = zk;
-            if (fm[k]) {
+            if (fm[k] && k < nown_dof) {
                 red[0] += rk * zk;
                 red[1] += rk * rk;
             }
@@ -554,18 +573,33 @@ __global__ void k_cg_update(int64_t ndof, const uint8_t* __restrict__ fm, const 
     block_reduce_store<2>(red, partials);
 }
 
-__global__ void k_cg_beta(const double* partials, int nb, CGScalars* s)
+__device__ __forceinline__ void cg_beta(const double* v, CGScalars* s)
 {
-    if (s->done) return;
-    double v[2];
-    final_sum<2>(partials, nb, v);
-    if (threadIdx.x == 0) {
+    {
         s->beta = (s->rz > 0.0) ? v[0] / s->rz : 0.0;
         s->rz = v[0];
         s->rr = v[1];
         s->it += 1;
         if (!s->fixed && v[1] <= s->tol2) s->done = 1;
     }
+}
+__global__ void k_cg_beta(const double* partials, int nb, CGScalars* s)
+{
+    if (s->done) return;
+    double v[2];
+    final_sum<2>(partials, nb, v);
+    if (threadIdx.x == 0) cg_beta(v, s);
+}
+__global__ void k_cg_beta_sum(const double* v, CGScalars* s)
+{
+    if (!s->done) cg_beta(v, s);
+}
+// single-block final sum that skips the work once CG is done (group reductions of the CG loop)
+template <int NV>
+__global__ void k_final_sum_cg(const double* partials, int nb, const CGScalars* s, double* out)
+{
+    if (s->done) return;
+    final_sum<NV>(partials, nb, out);
 }
 
 // p = z + beta p ; y = 0
@@ -609,10 +643,10 @@ __global__ void k_vnew(int64_t nn, const uint8_t* __restrict__ act, const double
 // dense <-> box node vectors
 // =============================================================================================
 template <int D, typename T>
-__global__ void k_box_to_dense(BoxDev b, int ncomp, const T* __restrict__ src, T* __restrict__ dst)
+__global__ void k_box_to_dense(BoxDev b, int64_t nown, int ncomp, const T* __restrict__ src, T* __restrict__ dst)
 {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= b.nnodes) return;
+    if (i >= nown) return;  // ghost planes are exported by their owner
     int i2 = (D == 3) ? (int)(i % b.nn[2]) : 0;
     int i1 = (D == 3) ? (int)((i / b.nn[2]) % b.nn[1]) : (int)(i % b.nn[1]);
     int i0 = (D == 3) ? (int)(i / ((int64_t)b.nn[2] * b.nn[1])) : (int)(i / b.nn[1]);
@@ -686,6 +720,13 @@ __global__ void k_fext(int64_t nn, const double* m, double g0, double g1, double
     for (int a = 0; a < D; ++a) out[i * D + a] = m[i] * gg[a];
 }
 
+// halo reverse-add: dst[i] += src[i]
+__global__ void k_add_vec(int64_t n, const double* __restrict__ src, double* __restrict__ dst)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) dst[i] += src[i];
+}
+
 template <int D>
 __global__ void k_add_mass(int64_t nn, const double* m, double idt2, const double* d, double* y)
 {
@@ -696,14 +737,14 @@ __global__ void k_add_mass(int64_t nn, const double* m, double idt2, const doubl
 
 // node part of E_h for the line search: {E_node, |E_node terms|}
 template <int D>
-__global__ void k_energy_nodes(int64_t nn, const double* __restrict__ m, const double* __restrict__ vn,
+__global__ void k_energy_nodes(int64_t nn, int64_t nown, const double* __restrict__ m, const double* __restrict__ vn,
                                const double* __restrict__ uu, double dt, double g0, double g1, double g2,
                                double* __restrict__ partials)
 {
     double red[2] = {0.0, 0.0};
     const double grav[3] = {g0, g1, g2};
     const double idt2 = 1.0 / (dt * dt);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nown; i += (int64_t)gridDim.x * blockDim.x) {
         double q = 0.0, wf = 0.0, qa = 0.0;
         for (int a = 0; a < D; ++a) {
             const double ua = uu[i * D + a], va = vn[i * D + a];

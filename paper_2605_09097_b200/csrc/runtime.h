@@ -1,6 +1,7 @@
 // runtime.h -- host-side runtime of libosmpm: context, subdomain interface, error state.
 #pragma once
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <cstdarg>
 #include <cstdint>
@@ -24,9 +25,9 @@ void set_error(const char* fmt, ...);
         }                                                                                           \
     } while (0)
 
-#define OSMPM_TRY(call)                                                                             \
+#define OSMPM_TRY(...)                                                                              \
     do {                                                                                            \
-        osmpm_status s_ = (call);                                                                   \
+        osmpm_status s_ = (__VA_ARGS__);                                                            \
         if (s_ != OSMPM_OK) return s_;                                                              \
     } while (0)
 
@@ -39,6 +40,27 @@ void set_error(const char* fmt, ...);
             return OSMPM_E_CUDA;                                                                    \
         }                                                                                           \
     } while (0)
+
+#define OSMPM_NCCL(call)                                                                            \
+    do {                                                                                            \
+        ncclResult_t r_ = (call);                                                                   \
+        if (r_ != ncclSuccess) {                                                                    \
+            ::osmpm::set_error("NCCL error %s at %s:%d: %s", #call, __FILE__, __LINE__,             \
+                               ncclGetErrorString(r_));                                             \
+            return OSMPM_E_NCCL;                                                                    \
+        }                                                                                           \
+    } while (0)
+
+// Process group of the slab decomposition: one rank per GPU over NCCL (NVLink /
+// NVSwitch).  Inside a rank the fine subdomain may additionally be split into `local_slabs`
+// slabs on the same device, exchanging halos by device copies (the 1-GPU stand-in for the same
+// decomposition: identical slab layout, halo and reduction logic, only the transport differs).
+struct GroupComm {
+    ncclComm_t comm = nullptr;
+    int rank = 0, nranks = 1;
+    int local_slabs = 1;
+    bool multi() const { return nranks > 1; }
+};
 
 // CUDA-event timing of kernel families on the ctx stream
 struct Profiler {
@@ -64,6 +86,7 @@ struct osmpm_ctx {
     osmpm::Profiler prof;
     int num_sms = 148;
     int64_t launches = 0;  // kernels launched through this ctx (bench gpu_launches)
+    osmpm::GroupComm gc;
 };
 
 struct osmpm_subdomain {

@@ -53,6 +53,55 @@ static inline int nblk_all(int64_t n, int bs)
     return (int)std::max<int64_t>(b, 1);
 }
 
+// Scalar / reduction buffers of a slab group (one standalone subdomain = a group of one slab).
+// Block partials of every slab of the group are laid out back to back in partA / partB so that ONE
+// fixed-order final sum reduces the whole group (deterministic); across ranks the sums are
+// ncclAllReduce'd before use.
+struct CGScalars;
+struct GroupBufs {
+    DBuf<double> partA, partB, scal, gsum, halo_tmp;
+    DBuf<CGScalars> cgs;
+    DBuf<int> gbounds;
+    double* h_scal = nullptr;  // pinned
+    CGScalars* h_cgs = nullptr;
+    int* h_bounds = nullptr;
+    osmpm_status init()
+    {
+        if (h_scal) return OSMPM_OK;
+        OSMPM_CU(cudaMallocHost((void**)&h_scal, 64 * sizeof(double)));
+        OSMPM_CU(cudaMallocHost((void**)&h_cgs, 256));
+        OSMPM_CU(cudaMallocHost((void**)&h_bounds, 8 * sizeof(int)));
+        OSMPM_TRY(scal.need(64));
+        OSMPM_TRY(gsum.need(8));
+        OSMPM_TRY(cgs.need(1));
+        OSMPM_TRY(gbounds.need(8));
+        return OSMPM_OK;
+    }
+    ~GroupBufs()
+    {
+        if (h_scal) cudaFreeHost(h_scal);
+        if (h_cgs) cudaFreeHost(h_cgs);
+        if (h_bounds) cudaFreeHost(h_bounds);
+    }
+};
+
+template <int D, typename R> struct Sub;
+template <int D, typename R> struct SlabGroup {
+    Sub<D, R>* const* s;  // local slabs, ordered along x
+    int ns;
+    GroupComm* gc;        // nullptr or nranks == 1: no inter-rank exchange
+    GroupBufs* gb;
+    cudaStream_t st;
+    osmpm_ctx* ctx;
+    bool multi() const { return gc && gc->multi(); }
+};
+template <int D, typename R> osmpm_status group_p2g(SlabGroup<D, R> G);
+template <int D, typename R> osmpm_status group_grad(SlabGroup<D, R> G, bool need_fmask);
+template <int D, typename R> osmpm_status group_energy(SlabGroup<D, R> G, bool trial);
+template <int D, typename R> osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s,
+                                                      osmpm_solve_stats* stats);
+template <int D, typename R> osmpm_status group_hvp(SlabGroup<D, R> G);
+
 // A Dirichlet list in global dense-box node indices (user constraints, or Schwarz receivers)
 struct DirList {
     DBuf<int64_t> idx;
@@ -93,20 +142,33 @@ struct Sub : public osmpm_subdomain {
     DBuf<double> stage_io;  // persistent host-I/O staging buffer
 
     // ---- reductions / scalars ---------------------------------------------------------------
-    DBuf<double> partA, partB, scal;
-    DBuf<CGScalars> cgs;
+    GroupBufs gbself;  // used when the subdomain is standalone (a group of one slab)
     DBuf<ErrLatch> err;
     DBuf<int> bounds;
-    double* h_scal = nullptr;  // pinned
-    CGScalars* h_cgs = nullptr;
     int* h_bounds = nullptr;
+    int part_off = 0;  // this slab's block-partial offset inside its group's partial buffers
+
+    // ---- slab decomposition --------------------------------------------------
+    // cells [cut_lo, cut_hi) along x (INT32_MIN / INT32_MAX: open end).  A slab with a right
+    // neighbour carries the neighbour's first two node planes as ghosts (the last two planes of its
+    // box, x being the slowest box axis): scatters into them are reverse-added to the owner, and the
+    // owner's sums copied back, so every node array is consistent on owners and ghosts.
+    int cut_lo = INT32_MIN, cut_hi = INT32_MAX;
+    bool ghost_right = false;
+    int64_t nown = 0;  // owned box nodes (all but the ghost planes)
 
     ~Sub() override
     {
-        if (h_scal) cudaFreeHost(h_scal);
-        if (h_cgs) cudaFreeHost(h_cgs);
         if (h_bounds) cudaFreeHost(h_bounds);
     }
+
+    SlabGroup<D, R> self_group()
+    {
+        Sub<D, R>* const* me = &self_ptr;
+        self_ptr = this;
+        return SlabGroup<D, R>{me, 1, nullptr, &gbself, st(), ctx};
+    }
+    Sub<D, R>* self_ptr = nullptr;
 
     cudaStream_t st() const { return ctx->stream; }
     void KC() const { ctx->launches++; }
@@ -114,8 +176,11 @@ struct Sub : public osmpm_subdomain {
     // =========================================================================================
     // creation
     // =========================================================================================
+    // sel: the creation indices of the particles this subdomain (slab) takes (nullptr: all of them);
+    // cap_min: particle capacity to reserve (slabs keep slack for migration)
     osmpm_status create(const osmpm_grid_desc* gd, double dt_, const osmpm_particles_view* pv,
-                        const osmpm_material* mt, int nm, const double* gravity)
+                        const osmpm_material* mt, int nm, const double* gravity, const int64_t* sel = nullptr,
+                        int64_t nsel = -1, int64_t cap_min = 0)
     {
         for (int a = 0; a < 3; ++a) {
             origin[a] = gd->origin[a];
@@ -133,12 +198,13 @@ struct Sub : public osmpm_subdomain {
             mats.mu[k] = mt[k].E / (2.0 * (1.0 + mt[k].nu));
             mats.lam[k] = mt[k].E * mt[k].nu / ((1.0 + mt[k].nu) * (1.0 - 2.0 * mt[k].nu));
         }
-        n = pv->n;
+        n = sel ? nsel : pv->n;
+        const int64_t nall = pv->n;
+        auto src_of = [&](int64_t i) -> int64_t { return sel ? sel[i] : i; };
         // field stride: a multiple of 4 (16-B aligned fields for the TMA bulk copies) with >= 4
         // elements of slack (bulk copies round their length up to 16 B)
-        cap = ((n + 4 + 3) / 4) * 4;
-        OSMPM_CU(cudaMallocHost((void**)&h_scal, 64 * sizeof(double)));
-        OSMPM_CU(cudaMallocHost((void**)&h_cgs, sizeof(CGScalars)));
+        cap = ((std::max(n, cap_min) + 4 + 3) / 4) * 4;
+        OSMPM_TRY(gbself.init());
         OSMPM_CU(cudaMallocHost((void**)&h_bounds, 8 * sizeof(int)));
         OSMPM_TRY(P.need(L::NF * cap));
         OSMPM_TRY(P2.need(L::NF * cap));
@@ -151,8 +217,6 @@ struct Sub : public osmpm_subdomain {
         OSMPM_TRY(bnd2.need(cap));
         OSMPM_TRY(err.need(1));
         OSMPM_TRY(bounds.need(8));
-        OSMPM_TRY(scal.need(64));
-        OSMPM_TRY(cgs.need(1));
         OSMPM_CU(cudaMemsetAsync(err.p, 0, sizeof(ErrLatch), st()));
         // host staging in creation order -> field-major SoA (the initial order is creation order)
         std::vector<R> h((size_t)L::NF * cap);
@@ -170,32 +234,37 @@ struct Sub : public osmpm_subdomain {
         const Fld flds[] = {{pv->x, L::X, D}, {pv->v, L::V, D}, {pv->F, L::F, D * D},
                             {pv->B, L::B, D * D}, {pv->m, L::M, 1}, {pv->V0, L::VOL, 1}};
         for (const Fld& fl : flds) {
-            const double* s = host_view(fl.src, (size_t)n * fl.nc);
+            const double* s = host_view(fl.src, (size_t)nall * fl.nc);
             for (int c = 0; c < fl.nc; ++c)
                 for (int64_t i = 0; i < n; ++i) {
-                    double v = s ? s[i * fl.nc + c] : ((fl.off == L::F || fl.off == L::B) ? 0.0 : 0.0);
+                    double v = s ? s[src_of(i) * fl.nc + c] : 0.0;
                     if (!s && fl.off == L::F && (c % (D + 1)) == 0) v = 1.0;
                     h[(size_t)(fl.off + c) * cap + i] = (R)v;
                 }
         }
         if (pv->material) {
+            std::vector<int> all(nall);
             if (pv->space == OSMPM_HOST)
-                std::memcpy(hm.data(), pv->material, n * sizeof(int));
+                std::memcpy(all.data(), pv->material, nall * sizeof(int));
             else
-                cudaMemcpy(hm.data(), pv->material, n * sizeof(int), cudaMemcpyDeviceToHost);
-            for (int64_t i = 0; i < n; ++i)
+                cudaMemcpy(all.data(), pv->material, nall * sizeof(int), cudaMemcpyDeviceToHost);
+            for (int64_t i = 0; i < n; ++i) {
+                hm[i] = all[src_of(i)];
                 if (hm[i] < 0 || hm[i] >= nm) {
-                    set_error("particle %lld: material %d outside [0, %d)", (long long)i, hm[i], nm);
+                    set_error("particle %lld: material %d outside [0, %d)", (long long)src_of(i), hm[i], nm);
                     return OSMPM_E_INVALID_ARG;
                 }
+            }
         }
         if (pv->is_boundary) {
+            std::vector<uint8_t> all(nall);
             if (pv->space == OSMPM_HOST)
-                std::memcpy(hb.data(), pv->is_boundary, n);
+                std::memcpy(all.data(), pv->is_boundary, nall);
             else
-                cudaMemcpy(hb.data(), pv->is_boundary, n, cudaMemcpyDeviceToHost);
+                cudaMemcpy(all.data(), pv->is_boundary, nall, cudaMemcpyDeviceToHost);
+            for (int64_t i = 0; i < n; ++i) hb[i] = all[src_of(i)];
         }
-        for (int64_t i = 0; i < n; ++i) hp[i] = (int)i;
+        for (int64_t i = 0; i < n; ++i) hp[i] = (int)src_of(i);
         // activity threshold 1e-12 * median particle mass (R4)
         if (n > 0) {
             std::vector<double> ms(n);
@@ -212,8 +281,11 @@ struct Sub : public osmpm_subdomain {
         OSMPM_CU(cudaMemcpy(pid.p, hp.data(), cap * sizeof(int), cudaMemcpyHostToDevice));
         OSMPM_CU(cudaMemcpy(bnd.p, hb.data(), cap, cudaMemcpyHostToDevice));
         // validate the safe interior right away
-        OSMPM_TRY(compute_box());
-        return check_err();
+        if (!sel) {
+            OSMPM_TRY(compute_box());
+            return check_err();
+        }
+        return OSMPM_OK;
     }
     double median_mass = 0, total_mass = 0;
 
@@ -271,7 +343,9 @@ struct Sub : public osmpm_subdomain {
         b.inv_dx = 1.0 / dx;
     }
 
-    osmpm_status compute_box()
+    // lowest / highest base node per axis of this subdomain's particles (and the safe-interior
+    // check); INT32_MAX / INT32_MIN when it holds none
+    osmpm_status bounds_local(int* lo, int* hi)
     {
         BoxDev b{};
         fill_box_common(b);
@@ -283,29 +357,44 @@ struct Sub : public osmpm_subdomain {
         }
         OSMPM_CU(cudaMemcpyAsync(h_bounds, bounds.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, st()));
         OSMPM_CU(cudaStreamSynchronize(st()));
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = h_bounds[a];
+            hi[a] = h_bounds[3 + a];
+        }
+        return OSMPM_OK;
+    }
+
+    // node box of the step from the GROUP's base-node bounds glo / ghi (whole tiles; the x range of
+    // a slab is its cut range, so neighbouring slabs share node planes exactly)
+    void set_box(const int* glo, const int* ghi)
+    {
+        BoxDev b{};
+        fill_box_common(b);
         const int tt[3] = {T::T0, T::T1, T::T2};
+        const bool any = glo[0] <= ghi[0];
         int64_t ncells = 1, nnodes = 1;
         int ntiles = 1;
         for (int a = 0; a < 3; ++a) {
-            if (a < D && n > 0) {
-                int lo = h_bounds[a], hi = h_bounds[3 + a];
-                int c = hi - lo + 1;
+            int lo = 0, c = tt[a];
+            if (a < D && any) {
+                lo = glo[a];
+                int hiex = ghi[a] + 1;
+                if (a == 0 && cut_lo != INT32_MIN) lo = cut_lo;
+                if (a == 0 && cut_lo == INT32_MIN && cut_hi != INT32_MAX) {
+                    // first slab: align down from the first cut so that the cut is a tile boundary
+                    const int w = std::max(cut_hi - glo[0], 1);
+                    lo = cut_hi - ((w + tt[0] - 1) / tt[0]) * tt[0];
+                }
+                if (a == 0 && cut_hi != INT32_MAX) hiex = cut_hi;
+                c = std::max(hiex - lo, 1);
                 c = ((c + tt[a] - 1) / tt[a]) * tt[a];
-                b.lo[a] = lo;
-                b.nc[a] = c;
-                b.nn[a] = c + 2;
-                b.nt[a] = c / tt[a];
-            } else if (a < D) {
-                b.lo[a] = 0;
-                b.nc[a] = tt[a];
-                b.nn[a] = tt[a] + 2;
-                b.nt[a] = 1;
-            } else {
-                b.lo[a] = 0;
-                b.nc[a] = 1;
-                b.nn[a] = 1;
-                b.nt[a] = 1;
+            } else if (a >= D) {
+                c = 1;
             }
+            b.lo[a] = lo;
+            b.nc[a] = c;
+            b.nn[a] = (a < D) ? c + 2 : 1;
+            b.nt[a] = (a < D) ? c / tt[a] : 1;
             ncells *= b.nc[a];
             nnodes *= b.nn[a];
             ntiles *= b.nt[a];
@@ -314,6 +403,17 @@ struct Sub : public osmpm_subdomain {
         b.nnodes = nnodes;
         b.ntiles = ntiles;
         box = b;
+        ghost_right = cut_hi != INT32_MAX;
+        const int64_t plane = (D == 3) ? (int64_t)b.nn[1] * b.nn[2] : b.nn[1];
+        nown = ghost_right ? nnodes - 2 * plane : nnodes;
+    }
+    int64_t plane_nodes() const { return (D == 3) ? (int64_t)box.nn[1] * box.nn[2] : box.nn[1]; }
+
+    osmpm_status compute_box()
+    {
+        int lo[3], hi[3];
+        OSMPM_TRY(bounds_local(lo, hi));
+        set_box(lo, hi);
         return OSMPM_OK;
     }
 
@@ -363,38 +463,38 @@ struct Sub : public osmpm_subdomain {
         OSMPM_TRY(act.need(nn));
         OSMPM_TRY(dmask.need(nn));
         OSMPM_TRY(fmask.need(nd));
-        OSMPM_TRY(partA.need((size_t)std::max<int64_t>(box.ntiles, 148 * 8) * 4));
-        OSMPM_TRY(partB.need((size_t)148 * 8 * 4));
         return OSMPM_OK;
     }
 
     // =========================================================================================
     // a2: P2G
     // =========================================================================================
-    osmpm_status p2g() override
+    // P2G of this slab: sort, scatter (the group then halo-sums m, mom, f^sigma), node pass
+    osmpm_status p2g_scatter()
     {
-        OSMPM_TRY(compute_box());
-        OSMPM_TRY(check_err());
         OSMPM_TRY(sort_particles());
         OSMPM_TRY(alloc_nodes());
         const size_t nn = box.nnodes;
         OSMPM_CU(cudaMemsetAsync(m.p, 0, nn * sizeof(double), st()));
         OSMPM_CU(cudaMemsetAsync(mom.p, 0, nn * D * sizeof(double), st()));
         OSMPM_CU(cudaMemsetAsync(fsig.p, 0, nn * D * sizeof(double), st()));
-        auto& pf = ctx->prof;
-        if (pf.on) pf.begin("p2g", st());
         if (n > 0) {
             KC(); k_p2g<D, R><<<nblk_all(n, 128), 128, 0, st()>>>(P.p, cap, n, mat.p, box, mats, m.p, mom.p, fsig.p);
             OSMPM_LAUNCH_CHECK();
         }
+        return OSMPM_OK;
+    }
+    osmpm_status p2g_nodes()
+    {
+        const size_t nn = box.nnodes;
         KC(); k_p2g_nodes<D><<<nblk_all(nn, 256), 256, 0, st()>>>(nn, m.p, mom.p, vn.p, act.p, mass_thr);
         OSMPM_LAUNCH_CHECK();
-        if (pf.on) pf.end("p2g", st());
         have_grid = true;
         have_lin = false;
         have_vnew = false;
         return OSMPM_OK;
     }
+    osmpm_status p2g() override { return group_p2g<D, R>(self_group()); }
 
     osmpm_status boundary_mass()
     {
@@ -425,7 +525,7 @@ struct Sub : public osmpm_subdomain {
         }
         OSMPM_CU(cudaMemsetAsync(dptr, 0, cnt * sizeof(Tv), st()));
         if (have_grid) {
-            KC(); k_box_to_dense<D, Tv><<<nblk_all(box.nnodes, 256), 256, 0, st()>>>(box, nc, src, dptr);
+            KC(); k_box_to_dense<D, Tv><<<nblk_all(box.nnodes, 256), 256, 0, st()>>>(box, nown, nc, src, dptr);
             OSMPM_LAUNCH_CHECK();
         }
         if (sp == OSMPM_HOST) {
@@ -483,47 +583,38 @@ struct Sub : public osmpm_subdomain {
 
 
     // =========================================================================================
-    // a4: gradient + energy at u (box vector) -> g (raw), dg (raw), scalars
-    // scal[0..2] particle {E, |E|, inverted}; scal[3..5] node {E, |E|, |g_free|^2}
+    // a4: gradient + energy at u (box vector) -> g (raw), dg (raw); block partials into the group's
+    // buffers: particle part {E, |E|, inverted} (partA), node part {E, |E|, |g_free|^2, f_scale^2}
+    // (partB, owned nodes only)
     // =========================================================================================
     size_t grad_smem() const { return grad_smem_bytes<D>(); }
     size_t hvp_smem() const { return hvp_smem_bytes<D, R>(); }
+    int grad_blocks_nodes() const { return nblk(box.nnodes, 256); }
 
-    osmpm_status grad_eval(const double* uu, bool need_fmask)
+    osmpm_status grad_scatter(const double* uu, bool need_fmask, double* partA)
     {
         const size_t nn = box.nnodes;
         OSMPM_TRY(cache.need(C::NF * cap));
         OSMPM_CU(cudaMemsetAsync(g.p, 0, nn * D * sizeof(double), st()));
         OSMPM_CU(cudaMemsetAsync(dg.p, 0, nn * D * sizeof(double), st()));
         if (!need_fmask) OSMPM_CU(cudaMemsetAsync(fmask.p, 1, nn * D, st()));
-        auto& pf = ctx->prof;
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(k_grad<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grad_smem());
             cudaFuncSetAttribute(k_hvp<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hvp_smem());
             attr = true;
         }
-        if (pf.on) pf.begin("grad", st());
         KC(); k_grad<D, R><<<box.ntiles, T::NT, grad_smem(), st()>>>(P.p, cache.p, cap, mat.p, cell_start.p, box, mats,
-                                                               uu, g.p, dg.p, partA.p);
+                                                                   uu, g.p, dg.p, partA);
         OSMPM_LAUNCH_CHECK();
-        if (pf.on) pf.end("grad", st());
-        const int nbn = nblk(nn, 256);
-        KC(); k_grad_nodes<D><<<nbn, 256, 0, st()>>>(nn, m.p, vn.p, uu, fmask.p, dt, grav[0], grav[1], grav[2], g.p, dg.p,
-                                                partB.p);
-        OSMPM_LAUNCH_CHECK();
-        // scal[0..2] particles {E, E_abs, inverted}; scal[3..6] nodes {E, E_abs, |g_free|^2, f_scale^2}
-        KC(); k_final_sum<3><<<1, 1024, 0, st()>>>(partA.p, box.ntiles, scal.p);
-        KC(); k_final_sum<4><<<1, 1024, 0, st()>>>(partB.p, nbn, scal.p + 3);
-        OSMPM_LAUNCH_CHECK();
-        have_lin = true;
         return OSMPM_OK;
     }
-
-    osmpm_status read_scal(int cnt)
+    osmpm_status grad_nodes(const double* uu, double* partB)
     {
-        OSMPM_CU(cudaMemcpyAsync(h_scal, scal.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, st()));
-        OSMPM_CU(cudaStreamSynchronize(st()));
+        KC(); k_grad_nodes<D><<<grad_blocks_nodes(), 256, 0, st()>>>(box.nnodes, nown, m.p, vn.p, uu, fmask.p, dt, grav[0],
+                                                                      grav[1], grav[2], g.p, dg.p, partB);
+        OSMPM_LAUNCH_CHECK();
+        have_lin = true;
         return OSMPM_OK;
     }
 
@@ -531,16 +622,12 @@ struct Sub : public osmpm_subdomain {
     {
         OSMPM_TRY(need_grid());
         OSMPM_TRY(import_dense(uin, D, u.p, sp));
-        OSMPM_TRY(grad_eval(u.p, false));
+        auto G = self_group();
+        OSMPM_TRY(group_grad<D, R>(G, false));
         if (gout) OSMPM_TRY(export_dense<double>(g.p, D, gout, sp));
-        if (E) {
-            OSMPM_TRY(read_scal(6));
-            *E = (h_scal[2] > 0) ? INFINITY : h_scal[0] + h_scal[3];
-        }
+        if (E) *E = (gbself.h_scal[2] > 0) ? INFINITY : gbself.h_scal[0] + gbself.h_scal[3];
         return OSMPM_OK;
     }
-
-
 
     // HVP variant: sliding-window tiled kernel (default, hvp_sw.cuh); OSMPM_HVP=tiled | tiled_nopf | ws
     // select the earlier variants, kept for A/B measurements
@@ -602,12 +689,8 @@ struct Sub : public osmpm_subdomain {
             set_error("newton_hvp needs a prior newton_gradient (linearisation point)");
             return OSMPM_E_STATE;
         }
-        const size_t nn = box.nnodes;
         OSMPM_TRY(import_dense(din, D, p.p, sp));
-        OSMPM_CU(cudaMemsetAsync(y.p, 0, nn * D * sizeof(double), st()));
-        OSMPM_TRY(launch_hvp(p.p, y.p));
-        KC(); k_add_mass<D><<<nblk_all(nn, 256), 256, 0, st()>>>(nn, m.p, 1.0 / (dt * dt), p.p, y.p);
-        OSMPM_LAUNCH_CHECK();
+        OSMPM_TRY(group_hvp<D, R>(self_group()));
         return export_dense<double>(y.p, D, yout, sp);
     }
 
@@ -660,141 +743,23 @@ struct Sub : public osmpm_subdomain {
         return OSMPM_OK;
     }
 
-    osmpm_status energy_eval(const double* uu)
+    // line-search energy at uu: block partials particle {E, |E|, inverted} (partA), node {E, |E|}
+    // (partB, owned nodes only)
+    int energy_blocks_particles() const { return nblk(n, 256); }
+    osmpm_status energy_launch(const double* uu, double* partA, double* partB)
     {
-        const size_t nn = box.nnodes;
-        auto& pf = ctx->prof;
-        const int nbp = nblk(n, 256);
-        if (pf.on) pf.begin("energy", st());
-        KC(); k_energy<D, R><<<nbp, 256, 0, st()>>>(P.p, cap, n, mat.p, box, mats, uu, partA.p);
+        KC(); k_energy<D, R><<<energy_blocks_particles(), 256, 0, st()>>>(P.p, cap, n, mat.p, box, mats, uu, partA);
         OSMPM_LAUNCH_CHECK();
-        if (pf.on) pf.end("energy", st());
-        const int nbn = nblk(nn, 256);
-        KC(); k_energy_nodes<D><<<nbn, 256, 0, st()>>>(nn, m.p, vn.p, uu, dt, grav[0], grav[1], grav[2], partB.p);
-        OSMPM_LAUNCH_CHECK();
-        // scal[8..10] particles {E, E_abs, inverted}; scal[11..12] nodes {E, E_abs}
-        KC(); k_final_sum<3><<<1, 1024, 0, st()>>>(partA.p, nbp, scal.p + 8);
-        KC(); k_final_sum<2><<<1, 1024, 0, st()>>>(partB.p, nbn, scal.p + 11);
+        KC(); k_energy_nodes<D><<<grad_blocks_nodes(), 256, 0, st()>>>(box.nnodes, nown, m.p, vn.p, uu, dt, grav[0],
+                                                                        grav[1], grav[2], partB);
         OSMPM_LAUNCH_CHECK();
         return OSMPM_OK;
     }
 
-
-
     osmpm_status implicit_solve(const osmpm_newton_settings* s, osmpm_solve_stats* stats) override
     {
         OSMPM_TRY(need_grid());
-        osmpm_solve_stats stl{};
-        osmpm_solve_stats* sts = stats ? stats : &stl;
-        std::memset(sts, 0, sizeof(*sts));
-        const size_t nn = box.nnodes, ndof = nn * D;
-        OSMPM_TRY(build_dirichlet());
-        KC(); k_newton_init<D><<<nblk_all(nn, 256), 256, 0, st()>>>(nn, act.p, dmask.p, dval.p, vn.p, dt, s->guess, fmask.p,
-                                                               u.p);
-        OSMPM_LAUNCH_CHECK();
-        const double idt2 = 1.0 / (dt * dt);
-        double g0 = 0.0, gref = 0.0;
-        // E(u) for the line search comes from the same energy kernel as the trial energies, so both
-        // sides of the comparison round alike (R8); later iterations reuse the accepted trial
-        double E0n = 0.0, Ea0n = 0.0;
-        if (s->max_newton > 0) {
-            OSMPM_TRY(energy_eval(u.p));
-            OSMPM_TRY(read_scal(13));
-            E0n = (h_scal[10] > 0) ? INFINITY : h_scal[8] + h_scal[11];
-            Ea0n = h_scal[9] + h_scal[12];
-        }
-        bool converged = false;
-        osmpm_status rc = OSMPM_OK;
-        const int nbd = nblk(ndof, 256), nbn = nblk(nn, 256);
-        const int chunk = s->fixed_iters ? s->max_cg : 8;
-        for (int it = 0; it < s->max_newton; ++it) {
-            OSMPM_TRY(grad_eval(u.p, true));
-            OSMPM_TRY(read_scal(7));
-            const double gn = std::sqrt(h_scal[5]);
-            const double E0 = E0n, Ea0 = Ea0n;
-            if (it == 0) {
-                // Newton test relative to max(|g^(0)|, force scale) (R6)
-                g0 = gn;
-                gref = std::max(g0, std::sqrt(h_scal[6]));
-            }
-            sts->grad_norm = gn;
-            if (!s->fixed_iters && (gn <= s->newton_rtol * gref || gn <= s->newton_atol)) {
-                converged = true;
-                break;
-            }
-            // Jacobi PCG on H dx = -g (R6, R7)
-            KC(); k_cg_init<D><<<nbd, 256, 0, st()>>>(ndof, fmask.p, g.p, dg.p, r.p, z.p, p.p, xs.p, y.p, partB.p);
-            KC(); k_cg_init_fin<<<1, 1024, 0, st()>>>(partB.p, nbd, cgs.p, gn, s->cg_rtol, s->fixed_iters);
-            OSMPM_LAUNCH_CHECK();
-            int done_it = 0;
-            while (done_it < s->max_cg) {
-                const int cnt = std::min(chunk, s->max_cg - done_it);
-                for (int c = 0; c < cnt; ++c) {
-                    OSMPM_TRY(launch_hvp(p.p, y.p));
-                    if (ctx->prof.on) ctx->prof.begin("cg", st());
-                    KC(); k_cg_q<D><<<nbn, 256, 0, st()>>>(nn, fmask.p, m.p, idt2, p.p, y.p, cgs.p, partB.p);
-                    KC(); k_cg_alpha<<<1, 1024, 0, st()>>>(partB.p, nbn, cgs.p);
-                    KC(); k_cg_update<<<nbd, 256, 0, st()>>>(ndof, fmask.p, p.p, y.p, dg.p, xs.p, r.p, z.p, cgs.p, partB.p);
-                    KC(); k_cg_beta<<<1, 1024, 0, st()>>>(partB.p, nbd, cgs.p);
-                    KC(); k_cg_p<<<nbd, 256, 0, st()>>>(ndof, z.p, p.p, y.p, cgs.p);
-                    if (ctx->prof.on) ctx->prof.end("cg", st());
-                    OSMPM_LAUNCH_CHECK();
-                }
-                done_it += cnt;
-                if (!s->fixed_iters) {
-                    OSMPM_CU(cudaMemcpyAsync(h_cgs, cgs.p, sizeof(CGScalars), cudaMemcpyDeviceToHost, st()));
-                    OSMPM_CU(cudaStreamSynchronize(st()));
-                    if (h_cgs->done) break;
-                }
-            }
-            OSMPM_CU(cudaMemcpyAsync(h_cgs, cgs.p, sizeof(CGScalars), cudaMemcpyDeviceToHost, st()));
-            OSMPM_CU(cudaStreamSynchronize(st()));
-            sts->cg_iters += h_cgs->it + (h_cgs->done == 2 ? 1 : 0);
-            if (h_cgs->negcurv_first) OSMPM_CU(cudaMemcpyAsync(xs.p, z.p, ndof * sizeof(double), cudaMemcpyDeviceToDevice, st()));
-            // backtracking line search (R8)
-            double alpha = 1.0, Et = 0.0, Eat = 0.0;
-            for (;;) {
-                KC(); k_axpy_free<<<nbd, 256, 0, st()>>>(ndof, fmask.p, u.p, alpha, xs.p, ut.p);
-                OSMPM_LAUNCH_CHECK();
-                OSMPM_TRY(energy_eval(ut.p));
-                OSMPM_TRY(read_scal(13));
-                const bool inv = h_scal[10] > 0;
-                Et = inv ? INFINITY : h_scal[8] + h_scal[11];
-                Eat = h_scal[9] + h_scal[12];
-                if (Et < E0 || (std::isfinite(Et) && std::fabs(Et - E0) <= s->energy_noise_rtol * Ea0)) break;
-                alpha *= 0.5;
-                sts->ls_halvings++;
-                if (alpha < s->ls_min_alpha) {
-                    set_error("line search stagnated at Newton iteration %d (alpha < %g)", it, s->ls_min_alpha);
-                    rc = OSMPM_E_LINESEARCH_STAGNATION;
-                    break;
-                }
-            }
-            if (rc != OSMPM_OK) break;
-            std::swap(u.p, ut.p);
-            std::swap(u.cap, ut.cap);
-            E0n = Et;
-            Ea0n = Eat;
-            sts->energy = Et;
-            sts->newton_iters = it + 1;
-        }
-        if (rc == OSMPM_OK && !s->fixed_iters && !converged) {
-            OSMPM_TRY(grad_eval(u.p, true));
-            OSMPM_TRY(read_scal(6));
-            const double gn = std::sqrt(h_scal[5]);
-            sts->grad_norm = gn;
-            if (!(gn <= s->newton_rtol * gref || gn <= s->newton_atol)) {
-                set_error("Newton did not converge in %d iterations (|g| = %g, |g0| = %g)", s->max_newton, gn, g0);
-                rc = OSMPM_E_NEWTON_NOT_CONVERGED;
-            }
-        }
-        sts->grad_norm0 = g0;
-        sts->status = rc;
-        KC(); k_vnew<D><<<nblk_all(nn, 256), 256, 0, st()>>>(nn, act.p, u.p, 1.0 / dt, vnew.p);
-        OSMPM_LAUNCH_CHECK();
-        have_vnew = true;
-        have_lin = false;  // the cache now refers to an intermediate point
-        return rc;
+        return group_solve<D, R>(self_group(), s, stats);
     }
 
     osmpm_status read_grid_velocity(double* v, osmpm_memspace sp) override

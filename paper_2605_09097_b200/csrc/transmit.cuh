@@ -3,7 +3,7 @@
 //   I_{B->S}   shape-function interpolation, Eq. interp_BtoS
 //   T_m        linear temporal interpolation, Eq. temporal_interp
 #pragma once
-#include "subdomain.cuh"
+#include "group.cuh"
 
 namespace osmpm {
 
