@@ -149,6 +149,26 @@ osmpm_status osmpm_kernel_time(osmpm_ctx* ctx, const char* family, int64_t* laun
 osmpm_status osmpm_launch_count(osmpm_ctx* ctx, int64_t* launches);
 
 /* ----------------------------------------------------------------------------------------------
+ * Slab decomposition of a fine subdomain (the paper's method is serial on one CPU,
+ * PAPER.md:508, and names scalable parallel implementations as future work).
+ * One process per GPU: rank 0 calls osmpm_comm_unique_id and shares the 128 bytes (e.g. with
+ * torch.distributed); every rank then calls osmpm_ctx_init_comm (ncclCommInitRank over NVLink /
+ * NVSwitch).  Subdomains created afterwards with decompose != 0 are split into x-slabs: each rank
+ * keeps the particles whose base node lies in its slabs, ghost node planes are exchanged after every
+ * scatter, reductions are all-reduced, and particles migrate across the cuts after G2P.
+ * osmpm_ctx_set_local_slabs splits each rank's share further into n slabs ON THE SAME DEVICE (halo
+ * exchange by device copies): the same decomposition testable on one GPU.
+ * Reads of a decomposed subdomain fill only this rank's particles / owned nodes (others untouched
+ * for particles, zero for dense node vectors); sum over ranks to assemble. */
+osmpm_status osmpm_comm_unique_id(uint8_t id[128]);
+osmpm_status osmpm_ctx_init_comm(osmpm_ctx* ctx, int rank, int nranks, const uint8_t id[128]);
+osmpm_status osmpm_ctx_set_local_slabs(osmpm_ctx* ctx, int n);
+/* slabs_total, slabs_local, first_slab (this rank's first global slab), n_local (particles on this
+ * rank now), cuts[slabs_total - 1] (cell index along x where slab k+1 starts; may be NULL). */
+osmpm_status osmpm_subdomain_decomp(osmpm_subdomain* sub, int32_t* slabs_total, int32_t* slabs_local,
+                                    int32_t* first_slab, int64_t* n_local, int32_t* cuts);
+
+/* ----------------------------------------------------------------------------------------------
  * Subdomain (§3.1: each subdomain owns a grid (dx, dt) and its particles)
  * ----------------------------------------------------------------------------------------------*/
 /* Copies the particles into library-owned device SoA (sorted internally; reads return creation
@@ -160,6 +180,13 @@ osmpm_status osmpm_subdomain_create(osmpm_ctx* ctx, const osmpm_grid_desc* grid,
                                     const osmpm_material* mats, int32_t n_mats,
                                     const double gravity[3], osmpm_precision prec,
                                     osmpm_subdomain** out);
+/* As osmpm_subdomain_create; decompose = 0 keeps the subdomain whole on this GPU even when the ctx
+ * has a process group or local slabs (e.g. the small coarse subdomain, replicated on every rank). */
+osmpm_status osmpm_subdomain_create_ex(osmpm_ctx* ctx, const osmpm_grid_desc* grid, double dt,
+                                       const osmpm_particles_view* particles,
+                                       const osmpm_material* mats, int32_t n_mats,
+                                       const double gravity[3], osmpm_precision prec, int32_t decompose,
+                                       osmpm_subdomain** out);
 void osmpm_subdomain_destroy(osmpm_subdomain* sub);
 
 osmpm_status osmpm_set_gravity(osmpm_subdomain* sub, const double gravity[3]);

@@ -6,6 +6,7 @@
 
 #include "coupler.cuh"
 #include "transmit.cuh"
+#include "dist.cuh"
 
 namespace osmpm {
 
@@ -118,6 +119,7 @@ void osmpm_ctx_destroy(osmpm_ctx* ctx)
 {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
+    if (ctx->gc.comm) ncclCommDestroy(ctx->gc.comm);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -150,10 +152,52 @@ osmpm_status osmpm_launch_count(osmpm_ctx* ctx, int64_t* launches)
     return OSMPM_OK;
 }
 
+osmpm_status osmpm_comm_unique_id(uint8_t id[128])
+{
+    CHECK_ARG(id, "id is NULL");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId u;
+    OSMPM_NCCL(ncclGetUniqueId(&u));
+    std::memcpy(id, &u, 128);
+    return OSMPM_OK;
+}
+
+osmpm_status osmpm_ctx_init_comm(osmpm_ctx* ctx, int rank, int nranks, const uint8_t id[128])
+{
+    CHECK_ARG(ctx && id, "NULL argument");
+    CHECK_ARG(nranks >= 1 && rank >= 0 && rank < nranks, "rank %d / nranks %d invalid", rank, nranks);
+    CHECK_ARG(!ctx->gc.comm, "communicator already initialised");
+    SET_DEVICE(ctx);
+    ctx->gc.rank = rank;
+    ctx->gc.nranks = nranks;
+    if (nranks > 1) {
+        ncclUniqueId u;
+        std::memcpy(&u, id, 128);
+        OSMPM_NCCL(ncclCommInitRank(&ctx->gc.comm, nranks, u, rank));
+    }
+    return OSMPM_OK;
+}
+
+osmpm_status osmpm_ctx_set_local_slabs(osmpm_ctx* ctx, int n)
+{
+    CHECK_ARG(ctx, "ctx is NULL");
+    CHECK_ARG(n >= 1 && n <= 64, "local slabs %d outside [1, 64]", n);
+    ctx->gc.local_slabs = n;
+    return OSMPM_OK;
+}
+
 osmpm_status osmpm_subdomain_create(osmpm_ctx* ctx, const osmpm_grid_desc* grid, double dt,
                                     const osmpm_particles_view* particles, const osmpm_material* mats,
                                     int32_t n_mats, const double gravity[3], osmpm_precision prec,
                                     osmpm_subdomain** out)
+{
+    return osmpm_subdomain_create_ex(ctx, grid, dt, particles, mats, n_mats, gravity, prec, 1, out);
+}
+
+osmpm_status osmpm_subdomain_create_ex(osmpm_ctx* ctx, const osmpm_grid_desc* grid, double dt,
+                                       const osmpm_particles_view* particles, const osmpm_material* mats,
+                                       int32_t n_mats, const double gravity[3], osmpm_precision prec,
+                                       int32_t decompose, osmpm_subdomain** out)
 {
     CHECK_ARG(ctx && grid && particles && mats && out, "NULL argument");
     CHECK_ARG(grid->dim == 2 || grid->dim == 3, "dim = %d (must be 2 or 3)", grid->dim);
@@ -169,8 +213,17 @@ osmpm_status osmpm_subdomain_create(osmpm_ctx* ctx, const osmpm_grid_desc* grid,
     SET_DEVICE(ctx);
     osmpm_subdomain* s = nullptr;
     osmpm_status rc;
+    const bool dist = decompose && (ctx->gc.nranks > 1 || ctx->gc.local_slabs > 1);
 #define MAKE(DD, RR)                                                                                \
-    {                                                                                               \
+    if (dist) {                                                                                     \
+        auto* q = new Dist<DD, RR>();                                                               \
+        q->ctx = ctx;                                                                               \
+        q->dim = DD;                                                                                \
+        q->prec = prec;                                                                             \
+        q->decomposed = true;                                                                       \
+        s = q;                                                                                      \
+        rc = q->create(grid, dt, particles, mats, n_mats, gravity);                                 \
+    } else {                                                                                        \
         auto* q = new Sub<DD, RR>();                                                                \
         q->ctx = ctx;                                                                               \
         q->dim = DD;                                                                                \
@@ -273,6 +326,34 @@ osmpm_status osmpm_subdomain_info(osmpm_subdomain* sub, int64_t* n_particles, in
 }
 osmpm_status osmpm_sync(osmpm_subdomain* sub) { SUB_CALL(sub, sync()); }
 
+osmpm_status osmpm_subdomain_decomp(osmpm_subdomain* sub, int32_t* slabs_total, int32_t* slabs_local,
+                                    int32_t* first_slab, int64_t* n_local, int32_t* cuts)
+{
+    CHECK_ARG(sub, "subdomain is NULL");
+    SET_DEVICE(sub->ctx);
+    int32_t st = 1, sl = 1, fs = 0;
+    std::vector<int> cv;
+#define DEC(DD, RR)                                                                                 \
+    if (sub->dim == DD && sub->prec == (sizeof(RR) == 8 ? OSMPM_F64 : OSMPM_F32)) {                 \
+        auto* d = static_cast<Dist<DD, RR>*>(sub);                                                  \
+        st = d->nslab_total;                                                                        \
+        sl = (int32_t)d->sp.size();                                                                 \
+        fs = d->first_slab;                                                                         \
+        cv = d->cuts;                                                                               \
+    }
+    if (sub->decomposed) {
+        DEC(3, double) DEC(2, double) DEC(3, float) DEC(2, float)
+    }
+#undef DEC
+    if (slabs_total) *slabs_total = st;
+    if (slabs_local) *slabs_local = sl;
+    if (first_slab) *first_slab = fs;
+    if (cuts)
+        for (size_t k = 0; k < cv.size(); ++k) cuts[k] = cv[k];
+    if (n_local) return sub->info(n_local, nullptr, nullptr);
+    return OSMPM_OK;
+}
+
 osmpm_status osmpm_transmit(osmpm_subdomain* src, osmpm_subdomain* dst, osmpm_direction dir, double alpha,
                             double eps_tol, int64_t n_targets, const int64_t* targets, double* v_out,
                             osmpm_memspace space)
@@ -283,8 +364,17 @@ osmpm_status osmpm_transmit(osmpm_subdomain* src, osmpm_subdomain* dst, osmpm_di
     CHECK_ARG(n_targets >= 0, "n_targets < 0");
     SET_DEVICE(src->ctx);
 #define TR(DD, RR)                                                                                  \
-    return transmit_impl<DD, RR>(static_cast<Sub<DD, RR>*>(src), static_cast<Sub<DD, RR>*>(dst), dir, alpha,      \
-                                 eps_tol, n_targets, targets, v_out, space)
+    {                                                                                               \
+        using SubT = Sub<DD, RR>;                                                                   \
+        using DistT = Dist<DD, RR>;                                                                 \
+        SubT* s_sub = src->decomposed ? nullptr : static_cast<SubT*>(src);                          \
+        SubT* d_sub = dst->decomposed ? nullptr : static_cast<SubT*>(dst);                          \
+        SlabGroup<DD, RR> SG = src->decomposed ? static_cast<DistT*>(src)->group() : s_sub->self_group(); \
+        GridGeo geo = dst->decomposed ? geo_of(static_cast<DistT*>(dst)) : geo_of(d_sub);           \
+        const int64_t dn = dst->decomposed ? static_cast<DistT*>(dst)->dense_nodes() : d_sub->dense_nodes(); \
+        return transmit_impl<DD, RR>(SG, s_sub, d_sub, geo, dn, dir, alpha, eps_tol, n_targets, targets, v_out, \
+                                     space);                                                        \
+    }
     if (src->dim == 3 && src->prec == OSMPM_F64) TR(3, double);
     if (src->dim == 2 && src->prec == OSMPM_F64) TR(2, double);
     if (src->dim == 3) TR(3, float);
@@ -298,6 +388,9 @@ osmpm_status osmpm_coupler_create(osmpm_subdomain* coarse, osmpm_subdomain* fine
     CHECK_ARG(coarse && fine && settings && out, "NULL argument");
     CHECK_ARG(coarse->dim == fine->dim && coarse->prec == fine->prec, "coupler: subdomains differ in dim / precision");
     CHECK_ARG(coarse->ctx == fine->ctx, "coupler: subdomains belong to different contexts");
+    CHECK_ARG(!coarse->decomposed && !fine->decomposed,
+              "coupler: slab-decomposed subdomains are driven by the caller (osmpm_transmit / osmpm_implicit_solve), "
+              "not by the coupler");
     CHECK_ARG(settings->M >= 1, "M must be >= 1");
     SET_DEVICE(coarse->ctx);
     return coupler_create(coarse, fine, settings, out);

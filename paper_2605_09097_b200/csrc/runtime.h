@@ -93,6 +93,7 @@ struct osmpm_subdomain {
     osmpm_ctx* ctx = nullptr;
     int dim = 3;
     osmpm_precision prec = OSMPM_F64;
+    bool decomposed = false;  // a Dist (slab-decomposed) subdomain
     virtual ~osmpm_subdomain() {}
     virtual osmpm_status set_gravity(const double* g) = 0;
     virtual osmpm_status set_dt(double dt) = 0;

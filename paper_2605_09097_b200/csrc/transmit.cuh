@@ -44,11 +44,11 @@ struct GridGeo {
 
 // Pi numerator / denominator: every ACTIVE fine box node scatters m_j [v_j, 1] N_B,I(x_j)
 template <int D>
-__global__ void k_project(BoxDev fb, const uint8_t* __restrict__ act, const double* __restrict__ m,
+__global__ void k_project(BoxDev fb, int64_t nown, const uint8_t* __restrict__ act, const double* __restrict__ m,
                           const double* __restrict__ v, GridGeo cg, double* __restrict__ num, double* __restrict__ den)
 {
     int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= fb.nnodes || !act[j]) return;
+    if (j >= nown || !act[j]) return;  // ghost planes are projected by their owner
     int i2 = (D == 3) ? (int)(j % fb.nn[2]) : 0;
     int i1 = (D == 3) ? (int)((j / fb.nn[2]) % fb.nn[1]) : (int)(j % fb.nn[1]);
     int i0 = (D == 3) ? (int)(j / ((int64_t)fb.nn[2] * fb.nn[1])) : (int)(j / fb.nn[1]);
@@ -122,8 +122,8 @@ __global__ void k_interp(int64_t nt, const int64_t* __restrict__ targets, GridGe
     for (int a = 0; a < D; ++a) out[t * D + a] = (1.0 - alpha) * I0[a] + alpha * I1[a];
 }
 
-template <int D, typename R>
-static GridGeo geo_of(const Sub<D, R>* s)
+template <typename S>
+static GridGeo geo_of(const S* s)
 {
     GridGeo g{};
     for (int a = 0; a < 3; ++a) {
@@ -135,48 +135,70 @@ static GridGeo geo_of(const Sub<D, R>* s)
     return g;
 }
 
-// Pi over ALL coarse dense nodes: num (nnB*D), den (nnB) device buffers of the coarse side
+// Pi over ALL coarse dense nodes: num (nnB*D), den (nnB) device buffers of the coarse side.  The
+// fine side may be a group of slabs (each projects its owned nodes; sums all-reduced over ranks).
+template <int D, typename R>
+osmpm_status project_accumulate_group(SlabGroup<D, R> F, Sub<D, R>* coarse, bool use_solved, DBuf<double>& num,
+                                      DBuf<double>& den)
+{
+    cudaStream_t st = F.st;
+    const int64_t nnb = coarse->dense_nodes();
+    OSMPM_TRY(num.need(nnb * (D + 1)));
+    OSMPM_CU(cudaMemsetAsync(num.p, 0, nnb * (D + 1) * sizeof(double), st));
+    double* denp = num.p + nnb * D;  // num and den contiguous: one all-reduce
+    auto& pf = F.ctx->prof;
+    if (pf.on) pf.begin("transmit", st);
+    for (int i = 0; i < F.ns; ++i) {
+        Sub<D, R>* fine = F.s[i];
+        const double* v = use_solved ? fine->vnew.p : fine->vn.p;
+        fine->KC();
+        k_project<D><<<nblk_all(fine->box.nnodes, 256), 256, 0, st>>>(fine->box, fine->nown, fine->act.p, fine->m.p, v,
+                                                                      geo_of(coarse), num.p, denp);
+        OSMPM_LAUNCH_CHECK();
+    }
+    OSMPM_TRY(group_allreduce<D, R>(F, num.p, (int)(nnb * (D + 1))));
+    if (pf.on) pf.end("transmit", st);
+    (void)den;
+    return OSMPM_OK;
+}
 template <int D, typename R>
 osmpm_status project_accumulate(Sub<D, R>* fine, Sub<D, R>* coarse, bool use_solved, DBuf<double>& num,
                                 DBuf<double>& den)
 {
-    cudaStream_t st = fine->st();
+    OSMPM_TRY(project_accumulate_group<D, R>(fine->self_group(), coarse, use_solved, num, den));
+    // den as its own buffer for the coupler's host reads
     const int64_t nnb = coarse->dense_nodes();
-    OSMPM_TRY(num.need(nnb * D));
     OSMPM_TRY(den.need(nnb));
-    OSMPM_CU(cudaMemsetAsync(num.p, 0, nnb * D * sizeof(double), st));
-    OSMPM_CU(cudaMemsetAsync(den.p, 0, nnb * sizeof(double), st));
-    const double* v = use_solved ? fine->vnew.p : fine->vn.p;
-    if (fine->ctx->prof.on) fine->ctx->prof.begin("transmit", st);
-    fine->KC();
-    k_project<D><<<nblk_all(fine->box.nnodes, 256), 256, 0, st>>>(fine->box, fine->act.p, fine->m.p, v, geo_of(coarse),
-                                                                  num.p, den.p);
-    OSMPM_LAUNCH_CHECK();
-    if (fine->ctx->prof.on) fine->ctx->prof.end("transmit", st);
+    OSMPM_CU(cudaMemcpyAsync(den.p, num.p + nnb * D, nnb * sizeof(double), cudaMemcpyDeviceToDevice, fine->st()));
     return OSMPM_OK;
 }
 
+// src / dst: a standalone subdomain (Sub) or, on the fine side, a slab group.  FINE_TO_COARSE reads
+// the source's (group's) grid and writes coarse values; COARSE_TO_FINE reads the coarse source's grid
+// and only the destination's geometry.
 template <int D, typename R>
-osmpm_status transmit_impl(Sub<D, R>* src, Sub<D, R>* dst, osmpm_direction dir, double alpha, double eps,
-                           int64_t nt, const int64_t* targets, double* out, osmpm_memspace sp)
+osmpm_status transmit_impl(SlabGroup<D, R> SG, Sub<D, R>* src, Sub<D, R>* dstc, GridGeo dst_geo, int64_t dst_nodes,
+                           osmpm_direction dir, double alpha, double eps, int64_t nt, const int64_t* targets,
+                           double* out, osmpm_memspace sp)
 {
-    cudaStream_t st = src->st();
-    if (!src->have_grid) {
-        set_error("transmit: source subdomain has no grid (call osmpm_p2g)");
-        return OSMPM_E_STATE;
-    }
+    cudaStream_t st = SG.st;
+    for (int i = 0; i < SG.ns; ++i)
+        if (!SG.s[i]->have_grid) {
+            set_error("transmit: source subdomain has no grid (call osmpm_p2g)");
+            return OSMPM_E_STATE;
+        }
     if (alpha < 0.0 || alpha > 1.0) {
         set_error("transmit: alpha = %g outside [0, 1] (m > M, SPEC.md:330)", alpha);
         return OSMPM_E_INVALID_ARG;
     }
     const bool need_solved = alpha > 0.0;
-    if (need_solved && !src->have_vnew) {
-        set_error("transmit: alpha > 0 needs the source's solved grid velocity");
-        return OSMPM_E_STATE;
-    }
-    if (!targets && nt != dst->dense_nodes()) {
-        set_error("transmit: targets == NULL requires n_targets == dst node count (%lld)",
-                  (long long)dst->dense_nodes());
+    for (int i = 0; i < SG.ns; ++i)
+        if (need_solved && !SG.s[i]->have_vnew) {
+            set_error("transmit: alpha > 0 needs the source's solved grid velocity");
+            return OSMPM_E_STATE;
+        }
+    if (!targets && nt != dst_nodes) {
+        set_error("transmit: targets == NULL requires n_targets == dst node count (%lld)", (long long)dst_nodes);
         return OSMPM_E_INVALID_ARG;
     }
     DBuf<int64_t> tg;
@@ -197,18 +219,27 @@ osmpm_status transmit_impl(Sub<D, R>* src, Sub<D, R>* dst, osmpm_direction dir, 
             set_error("transmit FINE_TO_COARSE: alpha selects v^n (0) or v^{n+1} (1)");
             return OSMPM_E_INVALID_ARG;
         }
+        if (!dstc) {
+            set_error("transmit FINE_TO_COARSE: the coarse subdomain must not be decomposed");
+            return OSMPM_E_INVALID_ARG;
+        }
         DBuf<double> num, den;
-        OSMPM_TRY(project_accumulate(src, dst, alpha == 1.0, num, den));
+        OSMPM_TRY(project_accumulate_group<D, R>(SG, dstc, alpha == 1.0, num, den));
         if (nt > 0) {
-            src->KC();
-            k_project_out<D><<<nblk_all(nt, 256), 256, 0, st>>>(nt, tptr, num.p, den.p, eps, optr);
+            SG.ctx->launches++;
+            k_project_out<D><<<nblk_all(nt, 256), 256, 0, st>>>(nt, tptr, num.p, num.p + dstc->dense_nodes() * D, eps,
+                                                               optr);
             OSMPM_LAUNCH_CHECK();
         }
     } else {
+        if (!src) {
+            set_error("transmit COARSE_TO_FINE: the coarse subdomain must not be decomposed");
+            return OSMPM_E_INVALID_ARG;
+        }
         if (nt > 0) {
             if (src->ctx->prof.on) src->ctx->prof.begin("transmit", st);
             src->KC();
-            k_interp<D><<<nblk_all(nt, 256), 256, 0, st>>>(nt, tptr, geo_of(dst), src->box, src->vn.p,
+            k_interp<D><<<nblk_all(nt, 256), 256, 0, st>>>(nt, tptr, dst_geo, src->box, src->vn.p,
                                                            need_solved ? src->vnew.p : nullptr, alpha, optr);
             OSMPM_LAUNCH_CHECK();
             if (src->ctx->prof.on) src->ctx->prof.end("transmit", st);

@@ -92,6 +92,12 @@ def _check(rc):
         raise OsmpmError(rc, lib().osmpm_last_error().decode())
 
 
+def comm_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(lib().osmpm_comm_unique_id(buf))
+    return bytes(buf)
+
+
 def newton_settings(max_newton=50, max_cg=1000, fixed_iters=0, guess=0, newton_rtol=1e-8, newton_atol=0.0,
                     cg_rtol=1e-8, ls_min_alpha=2.0 ** -20, energy_noise_rtol=1e-13) -> NewtonSettings:
     return NewtonSettings(max_newton, max_cg, fixed_iters, guess, newton_rtol, newton_atol, cg_rtol, ls_min_alpha,
@@ -167,6 +173,17 @@ class Context:
         _check(lib().osmpm_kernel_time(self._h, family.encode(), C.byref(n), C.byref(ms)))
         return n.value, ms.value
 
+    def init_comm(self, rank, nranks, uid: bytes):
+        """Join the NCCL process group (one rank per GPU); uid from comm_unique_id() on rank 0."""
+        assert len(uid) == 128
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        _check(lib().osmpm_ctx_init_comm(self._h, C.c_int(rank), C.c_int(nranks), buf))
+        self.rank, self.nranks = rank, nranks
+
+    def set_local_slabs(self, n):
+        """Split each rank's share of decomposed subdomains into n slabs on this device."""
+        _check(lib().osmpm_ctx_set_local_slabs(self._h, C.c_int(n)))
+
     def launch_count(self):
         n = C.c_int64()
         _check(lib().osmpm_launch_count(self._h, C.byref(n)))
@@ -202,7 +219,9 @@ def grid_desc(grid) -> GridDesc:
 class Subdomain:
     """One MPM subdomain (§3.1) living on the context's GPU."""
 
-    def __init__(self, ctx: Context, grid, dt, particles, materials, gravity=(0.0, 0.0, 0.0), precision=F64):
+    def __init__(self, ctx: Context, grid, dt, particles, materials, gravity=(0.0, 0.0, 0.0), precision=F64,
+                 decompose=True):
+        """decompose: split into x-slabs over the ctx's process group / local slabs (if any)."""
         self.ctx = ctx
         ctx._children.append(weakref.ref(self))
         self.grid = grid
@@ -230,8 +249,9 @@ class Subdomain:
         mats = (Material * len(materials))(*[Material(float(E), float(nu)) for (E, nu) in materials])
         gvec = (C.c_double * 3)(*[float(g) for g in gravity[:3]])
         gd = grid_desc(grid)
-        _check(lib().osmpm_subdomain_create(ctx._h, C.byref(gd), C.c_double(dt), C.byref(view), mats,
-                                            C.c_int32(len(materials)), gvec, C.c_int(precision), C.byref(self._h)))
+        _check(lib().osmpm_subdomain_create_ex(ctx._h, C.byref(gd), C.c_double(dt), C.byref(view), mats,
+                                               C.c_int32(len(materials)), gvec, C.c_int(precision),
+                                               C.c_int32(1 if decompose else 0), C.byref(self._h)))
         self._keep = []
         self.n = n
         self.n_nodes = int(np.prod(grid.dims[: grid.dim]))
@@ -338,6 +358,14 @@ class Subdomain:
 
     def sync(self):
         _check(lib().osmpm_sync(self._h))
+
+    def decomp(self):
+        """(slabs_total, slabs_local, first_slab, n_local_particles, cuts)"""
+        st, sl, fs = C.c_int32(), C.c_int32(), C.c_int32()
+        nl = C.c_int64()
+        cuts = (C.c_int32 * 4096)()
+        _check(lib().osmpm_subdomain_decomp(self._h, C.byref(st), C.byref(sl), C.byref(fs), C.byref(nl), cuts))
+        return st.value, sl.value, fs.value, nl.value, [cuts[k] for k in range(st.value - 1)]
 
     def close(self):
         if self._h:
