@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prof", action="store_true", help="skip the per-kernel event timing (A/B of its overhead)")
     ap.add_argument("--cpu-cells", type=int, default=14, help="oracle sample cube side (cells)")
+    ap.add_argument("--slabs", type=int, default=1,
+                    help="x-slabs per GPU (>1: the decomposed path on one device, halo by device copies)")
     return ap.parse_args()
 
 
@@ -203,6 +205,35 @@ def run_reference(args, rank):
 # GPU arm
 # ------------------------------------------------------------------------------------------------
 
+# ------------------------------------------------------------------------------------------------
+# multi-GPU plumbing (one process per GPU): the library's NCCL communicator is
+# bootstrapped through torch.distributed; timings are the max over ranks
+# ------------------------------------------------------------------------------------------------
+
+def share_unique_id(dist, rank, make_uid):
+    """rank 0's 128-byte communicator id, broadcast to every rank."""
+    obj = [make_uid() if rank == 0 else None]
+    if dist is not None:
+        dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def max_over_ranks(dist, value, device):
+    import torch
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(dist, value, device):
+    import torch
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -226,14 +257,20 @@ def main():
     dev = torch.device("cuda", local_rank)
     stream = torch.cuda.current_stream(dev)
     ctx = osmpm.Context(local_rank, stream.cuda_stream)
+    if world > 1:
+        ctx.init_comm(rank, world, share_unique_id(dist, rank, osmpm.comm_unique_id))
+    if args.slabs > 1:
+        ctx.set_local_slabs(args.slabs)
     prec = osmpm.F64 if args.precision == "f64" else osmpm.F32
     word = 8 if args.precision == "f64" else 4
 
     fine, coarse, cvel, recv = build_workload(args.cells)
     n = fine.particles.n
     sub = osmpm.Subdomain(ctx, fine.grid, fine.dt, fine.particles, fine.materials, fine.gravity, precision=prec)
+    # the small coarse overlap grid is replicated on every rank (decompose=False)
     csub = osmpm.Subdomain(ctx, coarse.grid, coarse.dt, coarse.particles, coarse.materials, coarse.gravity,
-                           precision=prec)
+                           precision=prec, decompose=False)
+    slabs_total, _, _, n_local, cuts = sub.decomp()
     csub.p2g()
     cg = csub.read_grid(device=dev)
     # v_B^{n+1}: the smooth field advanced (scaled) in time -> distinct endpoint for T_m
@@ -259,8 +296,9 @@ def main():
     sub.p2g()  # (untimed) grid of the current state, for the active-node count of the roofline
     _, _, box_dims = sub.info()
     g = sub.read_grid(device=dev)
-    n_active = int(g["active"].sum().item())
+    n_active = int(g["active"].sum().item())  # this rank's owned nodes (decomposed reads)
     del g
+    _, _, _, n_local, _ = sub.decomp()
 
     clocks = ClockSampler(local_rank)
     ctx.profile(not args.no_prof)
@@ -283,10 +321,7 @@ def main():
     hv_n, hv_ms = ctx.kernel_time("hvp")
     fam = {f: ctx.kernel_time(f) for f in ("hvp", "grad", "energy", "p2g", "g2p", "sort", "cg", "transmit")}
     ctx.profile(False)
-    t = torch.tensor([ms], device=dev, dtype=torch.float64)
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = max_over_ranks(dist, ms, dev)
 
     # end-to-end through the public API with pinned host buffers (H2D inputs, D2H result)
     e2e = None
@@ -314,11 +349,11 @@ def main():
             e2e_step()
         f1.record(stream)
         torch.cuda.synchronize(dev)
-        te = torch.tensor([f0.elapsed_time(f1) / args.steps], device=dev, dtype=torch.float64)
-        if dist:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * n / (float(te.item()) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": float(te.item())}
+        te = max_over_ranks(dist, f0.elapsed_time(f1) / args.steps, dev)
+        # every rank uploads the full creation-order state (it keeps its own slab's particles) and
+        # reads back its own particles into a full-size buffer
+        e2e = {"value": n / (te * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d * world,
+               "d2h_bytes_per_step": d2h * world, "ms_per_step": te}
 
     if rank != 0:
         if dist:
@@ -327,7 +362,7 @@ def main():
         return
 
     peak, peak_kind = peaks()
-    hvp_bytes = hvp_algorithmic_bytes(n, n_active, word)
+    hvp_bytes = hvp_algorithmic_bytes(n_local, n_active, word)  # rank 0's share per launch
     hvp_avg_ms = hv_ms / hv_n if hv_n else float("nan")
     achieved = hvp_bytes / (hvp_avg_ms * 1e-3) / 1e9 if hv_n else None
     traffic = load_traffic(args.precision)
@@ -338,15 +373,19 @@ def main():
                "sample": f"one fine sub-step ({args.newton} Newton x {args.cg} PCG) of a {args.cpu_cells}^3-cell C5 "
                          f"cube ({ncpu} particles), {dt:.1f} s single-threaded"}
     line = {
-        "metric": METRIC, "value": world * n / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "metric": METRIC, "value": n / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
         "config": {"workload": "C5 (BASELINE.json configs[4]): random-density neo-Hookean cube, 128^3 cells at "
                                "dx=1/512, 8 ppc, one fine implicit sub-step (10 Newton x 50 PCG) with "
                                "coarse<->fine transmission to the dx=1/128 overlap grid",
-                   "particles_per_gpu": n, "cells": args.cells, "newton": args.newton, "cg": args.cg,
-                   "active_nodes": n_active, "box_nodes": int(np.prod(box_dims)), "receivers": int(recv.shape[0]),
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "particles": n, "particles_rank0": n_local, "cells": args.cells, "newton": args.newton,
+                   "cg": args.cg, "active_nodes_rank0": n_active, "box_nodes_rank0": int(np.prod(box_dims)),
+                   "receivers": int(recv.shape[0]),
+                   "parallelism": (f"x-slabs x{slabs_total} (NCCL over NVLink, {world} GPUs)" if world > 1
+                                   else (f"x-slabs x{slabs_total} on one GPU" if slabs_total > 1 else "single GPU")),
+                   "slab_cuts": cuts,
                    "l2": "working set (>3 GB) far larger than the 126 MB L2; no flush needed"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak if achieved else None,
                      "traffic": traffic, "kernel": "k_hvp", "peak_kind": peak_kind,

@@ -163,6 +163,11 @@ osmpm_status osmpm_launch_count(osmpm_ctx* ctx, int64_t* launches);
 osmpm_status osmpm_comm_unique_id(uint8_t id[128]);
 osmpm_status osmpm_ctx_init_comm(osmpm_ctx* ctx, int rank, int nranks, const uint8_t id[128]);
 osmpm_status osmpm_ctx_set_local_slabs(osmpm_ctx* ctx, int n);
+/* Host-only (no GPU needed): the slab cuts the decomposition uses for particles with base nodes
+ * base_x[n] along x: nslab - 1 increasing cell indices, on the lattice of `tile`-cell columns from the
+ * lowest base node, each at the column boundary whose prefix particle count is nearest k n / nslab
+ * (at least one column per slab).  INVALID_ARG if fewer columns than slabs. */
+osmpm_status osmpm_slab_cuts(const int32_t* base_x, int64_t n, int32_t nslab, int32_t tile, int32_t* cuts);
 /* slabs_total, slabs_local, first_slab (this rank's first global slab), n_local (particles on this
  * rank now), cuts[slabs_total - 1] (cell index along x where slab k+1 starts; may be NULL). */
 osmpm_status osmpm_subdomain_decomp(osmpm_subdomain* sub, int32_t* slabs_total, int32_t* slabs_local,

@@ -178,6 +178,19 @@ osmpm_status osmpm_ctx_init_comm(osmpm_ctx* ctx, int rank, int nranks, const uin
     return OSMPM_OK;
 }
 
+osmpm_status osmpm_slab_cuts(const int32_t* base_x, int64_t n, int32_t nslab, int32_t tile, int32_t* cuts)
+{
+    CHECK_ARG(nslab >= 1 && tile >= 1 && n >= 0 && (n == 0 || base_x) && (nslab == 1 || cuts), "bad arguments");
+    std::vector<int> bx(base_x, base_x + n);
+    std::vector<int> c = balanced_cuts(bx, nslab, tile);
+    if ((int)c.size() != nslab - 1) {
+        set_error("cannot cut %d slabs of %d-cell columns from %lld particles", nslab, tile, (long long)n);
+        return OSMPM_E_INVALID_ARG;
+    }
+    for (int k = 0; k + 1 < nslab; ++k) cuts[k] = c[k];
+    return OSMPM_OK;
+}
+
 osmpm_status osmpm_ctx_set_local_slabs(osmpm_ctx* ctx, int n)
 {
     CHECK_ARG(ctx, "ctx is NULL");
