@@ -255,7 +255,10 @@ def main():
     from paper_2605_09097_b200 import osmpm
 
     dev = torch.device("cuda", local_rank)
-    stream = torch.cuda.current_stream(dev)
+    # one explicit stream for torch's tensor work and every library launch / NCCL call: the CUDA
+    # events below then time exactly the library's work
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
     ctx = osmpm.Context(local_rank, stream.cuda_stream)
     if world > 1:
         ctx.init_comm(rank, world, share_unique_id(dist, rank, osmpm.comm_unique_id))

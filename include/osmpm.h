@@ -133,8 +133,10 @@ typedef struct {
 const char* osmpm_last_error(void);
 const char* osmpm_version(void);
 
-/* device: CUDA ordinal; cuda_stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)
- * or NULL for a library-created stream.  The ctx never destroys a caller-supplied stream. */
+/* device: CUDA ordinal; cuda_stream: the cudaStream_t all work is enqueued on (e.g.
+ * torch.cuda.current_stream().cuda_stream; pass cudaStreamLegacy for the legacy default stream),
+ * or NULL for a library-created non-blocking stream.  The ctx never destroys a caller-supplied
+ * stream. */
 osmpm_status osmpm_ctx_create(int device, void* cuda_stream, osmpm_ctx** out);
 void osmpm_ctx_destroy(osmpm_ctx* ctx);
 

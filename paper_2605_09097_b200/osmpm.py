@@ -155,8 +155,11 @@ def _empty_like_space(shape, dtype, device):
 
 class Context:
     def __init__(self, device=0, stream=None):
+        """stream: a cudaStream_t handle (e.g. torch.cuda.current_stream().cuda_stream) the library
+        enqueues all its work on, or None for a library-owned stream.  Handle 0 (torch's default
+        stream) is passed as cudaStreamLegacy so the work stays ordered with torch's."""
         self._h = C.c_void_p()
-        s = None if stream is None else C.c_void_p(stream)
+        s = None if stream is None else C.c_void_p(stream if stream != 0 else 1)  # 1 == cudaStreamLegacy
         _check(lib().osmpm_ctx_create(C.c_int(device), s, C.byref(self._h)))
         self.device = device
         self._children = []  # weakrefs to subdomains / couplers: destroyed before the context
