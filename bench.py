@@ -303,6 +303,9 @@ def main():
     del g
     _, _, _, n_local, _ = sub.decomp()
 
+    import gc
+    gc.collect()
+    gc.disable()  # no collector pauses inside the timed region (the step syncs with the host)
     clocks = ClockSampler(local_rank)
     ctx.profile(not args.no_prof)
     ctx.profile_reset()
@@ -358,6 +361,7 @@ def main():
         e2e = {"value": n / (te * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d * world,
                "d2h_bytes_per_step": d2h * world, "ms_per_step": te}
 
+    gc.enable()
     if rank != 0:
         if dist:
             dist.barrier()

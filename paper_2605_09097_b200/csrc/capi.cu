@@ -120,6 +120,8 @@ void osmpm_ctx_destroy(osmpm_ctx* ctx)
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->gc.comm) ncclCommDestroy(ctx->gc.comm);
+    for (void* p : ctx->scratch)
+        if (p) cudaFree(p);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

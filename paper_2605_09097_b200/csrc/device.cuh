@@ -13,9 +13,12 @@ namespace osmpm {
 // ---------------------------------------------------------------------------------------------
 // Inside a tile, cells are ordered LAYER-MAJOR along the last axis (z in 3D, y in 2D): a layer
 // is the LC = T0 (x T1) cells with one last-axis index; the tiled kernels walk the layers in order.
+#ifndef OSMPM_T2
+#define OSMPM_T2 8  // layers per 3D tile (cells along z)
+#endif
 template <int D> struct Tile;
 template <> struct Tile<3> {
-    static constexpr int T0 = 4, T1 = 4, T2 = 4;
+    static constexpr int T0 = 4, T1 = 4, T2 = OSMPM_T2;
     static constexpr int NC = T0 * T1 * T2;                   // cells per tile
     static constexpr int LC = T0 * T1;                        // cells per layer
     static constexpr int NL = T2;                             // layers per tile

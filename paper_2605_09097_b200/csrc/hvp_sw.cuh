@@ -25,9 +25,7 @@ namespace osmpm {
 
 template <int D> struct SW {
     using T = Tile<D>;
-    // padded last-axis stride of the node tile (3D: 7 nodes -> 224-B rows, 4 cells of a warp at bank
-    // groups 0, 24, 16, 8); 2D unpadded
-    static constexpr int NZP = (D == 3) ? T::N2 + 1 : T::N1;
+    static constexpr int NZP = (D == 3) ? T::N2 : T::N1;  // last-axis stride of the node tile
     static constexpr int NNP = (D == 3) ? T::N0 * T::N1 * NZP : T::N0 * T::N1;
     static constexpr int NLAT = (D == 3) ? T::N0 * T::N1 : T::N0;   // lateral nodes of a plane
     static constexpr int NSLOT = (D == 3) ? 9 : 3;                  // contributing cells per node
@@ -35,6 +33,10 @@ template <int D> struct SW {
     static constexpr int STG = NITEM * NSLOT;
     static constexpr int NACC = T::NACC;                            // 3D: (j, kk); 2D: kk
 };
+
+// reals per node of the node tile: 3D fp64 3 (24-B nodes; with 4x4xT2 tiles the rows of the four
+// cells of a warp's lanes start 4 banks apart: conflict-free 8-B loads), 3D fp32 4 (16-B nodes), 2D 2
+template <int D, typename R> struct SVS { static constexpr int S = (D == 3) ? (sizeof(R) == 8 ? 3 : 4) : 2; };
 
 template <int D>
 __device__ __forceinline__ int sw_node(int l0, int l1, int l2)
@@ -47,7 +49,7 @@ template <int D, typename R>
 constexpr size_t hvp_sw_smem_bytes()
 {
     using T = Tile<D>;
-    return 16 + ((size_t)SW<D>::NNP * SV<D>::S + SW<D>::STG + (size_t)HvpIn<D, R>::NF * HvpIn<D, R>::PFS +
+    return 16 + ((size_t)SW<D>::NNP * SVS<D, R>::S + SW<D>::STG + (size_t)HvpIn<D, R>::NF * HvpIn<D, R>::PFS +
                  (size_t)HvpRec<D, R>::RS * T::NT) *
                     sizeof(R);
 }
@@ -61,7 +63,8 @@ __device__ __forceinline__ void sw_gather(const R* sv, const int* lc, const R (*
 #pragma unroll
     for (int k = 0; k < D * D; ++k) gd[k] = R(0);
     if (D == 3) {
-        const R* base = sv + sw_node<D>(lc[0], lc[1], lc[2]) * 4;
+        constexpr int NS = SVS<D, R>::S;
+        const R* base = sv + sw_node<D>(lc[0], lc[1], lc[2]) * NS;
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
             R U0[3] = {0, 0, 0}, U1[3] = {0, 0, 0}, U2[3] = {0, 0, 0};
@@ -70,9 +73,17 @@ __device__ __forceinline__ void sw_gather(const R* sv, const int* lc, const R (*
                 R T0[3] = {0, 0, 0}, T1[3] = {0, 0, 0};
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
-                    const R* sp = base + ((i * T::N1 + j) * SW<D>::NZP + k) * 4;
-                    const V2 v01 = *reinterpret_cast<const V2*>(sp);
-                    const R s[3] = {v01.x, v01.y, sp[2]};
+                    const R* sp = base + ((i * T::N1 + j) * SW<D>::NZP + k) * NS;
+                    R s[3];
+                    if constexpr (NS == 4) {
+                        const V2 v01 = *reinterpret_cast<const V2*>(sp);
+                        s[0] = v01.x;
+                        s[1] = v01.y;
+                    } else {
+                        s[0] = sp[0];
+                        s[1] = sp[1];
+                    }
+                    s[2] = sp[2];
 #pragma unroll
                     for (int a = 0; a < 3; ++a) {
                         T0[a] = fma(s[a], w[2][k], T0[a]);
@@ -177,7 +188,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
     R* sv = reinterpret_cast<R*>(smem_raw + 16);
-    R* stg = sv + S::NNP * SV<D>::S;
+    R* stg = sv + S::NNP * SVS<D, R>::S;
     R* pf = stg + S::STG;
     R* rec = pf + In::NF * In::PFS;
     const int tile = blockIdx.x;
@@ -203,7 +214,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
         int c[3];
         tnode_coords<D>(l, c);
         const int64_t g = box_node<D>(b, t[0] * T::T0 + c[0], t[1] * T::T1 + c[1], t[2] * T::T2 + c[2]);
-        sv[sw_node<D>(c[0], c[1], c[2]) * SV<D>::S + a] = (R)din[g * D + a];
+        sv[sw_node<D>(c[0], c[1], c[2]) * SVS<D, R>::S + a] = (R)din[g * D + a];
     }
     for (int k = threadIdx.x; k < S::STG; k += T::NT) stg[k] = R(0);
     __syncthreads();

@@ -87,6 +87,21 @@ struct osmpm_ctx {
     int num_sms = 148;
     int64_t launches = 0;  // kernels launched through this ctx (bench gpu_launches)
     osmpm::GroupComm gc;
+    // grow-only device scratch of the per-call operators (transmit): no cudaMalloc / cudaFree (an
+    // implicit device synchronisation) inside a time step
+    void* scratch[4] = {nullptr, nullptr, nullptr, nullptr};
+    size_t scratch_cap[4] = {0, 0, 0, 0};
+    void* get_scratch(int k, size_t bytes)
+    {
+        if (scratch_cap[k] < bytes) {
+            if (scratch[k]) cudaFree(scratch[k]);
+            scratch[k] = nullptr;
+            scratch_cap[k] = 0;
+            if (cudaMalloc(&scratch[k], bytes + bytes / 8) != cudaSuccess) return nullptr;
+            scratch_cap[k] = bytes + bytes / 8;
+        }
+        return scratch[k];
+    }
 };
 
 struct osmpm_subdomain {

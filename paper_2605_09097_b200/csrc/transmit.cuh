@@ -138,14 +138,12 @@ static GridGeo geo_of(const S* s)
 // Pi over ALL coarse dense nodes: num (nnB*D), den (nnB) device buffers of the coarse side.  The
 // fine side may be a group of slabs (each projects its owned nodes; sums all-reduced over ranks).
 template <int D, typename R>
-osmpm_status project_accumulate_group(SlabGroup<D, R> F, Sub<D, R>* coarse, bool use_solved, DBuf<double>& num,
-                                      DBuf<double>& den)
+osmpm_status project_accumulate_group(SlabGroup<D, R> F, Sub<D, R>* coarse, bool use_solved, double* num)
 {
     cudaStream_t st = F.st;
     const int64_t nnb = coarse->dense_nodes();
-    OSMPM_TRY(num.need(nnb * (D + 1)));
-    OSMPM_CU(cudaMemsetAsync(num.p, 0, nnb * (D + 1) * sizeof(double), st));
-    double* denp = num.p + nnb * D;  // num and den contiguous: one all-reduce
+    OSMPM_CU(cudaMemsetAsync(num, 0, nnb * (D + 1) * sizeof(double), st));
+    double* denp = num + nnb * D;  // num and den contiguous: one all-reduce
     auto& pf = F.ctx->prof;
     if (pf.on) pf.begin("transmit", st);
     for (int i = 0; i < F.ns; ++i) {
@@ -153,21 +151,21 @@ osmpm_status project_accumulate_group(SlabGroup<D, R> F, Sub<D, R>* coarse, bool
         const double* v = use_solved ? fine->vnew.p : fine->vn.p;
         fine->KC();
         k_project<D><<<nblk_all(fine->box.nnodes, 256), 256, 0, st>>>(fine->box, fine->nown, fine->act.p, fine->m.p, v,
-                                                                      geo_of(coarse), num.p, denp);
+                                                                      geo_of(coarse), num, denp);
         OSMPM_LAUNCH_CHECK();
     }
-    OSMPM_TRY(group_allreduce<D, R>(F, num.p, (int)(nnb * (D + 1))));
+    OSMPM_TRY(group_allreduce<D, R>(F, num, (int)(nnb * (D + 1))));
     if (pf.on) pf.end("transmit", st);
-    (void)den;
     return OSMPM_OK;
 }
 template <int D, typename R>
 osmpm_status project_accumulate(Sub<D, R>* fine, Sub<D, R>* coarse, bool use_solved, DBuf<double>& num,
                                 DBuf<double>& den)
 {
-    OSMPM_TRY(project_accumulate_group<D, R>(fine->self_group(), coarse, use_solved, num, den));
-    // den as its own buffer for the coupler's host reads
     const int64_t nnb = coarse->dense_nodes();
+    OSMPM_TRY(num.need(nnb * (D + 1)));
+    OSMPM_TRY(project_accumulate_group<D, R>(fine->self_group(), coarse, use_solved, num.p));
+    // den as its own buffer for the coupler's host reads
     OSMPM_TRY(den.need(nnb));
     OSMPM_CU(cudaMemcpyAsync(den.p, num.p + nnb * D, nnb * sizeof(double), cudaMemcpyDeviceToDevice, fine->st()));
     return OSMPM_OK;
@@ -201,18 +199,18 @@ osmpm_status transmit_impl(SlabGroup<D, R> SG, Sub<D, R>* src, Sub<D, R>* dstc, 
         set_error("transmit: targets == NULL requires n_targets == dst node count (%lld)", (long long)dst_nodes);
         return OSMPM_E_INVALID_ARG;
     }
-    DBuf<int64_t> tg;
+    osmpm_ctx* cx = SG.ctx;
     const int64_t* tptr = targets;
     if (targets && sp == OSMPM_HOST) {
-        OSMPM_TRY(tg.need(nt));
-        OSMPM_CU(cudaMemcpyAsync(tg.p, targets, nt * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-        tptr = tg.p;
+        int64_t* tg = (int64_t*)cx->get_scratch(0, nt * sizeof(int64_t));
+        if (!tg) return OSMPM_E_OOM;
+        OSMPM_CU(cudaMemcpyAsync(tg, targets, nt * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        tptr = tg;
     }
-    DBuf<double> ob;
     double* optr = out;
     if (sp == OSMPM_HOST) {
-        OSMPM_TRY(ob.need(nt * D));
-        optr = ob.p;
+        optr = (double*)cx->get_scratch(1, nt * D * sizeof(double));
+        if (!optr) return OSMPM_E_OOM;
     }
     if (dir == OSMPM_FINE_TO_COARSE) {
         if (alpha != 0.0 && alpha != 1.0) {
@@ -223,11 +221,12 @@ osmpm_status transmit_impl(SlabGroup<D, R> SG, Sub<D, R>* src, Sub<D, R>* dstc, 
             set_error("transmit FINE_TO_COARSE: the coarse subdomain must not be decomposed");
             return OSMPM_E_INVALID_ARG;
         }
-        DBuf<double> num, den;
-        OSMPM_TRY(project_accumulate_group<D, R>(SG, dstc, alpha == 1.0, num, den));
+        double* num = (double*)cx->get_scratch(2, dstc->dense_nodes() * (D + 1) * sizeof(double));
+        if (!num) return OSMPM_E_OOM;
+        OSMPM_TRY(project_accumulate_group<D, R>(SG, dstc, alpha == 1.0, num));
         if (nt > 0) {
             SG.ctx->launches++;
-            k_project_out<D><<<nblk_all(nt, 256), 256, 0, st>>>(nt, tptr, num.p, num.p + dstc->dense_nodes() * D, eps,
+            k_project_out<D><<<nblk_all(nt, 256), 256, 0, st>>>(nt, tptr, num, num + dstc->dense_nodes() * D, eps,
                                                                optr);
             OSMPM_LAUNCH_CHECK();
         }
@@ -247,8 +246,8 @@ osmpm_status transmit_impl(SlabGroup<D, R> SG, Sub<D, R>* src, Sub<D, R>* dstc, 
     }
     if (sp == OSMPM_HOST) {
         OSMPM_CU(cudaMemcpyAsync(out, optr, nt * D * sizeof(double), cudaMemcpyDeviceToHost, st));
+        OSMPM_CU(cudaStreamSynchronize(st));
     }
-    OSMPM_CU(cudaStreamSynchronize(st));
     return OSMPM_OK;
 }
 

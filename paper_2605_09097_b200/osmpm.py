@@ -14,7 +14,7 @@ import weakref
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libosmpm.so")
+LIB_PATH = os.environ.get("OSMPM_LIB", os.path.join(_HERE, "libosmpm.so"))  # OSMPM_LIB: A/B builds
 
 OK = 0
 HOST, DEVICE = 0, 1
