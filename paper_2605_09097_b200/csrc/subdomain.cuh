@@ -7,6 +7,7 @@
 #include <type_traits>
 #include <cmath>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "kernels.cuh"
@@ -479,7 +480,20 @@ struct Sub : public osmpm_subdomain {
         OSMPM_CU(cudaMemsetAsync(mom.p, 0, nn * D * sizeof(double), st()));
         OSMPM_CU(cudaMemsetAsync(fsig.p, 0, nn * D * sizeof(double), st()));
         if (n > 0) {
-            KC(); k_p2g<D, R><<<nblk_all(n, 128), 128, 0, st()>>>(P.p, cap, n, mat.p, box, mats, m.p, mom.p, fsig.p);
+            // tiled P2G (p2g_tiled.cuh); OSMPM_P2G=atomic selects the per-particle scatter for A/B
+            static const bool atomic_p2g = getenv("OSMPM_P2G") && std::string(getenv("OSMPM_P2G")) == "atomic";
+            if (atomic_p2g) {
+                KC(); k_p2g<D, R><<<nblk_all(n, 128), 128, 0, st()>>>(P.p, cap, n, mat.p, box, mats, m.p, mom.p, fsig.p);
+            } else {
+                static bool attr = false;
+                if (!attr) {
+                    cudaFuncSetAttribute(k_p2g_tiled<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)p2g_tiled_smem_bytes<D, R>());
+                    attr = true;
+                }
+                KC(); k_p2g_tiled<D, R><<<box.ntiles, T::NT, p2g_tiled_smem_bytes<D, R>(), st()>>>(
+                    P.p, cap, mat.p, cell_start.p, box, mats, m.p, mom.p, fsig.p);
+            }
             OSMPM_LAUNCH_CHECK();
         }
         return OSMPM_OK;
