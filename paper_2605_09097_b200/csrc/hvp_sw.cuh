@@ -23,6 +23,10 @@
 
 namespace osmpm {
 
+#ifndef OSMPM_SW_UNROLL
+#define OSMPM_SW_UNROLL 4
+#endif
+
 template <int D> struct SW {
     using T = Tile<D>;
     static constexpr int NZP = (D == 3) ? T::N2 : T::N1;  // last-axis stride of the node tile
@@ -298,7 +302,13 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                 }
                 if (it < T::ITEMS) {
                     const int p0 = max(ks, sb), p1 = min(ke, se);
+#ifdef OSMPM_SW_NOROT
+                    const int len = p1 - p0, rot = 0;
+#else
                     const int len = p1 - p0, rot = len > 0 ? (icell & 7) % len : 0;
+#endif
+                    constexpr int kUnroll = OSMPM_SW_UNROLL;  // 4 (measured: 2 / 8 slower)
+#pragma unroll kUnroll
                     for (int k = 0; k < len; ++k) {
                         const RecPtr<R> r(rec, rotated(p0, len, k, rot) - sb, RS);
                         ItemW<D, R> W;
