@@ -1,0 +1,229 @@
+// grad_sw.cuh -- sliding-window tiled Newton gradient + energy + Jacobi diagonal + linearisation
+// cache (a4), the default gradient kernel; same arithmetic as k_grad (tiled.cuh):
+//   M = I + grad u, F(u) = M F^n, J = det M det F^n,  Ah = M^{-T},  S' = V0 mu F^n F^nT
+//   G_grad = V0 P(F(u)) F^nT = M S' - c' Ah ;  diag_a += gradN^T (S' + (c' + l') Ah_a Ah_a^T) gradN
+//   V0 Psi = 1/2 (tr(M S' M^T) - V0 mu d) - V0 mu ln J + V0 lam/2 ln^2 J
+// (PAPER.md:151-164 Eq. discrete_energy, 186-191 Eq. F_update, 205-210 Newton).
+// Structure of k_hvp_sw (hvp_sw.cuh): per layer, phase 1 (thread per particle) with the particle
+// inputs x, F^n, V0 streamed by TMA bulk copies, phase 2 (thread per (cell, a, i)) accumulating the
+// gradient and the diagonal in two 3-plane register windows, plane-wise staged fixed-order sums and
+// one fp64 RED per node; fp64 arithmetic for every particle precision (R14).
+#pragma once
+#include "hvp_sw.cuh"
+
+namespace osmpm {
+
+template <int D, typename R> struct GradIn {
+    static constexpr int NF = D + D * D + 1;  // x, F^n, V0
+    static constexpr int UE = 16 / sizeof(R);
+    static constexpr int PFS = Tile<D>::NT + 2 * UE;
+    __device__ static int field(int f) { return f < D ? PL<D>::X + f : (f < D + D * D ? PL<D>::F + f - D : PL<D>::VOL); }
+};
+
+template <int D, typename R>
+constexpr size_t grad_sw_smem_bytes()
+{
+    using T = Tile<D>;
+    return 16 + ((size_t)SW<D>::NNP * SVS<D, double>::S + 2 * SW<D>::STG + (size_t)GradRec<D>::RS * T::NT) *
+                    sizeof(double) +
+           (size_t)GradIn<D, R>::NF * GradIn<D, R>::PFS * sizeof(R);
+}
+
+template <int D, typename R>
+__device__ __forceinline__ void grad_prefetch(const R* __restrict__ P, int64_t cap, int lb, int le, R* pf, uint64_t* bar,
+                                              int lane)
+{
+    using In = GradIn<D, R>;
+    static_assert(In::NF <= 32, "one field per lane");
+    const int lb0 = lb & ~(In::UE - 1);
+    const int cnt = min(le, lb + Tile<D>::NT) - lb0;
+    const uint32_t bytes = (uint32_t)((cnt + In::UE - 1) & ~(In::UE - 1)) * sizeof(R);
+    fence_async_smem();
+    if (lane == 0) mbar_expect_tx(bar, bytes * In::NF);
+    __syncwarp();
+    if (lane < In::NF) bulk_g2s(pf + lane * In::PFS, P + (int64_t)In::field(lane) * cap + lb0, bytes, bar);
+}
+
+template <int D, typename R>
+__global__ void __launch_bounds__(Tile<D>::NT, 2)
+k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int* __restrict__ mat,
+          const int* __restrict__ cell_start, BoxDev b, MatTable mt, const double* __restrict__ uin,
+          double* __restrict__ gout, double* __restrict__ dout, double* __restrict__ partials)
+{
+    using T = Tile<D>;
+    using GR = GradRec<D>;
+    using C = CL<D>;
+    using In = GradIn<D, R>;
+    using S = SW<D>;
+    using Rd = double;
+    constexpr int RS = GR::RS;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+    Rd* sv = reinterpret_cast<Rd*>(smem_raw + 16);
+    Rd* stg = sv + S::NNP * SVS<D, Rd>::S;
+    Rd* stgd = stg + S::STG;
+    Rd* rec = stgd + S::STG;
+    R* pf = reinterpret_cast<R*>(rec + RS * T::NT);
+    const int tile = blockIdx.x;
+    const int64_t kt = (int64_t)tile * T::NC;
+    double red[3] = {0.0, 0.0, 0.0};
+    __shared__ int scs[T::NC + 1];
+    for (int i = threadIdx.x; i <= T::NC; i += T::NT) scs[i] = cell_start[kt + i];
+    __syncthreads();
+    if (scs[0] == scs[T::NC]) {
+        if (threadIdx.x == 0) partials[blockIdx.x * 3 + 0] = partials[blockIdx.x * 3 + 1] = partials[blockIdx.x * 3 + 2] = 0.0;
+        return;
+    }
+    auto layer_empty = [&](int l) { return scs[l * T::LC] == scs[(l + 1) * T::LC]; };
+    int first = 0;
+    while (layer_empty(first)) ++first;
+    if (threadIdx.x < 32) {
+        if (threadIdx.x == 0) mbar_init(bar, 1);
+        __syncwarp();
+        grad_prefetch<D, R>(P, cap, scs[first * T::LC], scs[(first + 1) * T::LC], pf, bar, threadIdx.x);
+    }
+    int t[3];
+    tile_coords<D>(b, tile, t);
+    for (int idx = threadIdx.x; idx < T::NN * D; idx += T::NT) {
+        const int a = idx % D, l = idx / D;
+        int c[3];
+        tnode_coords<D>(l, c);
+        const int64_t g = box_node<D>(b, t[0] * T::T0 + c[0], t[1] * T::T1 + c[1], t[2] * T::T2 + c[2]);
+        sv[sw_node<D>(c[0], c[1], c[2]) * SVS<D, Rd>::S + a] = uin[g * D + a];
+    }
+    for (int k = threadIdx.x; k < 2 * S::STG; k += T::NT) stg[k] = 0.0;
+    __syncthreads();
+    const int it = threadIdx.x;
+    const int icell = it / (D * 3), icomp = (it / 3) % D, ii = it % 3;
+    uint32_t parity = 0;
+    Rd acc[S::NACC], accd[S::NACC];
+#pragma unroll
+    for (int k = 0; k < S::NACC; ++k) acc[k] = accd[k] = 0.0;
+    for (int layer = 0; layer < T::NL + 2; ++layer) {
+        if (layer < T::NL && !layer_empty(layer)) {
+            const int lb = scs[layer * T::LC], le = scs[(layer + 1) * T::LC];
+            int next = layer + 1;
+            while (next < T::NL && layer_empty(next)) ++next;
+            const int pf_base = lb & ~(In::UE - 1);
+            const int ks = scs[layer * T::LC + icell];
+            const int ke = scs[layer * T::LC + icell + 1];
+            for (int sb = lb; sb < le; sb += T::NT) {
+                const int se = min(sb + T::NT, le);
+                const int q = threadIdx.x, p = sb + q;
+                const bool from_pf = (sb == lb);
+                if (sb != lb) __syncthreads();
+                if (from_pf) mbar_wait(bar, parity);
+                if (p < se) {
+                    const R* s = pf + (p - pf_base);
+                    auto in = [&](int f) -> Rd {
+                        return (Rd)(from_pf ? s[f * In::PFS] : P[(int64_t)In::field(f) * cap + p]);
+                    };
+                    Rd x[3], w[3][3], dw[3][3];
+                    int lc[3] = {0, 0, 0};
+#pragma unroll
+                    for (int a = 0; a < D; ++a) x[a] = in(a);
+                    weights_at<D, Rd>(x, b, t, lc, w, dw);
+                    const RecPtr<Rd> r(rec, q, RS);
+                    store_weights<D, Rd>(r, w, dw);
+                    Rd Mx[D * D];
+                    sw_gather<D, Rd>(sv, lc, w, dw, Mx);
+#pragma unroll
+                    for (int a = 0; a < D; ++a) Mx[a * D + a] += 1.0;
+                    Rd Fn[D * D];
+#pragma unroll
+                    for (int k = 0; k < D * D; ++k) Fn[k] = in(D + k);
+                    const Rd V0 = in(D + D * D);
+                    const int mid = mat[p];
+                    const Rd mu = mt.mu[mid], lam = mt.lam[mid];
+                    Rd Sm[Sym<D>::N];
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+#pragma unroll
+                        for (int bb = a; bb < D; ++bb) {
+                            Rd sm = 0;
+#pragma unroll
+                            for (int k = 0; k < D; ++k) sm = fma(Fn[a * D + k], Fn[bb * D + k], sm);
+                            Sm[sym_idx<D>(a, bb)] = V0 * mu * sm;
+                        }
+                    const Rd detM = det<D, Rd>(Mx), detFn = det<D, Rd>(Fn);
+                    Rd Ah[D * D];
+                    cofactor<D, Rd>(Mx, Ah);
+                    const Rd invdet = 1.0 / detM;
+#pragma unroll
+                    for (int k = 0; k < D * D; ++k) Ah[k] *= invdet;
+                    const bool ok = detM > 0.0 && detFn > 0.0;
+                    const Rd lnJ = ok ? log(detM) + log(detFn) : 0.0;
+                    const Rd cc = V0 * (mu - lam * lnJ), ll = V0 * lam;
+                    Rd trMSM = 0;
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+#pragma unroll
+                        for (int bb = 0; bb < D; ++bb) {
+                            Rd sm = 0;
+#pragma unroll
+                            for (int k = 0; k < D; ++k) sm = fma(Mx[a * D + k], Sm[sym_idx<D>(k, bb)], sm);
+                            trMSM = fma(sm, Mx[a * D + bb], trMSM);
+                            *r.at(Rec<D>::G + a * D + bb) = fma(-cc, Ah[a * D + bb], sm);
+                        }
+                    const Rd psiV = 0.5 * (trMSM - V0 * mu * D) - V0 * mu * lnJ + 0.5 * V0 * lam * lnJ * lnJ;
+                    red[0] += psiV;
+                    red[1] += fabs(psiV);
+                    if (!ok) red[2] += 1.0;
+#pragma unroll
+                    for (int k = 0; k < Sym<D>::N; ++k) {
+                        *r.at(GR::S + k) = Sm[k];
+                        cache[(C::S + k) * cap + p] = (R)Sm[k];
+                    }
+#pragma unroll
+                    for (int k = 0; k < D * D; ++k) {
+                        *r.at(GR::A + k) = Ah[k];
+                        cache[(C::A + k) * cap + p] = (R)Ah[k];
+                    }
+                    cache[C::C * cap + p] = (R)cc;
+                    cache[C::L * cap + p] = (R)ll;
+                    *r.at(GR::CL) = cc + ll;
+                }
+                __syncthreads();  // records ready; the streamed buffer is free
+                if (from_pf) {
+                    parity ^= 1u;
+                    if (threadIdx.x < 32 && next < T::NL)
+                        grad_prefetch<D, R>(P, cap, scs[next * T::LC], scs[(next + 1) * T::LC], pf, bar, threadIdx.x);
+                }
+                if (it < T::ITEMS) {
+                    const int p0 = max(ks, sb), p1 = min(ke, se);
+                    const int len = p1 - p0, rot = len > 0 ? (icell & 7) % len : 0;
+                    for (int k = 0; k < len; ++k) {
+                        const RecPtr<Rd> r(rec, rotated(p0, len, k, rot) - sb, RS);
+                        ItemW<D, Rd> W;
+                        W.load(r, ii);
+                        Rd sg[D], Ar[D], Q[Sym<D>::N];
+#pragma unroll
+                        for (int bb = 0; bb < D; ++bb) {
+                            sg[bb] = *r.at(Rec<D>::G + icomp * D + bb);
+                            Ar[bb] = *r.at(GR::A + icomp * D + bb);
+                        }
+                        const Rd clv = *r.at(GR::CL);
+#pragma unroll
+                        for (int a = 0; a < D; ++a)
+#pragma unroll
+                            for (int bb = a; bb < D; ++bb)
+                                Q[sym_idx<D>(a, bb)] = fma(clv * Ar[a], Ar[bb], *r.at(GR::S + sym_idx<D>(a, bb)));
+                        item_linear<D, Rd>(sg, W, acc);
+                        item_quadratic<D, Rd>(Q, W, accd);
+                    }
+                }
+            }
+        }
+        if (it < T::ITEMS) {
+            sw_emit<D, Rd>(icell, icomp, ii, acc, stg);
+            sw_emit<D, Rd>(icell, icomp, ii, accd, stgd);
+        }
+        __syncthreads();
+        sw_flush<D, Rd>(b, t, layer, stg, gout);
+        sw_flush<D, Rd>(b, t, layer, stgd, dout);
+        if (layer + 1 >= T::NL || layer_empty(layer + 1)) __syncthreads();
+    }
+    block_reduce_store<3>(red, partials);
+}
+
+}  // namespace osmpm

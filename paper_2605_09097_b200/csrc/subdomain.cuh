@@ -618,8 +618,21 @@ struct Sub : public osmpm_subdomain {
             cudaFuncSetAttribute(k_hvp<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hvp_smem());
             attr = true;
         }
-        KC(); k_grad<D, R><<<box.ntiles, T::NT, grad_smem(), st()>>>(P.p, cache.p, cap, mat.p, cell_start.p, box, mats,
-                                                                   uu, g.p, dg.p, partA);
+        // sliding-window gradient (grad_sw.cuh); OSMPM_GRAD=tiled selects k_grad for A/B
+        static const bool tiled_grad = getenv("OSMPM_GRAD") && std::string(getenv("OSMPM_GRAD")) == "tiled";
+        if (tiled_grad) {
+            KC(); k_grad<D, R><<<box.ntiles, T::NT, grad_smem(), st()>>>(P.p, cache.p, cap, mat.p, cell_start.p, box,
+                                                                       mats, uu, g.p, dg.p, partA);
+        } else {
+            static bool attr_sw = false;
+            if (!attr_sw) {
+                cudaFuncSetAttribute(k_grad_sw<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)grad_sw_smem_bytes<D, R>());
+                attr_sw = true;
+            }
+            KC(); k_grad_sw<D, R><<<box.ntiles, T::NT, grad_sw_smem_bytes<D, R>(), st()>>>(
+                P.p, cache.p, cap, mat.p, cell_start.p, box, mats, uu, g.p, dg.p, partA);
+        }
         OSMPM_LAUNCH_CHECK();
         return OSMPM_OK;
     }
