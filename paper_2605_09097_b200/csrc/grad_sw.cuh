@@ -227,3 +227,74 @@ k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int
 }
 
 }  // namespace osmpm
+
+namespace osmpm {
+
+// a7: line-search energy sum_p V0 Psi(F_p(u)), tiled: one CTA per tile stages u on the
+// tile's nodes in shared memory and evaluates Psi for the tile's (contiguous) particles; per-CTA
+// partials {sum V0 Psi, sum V0 |Psi|, inverted}.  Same formula as k_energy.
+template <int D, typename R>
+__global__ void __launch_bounds__(Tile<D>::NT)
+k_energy_tiled(const R* __restrict__ P, int64_t cap, const int* __restrict__ mat, const int* __restrict__ cell_start,
+               BoxDev b, MatTable mt, const double* __restrict__ u, double* __restrict__ partials)
+{
+    using T = Tile<D>;
+    using L = PL<D>;
+    __shared__ double sv[SW<D>::NNP * SVS<D, double>::S];
+    const int tile = blockIdx.x;
+    const int64_t kt = (int64_t)tile * T::NC;
+    const int p_lo = cell_start[kt], p_hi = cell_start[kt + T::NC];
+    double red[3] = {0.0, 0.0, 0.0};
+    if (p_lo == p_hi) {
+        if (threadIdx.x == 0) partials[blockIdx.x * 3 + 0] = partials[blockIdx.x * 3 + 1] = partials[blockIdx.x * 3 + 2] = 0.0;
+        return;
+    }
+    int t[3];
+    tile_coords<D>(b, tile, t);
+    for (int idx = threadIdx.x; idx < T::NN * D; idx += T::NT) {
+        const int a = idx % D, l = idx / D;
+        int c[3];
+        tnode_coords<D>(l, c);
+        const int64_t g = box_node<D>(b, t[0] * T::T0 + c[0], t[1] * T::T1 + c[1], t[2] * T::T2 + c[2]);
+        sv[sw_node<D>(c[0], c[1], c[2]) * SVS<D, double>::S + a] = u[g * D + a];
+    }
+    __syncthreads();
+    for (int p = p_lo + threadIdx.x; p < p_hi; p += T::NT) {
+        double x[3], w[3][3], dw[3][3], Mx[D * D];
+        int lc[3] = {0, 0, 0};
+#pragma unroll
+        for (int a = 0; a < D; ++a) x[a] = (double)P[(L::X + a) * cap + p];
+        weights_at<D, double>(x, b, t, lc, w, dw);
+        sw_gather<D, double>(sv, lc, w, dw, Mx);
+#pragma unroll
+        for (int a = 0; a < D; ++a) Mx[a * D + a] += 1.0;
+        double Fn[D * D];
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) Fn[k] = (double)P[(L::F + k) * cap + p];
+        const double V0 = (double)P[L::VOL * cap + p];
+        const int mid = mat[p];
+        const double mu = mt.mu[mid], lam = mt.lam[mid];
+        const double detM = det<D, double>(Mx), detFn = det<D, double>(Fn);
+        if (!(detM > 0.0 && detFn > 0.0)) {
+            red[2] += 1.0;
+            continue;
+        }
+        const double lnJ = log(detM) + log(detFn);
+        double tr = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int bb = 0; bb < D; ++bb) {
+                double s = 0.0;
+#pragma unroll
+                for (int k = 0; k < D; ++k) s += Mx[a * D + k] * Fn[k * D + bb];
+                tr += s * s;  // |M F^n|_F^2 = tr(M S M^T)
+            }
+        const double psiV = V0 * (0.5 * mu * (tr - D) - mu * lnJ + 0.5 * lam * lnJ * lnJ);
+        red[0] += psiV;
+        red[1] += fabs(psiV);
+    }
+    block_reduce_store<3>(red, partials);
+}
+
+}  // namespace osmpm

@@ -772,10 +772,21 @@ struct Sub : public osmpm_subdomain {
 
     // line-search energy at uu: block partials particle {E, |E|, inverted} (partA), node {E, |E|}
     // (partB, owned nodes only)
-    int energy_blocks_particles() const { return nblk(n, 256); }
+    // tiled (k_energy_tiled, one CTA per tile) unless OSMPM_ENERGY=particle (k_energy, for A/B)
+    static bool particle_energy()
+    {
+        static const bool v = getenv("OSMPM_ENERGY") && std::string(getenv("OSMPM_ENERGY")) == "particle";
+        return v;
+    }
+    int energy_blocks_particles() const { return particle_energy() ? nblk(n, 256) : box.ntiles; }
     osmpm_status energy_launch(const double* uu, double* partA, double* partB)
     {
-        KC(); k_energy<D, R><<<energy_blocks_particles(), 256, 0, st()>>>(P.p, cap, n, mat.p, box, mats, uu, partA);
+        if (particle_energy()) {
+            KC(); k_energy<D, R><<<energy_blocks_particles(), 256, 0, st()>>>(P.p, cap, n, mat.p, box, mats, uu, partA);
+        } else {
+            KC(); k_energy_tiled<D, R><<<box.ntiles, T::NT, 0, st()>>>(P.p, cap, mat.p, cell_start.p, box, mats, uu,
+                                                                        partA);
+        }
         OSMPM_LAUNCH_CHECK();
         KC(); k_energy_nodes<D><<<grad_blocks_nodes(), 256, 0, st()>>>(box.nnodes, nown, m.p, vn.p, uu, dt, grav[0],
                                                                         grav[1], grav[2], partB);
