@@ -1,0 +1,55 @@
+"""Physics pin of the oracle's whole single-subdomain implicit step against a closed form the paper
+fixes: the static cantilever under gravity in the Euler-Bernoulli (small-deflection) limit of the
+elastica, tip deflection = Gamma L / 8 with Gamma = q L^3 / D, D = E h^3 / (12 (1 - nu^2))
+(§4.1; tests/golden/g6_euler_bernoulli.txt).  One backward-Euler step with a time
+step large enough that the inertia term vanishes: Newton-PCG then finds the static equilibrium of the
+MPM discretisation (APIC P2G, neo-Hookean energy, B-spline gradients, clamp at x <= 0, G2P).  A
+dropped or mis-signed term anywhere in energy / gradient / Hessian / G2P moves the tip far outside
+the bands below; the discretisation error must shrink at first order under refinement."""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import read_golden
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
+import eb_cantilever as eb  # noqa: E402
+
+
+def test_golden_matches_closed_form():
+    L, h, E, nu, rho, g, gamma, tip = read_golden("g6_euler_bernoulli.txt")[0]
+    D = E * h ** 3 / (12 * (1 - nu ** 2))
+    assert gamma == pytest.approx(rho * g * h * L ** 3 / D, rel=1e-3)
+    assert tip == pytest.approx(gamma * L / 8, rel=1e-6)
+    assert (eb.L, eb.H, eb.E, eb.NU, eb.RHO) == (L, h, E, nu, rho)
+
+
+def test_oracle_cantilever_converges_to_euler_bernoulli():
+    tips = {}
+    for dx in (0.05, 0.025):
+        tip, ref, st = eb.run_oracle(dx)
+        assert st.status == 0
+        tips[dx] = tip / ref
+    # MPM is a few % too flexible at 4 cells through the thickness, first order in dx
+    assert 1.0 < tips[0.05] < 1.10
+    assert 1.0 < tips[0.025] < 1.05
+    assert (tips[0.05] - 1) / (tips[0.025] - 1) > 1.8
+
+
+def test_oracle_cantilever_quasi_static():
+    # the inertia term m / dt^2 no longer matters at dt = 10 s: dt = 20 s moves the tip by < 1 %
+    t10, _, _ = eb.run_oracle(0.05)
+    sc, idx, ref = eb.scene(0.05, dt=20.0)
+    import oracle
+    gs = oracle.p2g(sc)
+    dm = np.zeros((oracle.n_nodes(sc.grid), 2), np.uint8)
+    dm[idx] = 1
+    u, st = oracle.implicit_solve(sc, gs, oracle.default_settings(newton_rtol=1e-10, cg_rtol=1e-10, max_cg=20000,
+                                                                   max_newton=30),
+                                  dirichlet_mask=dm, dirichlet_v=np.zeros((oracle.n_nodes(sc.grid), 2)),
+                                  raise_on_error=False)
+    act = gs.active.astype(bool)
+    t20 = eb.tip_deflection(sc.particles.x, oracle.g2p(sc, np.where(act[:, None], u / sc.dt, 0.0)).x)
+    assert abs(t20 - t10) / t10 < 0.01
