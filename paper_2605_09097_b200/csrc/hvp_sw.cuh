@@ -23,6 +23,21 @@
 
 namespace osmpm {
 
+// OSMPM_SW_RECOMPUTE: the per-particle record holds only the fractional position f and G (rows padded
+// to 16 B); phase 2 recomputes the B-spline weights from f (fp64 issue traded for shared-memory
+// bandwidth, the binding resource of the stored-weights layout)
+#ifndef OSMPM_SW_RECOMPUTE
+#define OSMPM_SW_RECOMPUTE 0
+#endif
+
+template <int D, typename R> struct SWRec {
+    static constexpr bool RECOMPUTE = OSMPM_SW_RECOMPUTE != 0;
+    static constexpr int F0 = 0;
+    static constexpr int G0 = (D == 3) ? 4 : 2, GS = (D == 3) ? 4 : 2;  // G row a at G0 + GS a
+    static constexpr int RS = !RECOMPUTE ? HvpRec<D, R>::RS
+                                         : (sizeof(R) == 8 ? ((D == 3) ? 18 : 6) : ((D == 3) ? 20 : 12));
+};
+
 #ifndef OSMPM_SW_UNROLL
 #define OSMPM_SW_UNROLL 4
 #endif
@@ -54,7 +69,7 @@ constexpr size_t hvp_sw_smem_bytes()
 {
     using T = Tile<D>;
     return 16 + ((size_t)SW<D>::NNP * SVS<D, R>::S + SW<D>::STG + (size_t)HvpIn<D, R>::NF * HvpIn<D, R>::PFS +
-                 (size_t)HvpRec<D, R>::RS * T::NT) *
+                 (size_t)SWRec<D, R>::RS * T::NT) *
                     sizeof(R);
 }
 
@@ -188,7 +203,8 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
     using C = CL<D>;
     using In = HvpIn<D, R>;
     using S = SW<D>;
-    constexpr int RS = HvpRec<D, R>::RS;
+    using SR = SWRec<D, R>;
+    constexpr int RS = SR::RS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
     R* sv = reinterpret_cast<R*>(smem_raw + 16);
@@ -258,7 +274,16 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                     int lc[3] = {0, 0, 0};
                     weights_at<D, R>(x, b, t, lc, w, dw);
                     const RecPtr<R> r(rec, q, RS);
-                    store_weights<D, R>(r, w, dw);
+                    if constexpr (SR::RECOMPUTE) {
+#pragma unroll
+                        for (int a = 0; a < D; ++a) {
+                            R fa;
+                            base_of<R>(x[a], b.o[a], b.inv_dx, &fa);
+                            *r.at(SR::F0 + a) = fa;
+                        }
+                    } else {
+                        store_weights<D, R>(r, w, dw);
+                    }
                     R gd[D * D];
                     sw_gather<D, R>(sv, lc, w, dw, gd);
                     R Sv[Sym<D>::N], A[D * D];
@@ -290,7 +315,8 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                                 s1 = fma(gd[a * D + k], Sv[sym_idx<D>(k, bb)], s1);
                                 s2 = fma(M2[a * D + k], A[k * D + bb], s2);
                             }
-                            *r.at(Rec<D>::G + a * D + bb) = fma(cc, s2, fma(ltr, A[a * D + bb], s1));
+                            *r.at((SR::RECOMPUTE ? SR::G0 + SR::GS * a : Rec<D>::G + a * D) + bb) =
+                                fma(cc, s2, fma(ltr, A[a * D + bb], s1));
                         }
                 }
                 __syncthreads();  // records ready; the streamed buffer is free
@@ -312,10 +338,34 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                     for (int k = 0; k < len; ++k) {
                         const RecPtr<R> r(rec, rotated(p0, len, k, rot) - sb, RS);
                         ItemW<D, R> W;
-                        W.load(r, ii);
                         R s[D];
+                        if constexpr (SR::RECOMPUTE) {
+                            // quadratic B-spline from f (bspline(): w = 0.5 t^2 | 0.75 - t^2 | 0.5 t^2,
+                            // dw = t | -2t | t times 1/dx with t = f - 3/2, f - 1, f - 1/2)
+                            const R inv = (R)b.inv_dx;
+                            const R tx = *r.at(SR::F0) - (R(1.5) - R(0.5) * ii);
+                            W.wx = (ii == 1) ? fma(-tx, tx, R(0.75)) : R(0.5) * tx * tx;
+                            W.dwx = (ii == 1) ? R(-2) * tx * inv : tx * inv;
 #pragma unroll
-                        for (int bb = 0; bb < D; ++bb) s[bb] = *r.at(Rec<D>::G + icomp * D + bb);
+                            for (int ax = 1; ax < D; ++ax) {
+                                const R f = *r.at(SR::F0 + ax);
+                                const R t0 = f - R(1.5), t1 = f - R(1), t2 = f - R(0.5);
+                                R* wv = (ax == 1) ? W.wy : W.wz;
+                                R* dv = (ax == 1) ? W.dwy : W.dwz;
+                                wv[0] = R(0.5) * t0 * t0;
+                                wv[1] = fma(-t1, t1, R(0.75));
+                                wv[2] = R(0.5) * t2 * t2;
+                                dv[0] = t0 * inv;
+                                dv[1] = R(-2) * t1 * inv;
+                                dv[2] = t2 * inv;
+                            }
+#pragma unroll
+                            for (int bb = 0; bb < D; ++bb) s[bb] = *r.at(SR::G0 + SR::GS * icomp + bb);
+                        } else {
+                            W.load(r, ii);
+#pragma unroll
+                            for (int bb = 0; bb < D; ++bb) s[bb] = *r.at(Rec<D>::G + icomp * D + bb);
+                        }
                         item_linear<D, R>(s, W, acc);
                     }
                 }

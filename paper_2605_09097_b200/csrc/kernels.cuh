@@ -217,7 +217,6 @@ __global__ void k_bmass(const R* __restrict__ P, int64_t cap, int64_t n, const u
 
 }  // namespace osmpm
 #include "tiled.cuh"
-#include "hvp_ws.cuh"
 #include "hvp_sw.cuh"
 #include "p2g_tiled.cuh"
 #include "grad_sw.cuh"

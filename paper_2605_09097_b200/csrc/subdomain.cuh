@@ -656,15 +656,15 @@ struct Sub : public osmpm_subdomain {
         return OSMPM_OK;
     }
 
-    // HVP variant: sliding-window tiled kernel (default, hvp_sw.cuh); OSMPM_HVP=tiled | tiled_nopf | ws
-    // select the earlier variants, kept for A/B measurements
+    // HVP variant: sliding-window tiled kernel (default, hvp_sw.cuh); OSMPM_HVP=tiled | tiled_nopf
+    // select the earlier barrier-phased kernel of tiled.cuh, kept for A/B measurements
     int hvp_variant() const
     {
         static int v = -1;
         if (v < 0) {
             const char* e = getenv("OSMPM_HVP");
             const std::string s = e ? e : "";
-            v = (s == "ws") ? 1 : (s == "tiled_nopf") ? 2 : (s == "tiled") ? 0 : 3;
+            v = (s == "tiled_nopf") ? 2 : (s == "tiled") ? 0 : 3;
         }
         return v;
     }
@@ -673,17 +673,7 @@ struct Sub : public osmpm_subdomain {
     {
         auto& pf = ctx->prof;
         if (pf.on) pf.begin("hvp", st());
-        if (hvp_variant() == 1) {
-            using Lay = WSLayout<D, R>;
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(k_hvp_ws<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::BYTES);
-                attr = true;
-            }
-            const int grid = std::max(1, std::min(box.ntiles, ctx->num_sms));
-            KC(); k_hvp_ws<D, R><<<grid, WS<D>::NTHR, Lay::BYTES, st()>>>(P.p, cache.p, cap, cell_start.p, box, din,
-                                                                          yout);
-        } else if (hvp_variant() == 2) {
+        if (hvp_variant() == 2) {
             static bool attr2 = false;
             if (!attr2) {
                 cudaFuncSetAttribute(k_hvp<D, R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
