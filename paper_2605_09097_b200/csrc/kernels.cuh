@@ -59,15 +59,22 @@ __global__ void k_bounds(const R* __restrict__ P, int64_t cap, int64_t n, BoxDev
 }
 
 template <int D, typename R>
-__global__ void k_keys(const R* __restrict__ P, int64_t cap, int64_t n, BoxDev b, uint32_t* keys, int* vals)
+__global__ void k_keys(const R* __restrict__ P, int64_t cap, int64_t n, BoxDev b, uint32_t* keys, int* vals,
+                       const int* __restrict__ pid, ErrLatch* err)
 {
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= n) return;
     int c[3] = {0, 0, 0};
+    bool in = true;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
         R f;
         c[a] = base_of<R>(P[(PL<D>::X + a) * cap + p], b.o[a], b.inv_dx, &f) - b.lo[a];
+        in = in && c[a] >= 0 && c[a] < b.nc[a];
+    }
+    if (!in) {  // outside this (slab's) box: a missed migration; never silently corrupt the sort
+        latch_error(err, 2 /*OUT_OF_DOMAIN*/, pid[p]);
+        c[0] = c[1] = c[2] = 0;
     }
     keys[p] = cell_key<D>(b, c[0], c[1], c[2]);
     vals[p] = (int)p;

@@ -428,7 +428,7 @@ struct Sub : public osmpm_subdomain {
         OSMPM_TRY(cell_start.need(box.ncells + 1));
         auto& pf = ctx->prof;
         if (pf.on) pf.begin("sort", st());
-        KC(); k_keys<D, R><<<nblk_all(n, 256), 256, 0, st()>>>(P.p, cap, n, box, keys.p, vals.p);
+        KC(); k_keys<D, R><<<nblk_all(n, 256), 256, 0, st()>>>(P.p, cap, n, box, keys.p, vals.p, pid.p, err.p);
         OSMPM_LAUNCH_CHECK();
         int nbits = 1;
         while ((int64_t(1) << nbits) < box.ncells) ++nbits;
