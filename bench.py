@@ -132,6 +132,15 @@ class ClockSampler:
 # roofline accounting: algorithmic bytes of one HVP launch
 # ------------------------------------------------------------------------------------------------
 
+# algorithmic floating-point operations of one particle's HVP (3D): tensor-product
+# gather 270 FMA (540 flops), constitutive G_p 217 flops, scatter 9 items x 51 flops (459), B-spline
+# weights 40 flops
+HVP_FLOPS_PER_PARTICLE = 540 + 217 + 459 + 40
+# FP64 (and, at 2x, FP32) vector peak: 148 SMs x 64 FP64 lanes x 2 flops (FMA) x 1.965 GHz
+# (B200_PROFILING.md: 148 SMs, clocks.max.sm 1965 MHz; sm_100 FP64 rate half of FP32's 128 lanes/SM)
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+
+
 def hvp_algorithmic_bytes(n_particles, n_active_nodes, word):
     # per particle: x (3) + Newton cache S' (6) + Ah (9) + c' + l' (2) = 20 words of the particle
     # precision; per active node: read d (3) + write y (3) fp64 words
@@ -397,7 +406,15 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak if achieved else None,
                      "traffic": traffic, "kernel": "k_hvp", "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": hvp_bytes, "avg_launch_ms": hvp_avg_ms,
-                     "launches": hv_n},
+                     "launches": hv_n,
+                     # the same launches against the CUDA-core floating-point peak (the
+                     # fp64 HVP's compute ceiling lies at 68 % of the HBM roofline)
+                     "fp_pipe": ({"achieved_tflops": n_local * HVP_FLOPS_PER_PARTICLE / (hvp_avg_ms * 1e-3) / 1e12,
+                                  "peak_tflops": FP64_PEAK_TFLOPS * (2 if word == 4 else 1),
+                                  "frac": n_local * HVP_FLOPS_PER_PARTICLE / (hvp_avg_ms * 1e-3) / 1e12
+                                  / (FP64_PEAK_TFLOPS * (2 if word == 4 else 1)),
+                                  "flops_per_particle": HVP_FLOPS_PER_PARTICLE, "peak_kind": "derived (DESIGN.md §5)"}
+                                 if hv_n else None)},
         "kernel_ms_per_step": {f: v[1] / args.steps for f, v in fam.items()},
         "cpu_baseline": cpu,
         "e2e": e2e,
