@@ -94,7 +94,8 @@ k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int
     for (int k = threadIdx.x; k < 2 * S::STG; k += T::NT) stg[k] = 0.0;
     __syncthreads();
     const int it = threadIdx.x;
-    const int icell = it / (D * 3), icomp = (it / 3) % D, ii = it % 3;
+    int icell, icomp, ii;
+    item_of<D>(it, icell, icomp, ii);
     uint32_t parity = 0;
     Rd acc[S::NACC], accd[S::NACC];
 #pragma unroll

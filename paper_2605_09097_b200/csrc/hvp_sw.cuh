@@ -239,7 +239,8 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
     for (int k = threadIdx.x; k < S::STG; k += T::NT) stg[k] = R(0);
     __syncthreads();
     const int it = threadIdx.x;
-    const int icell = it / (D * 3), icomp = (it / 3) % D, ii = it % 3;
+    int icell, icomp, ii;
+    item_of<D>(it, icell, icomp, ii);
     uint32_t parity = 0;
     R acc[S::NACC];
 #pragma unroll

@@ -128,6 +128,27 @@ struct RecPtr {
     __device__ __forceinline__ R* at(int e) const { return base + e; }
 };
 
+// Phase-2 item (cell, component a, x-offset i) of thread `it`.  3D: the 9 items of a cell do not fit
+// an 8-lane quarter-warp, and shared-memory broadcast loads cost twice as many wavefronts when a
+// broadcast group straddles quarters (scripts/smem_probe.cu: LDS.128 2 vs 4, LDS.64 1 vs 2).  So
+// threads 0-127 hold the first 8 items of cells 0-15 (one cell per quarter) and threads 128-143 the
+// ninth item (a = 2, i = 2) of each cell.  2D: consecutive (cell, a, i).
+template <int D>
+__device__ __forceinline__ void item_of(int it, int& icell, int& icomp, int& ii)
+{
+    using T = Tile<D>;
+    if (D == 3 && T::LC == 16) {
+        const int pair = it < 128 ? (it & 7) : 8;
+        icell = it < 128 ? (it >> 3) : it - 128;
+        icomp = pair / 3;
+        ii = pair % 3;
+    } else {
+        icell = it / (D * 3);
+        icomp = (it / 3) % D;
+        ii = it % 3;
+    }
+}
+
 // k-th particle of [p0, p1) in the rotated order starting at offset rot
 __device__ __forceinline__ int rotated(int p0, int len, int k, int rot)
 {
