@@ -89,7 +89,7 @@ k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int
         int c[3];
         tnode_coords<D>(l, c);
         const int64_t g = box_node<D>(b, t[0] * T::T0 + c[0], t[1] * T::T1 + c[1], t[2] * T::T2 + c[2]);
-        sv[sw_node<D>(c[0], c[1], c[2]) * SVS<D, Rd>::S + a] = uin[g * D + a];
+        sv[sv_elem<D, Rd>(sw_node<D>(c[0], c[1], c[2]), a, S::NNP)] = uin[g * D + a];
     }
     for (int k = threadIdx.x; k < 2 * S::STG; k += T::NT) stg[k] = 0.0;
     __syncthreads();
@@ -257,7 +257,7 @@ k_energy_tiled(const R* __restrict__ P, int64_t cap, const int* __restrict__ mat
         int c[3];
         tnode_coords<D>(l, c);
         const int64_t g = box_node<D>(b, t[0] * T::T0 + c[0], t[1] * T::T1 + c[1], t[2] * T::T2 + c[2]);
-        sv[sw_node<D>(c[0], c[1], c[2]) * SVS<D, double>::S + a] = u[g * D + a];
+        sv[sv_elem<D, double>(sw_node<D>(c[0], c[1], c[2]), a, SW<D>::NNP)] = u[g * D + a];
     }
     __syncthreads();
     for (int p = p_lo + threadIdx.x; p < p_hi; p += T::NT) {

@@ -38,6 +38,10 @@ template <int D, typename R> struct SWRec {
                                          : (sizeof(R) == 8 ? ((D == 3) ? 18 : 6) : ((D == 3) ? 20 : 12));
 };
 
+#ifndef OSMPM_SW_SPLIT
+#define OSMPM_SW_SPLIT 1
+#endif
+
 #ifndef OSMPM_SW_UNROLL
 #define OSMPM_SW_UNROLL 4
 #endif
@@ -55,7 +59,21 @@ template <int D> struct SW {
 
 // reals per node of the node tile: 3D fp64 3 (24-B nodes; with 4x4xT2 tiles the rows of the four
 // cells of a warp's lanes start 4 banks apart: conflict-free 8-B loads), 3D fp32 4 (16-B nodes), 2D 2
-template <int D, typename R> struct SVS { static constexpr int S = (D == 3) ? (sizeof(R) == 8 ? 3 : 4) : 2; };
+template <int D, typename R> struct SVS {
+    static constexpr int S = (D == 3) ? (sizeof(R) == 8 ? 3 : 4) : 2;
+    // 3D fp64 split layout (OSMPM_SW_SPLIT): components 0,1 as 16-B pairs [NNP][2], component 2 as a
+    // separate [NNP] plane -- one 16-B and one 8-B load per node instead of three 8-B loads, same
+    // footprint; rows of 10 nodes put the four cells of a warp at bank offsets 0/8/16/24 (pairs) and
+    // 0/20/8/28 (plane): conflict-free
+    static constexpr bool SPLIT = OSMPM_SW_SPLIT && D == 3 && sizeof(R) == 8;
+};
+// shared-memory element of (node, component) in the node tile
+template <int D, typename R>
+__device__ __forceinline__ int sv_elem(int node, int a, int nnp)
+{
+    if constexpr (SVS<D, R>::SPLIT) return a < 2 ? node * 2 + a : 2 * nnp + node;
+    return node * SVS<D, R>::S + a;
+}
 
 template <int D>
 __device__ __forceinline__ int sw_node(int l0, int l1, int l2)
@@ -83,7 +101,8 @@ __device__ __forceinline__ void sw_gather(const R* sv, const int* lc, const R (*
     for (int k = 0; k < D * D; ++k) gd[k] = R(0);
     if (D == 3) {
         constexpr int NS = SVS<D, R>::S;
-        const R* base = sv + sw_node<D>(lc[0], lc[1], lc[2]) * NS;
+        const int n0 = sw_node<D>(lc[0], lc[1], lc[2]);
+        const R* base = sv + n0 * NS;
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
             R U0[3] = {0, 0, 0}, U1[3] = {0, 0, 0}, U2[3] = {0, 0, 0};
@@ -92,9 +111,14 @@ __device__ __forceinline__ void sw_gather(const R* sv, const int* lc, const R (*
                 R T0[3] = {0, 0, 0}, T1[3] = {0, 0, 0};
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
-                    const R* sp = base + ((i * T::N1 + j) * SW<D>::NZP + k) * NS;
+                    const int off = (i * T::N1 + j) * SW<D>::NZP + k;
+                    const R* sp = base + off * NS;
                     R s[3];
-                    if constexpr (NS == 4) {
+                    if constexpr (SVS<D, R>::SPLIT) {
+                        const V2 v01 = *reinterpret_cast<const V2*>(sv + (n0 + off) * 2);
+                        s[0] = v01.x;
+                        s[1] = v01.y;
+                    } else if constexpr (NS == 4) {
                         const V2 v01 = *reinterpret_cast<const V2*>(sp);
                         s[0] = v01.x;
                         s[1] = v01.y;
@@ -102,7 +126,7 @@ __device__ __forceinline__ void sw_gather(const R* sv, const int* lc, const R (*
                         s[0] = sp[0];
                         s[1] = sp[1];
                     }
-                    s[2] = sp[2];
+                    s[2] = SVS<D, R>::SPLIT ? sv[2 * SW<D>::NNP + n0 + off] : sp[2];
 #pragma unroll
                     for (int a = 0; a < 3; ++a) {
                         T0[a] = fma(s[a], w[2][k], T0[a]);
@@ -234,7 +258,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
         int c[3];
         tnode_coords<D>(l, c);
         const int64_t g = box_node<D>(b, t[0] * T::T0 + c[0], t[1] * T::T1 + c[1], t[2] * T::T2 + c[2]);
-        sv[sw_node<D>(c[0], c[1], c[2]) * SVS<D, R>::S + a] = (R)din[g * D + a];
+        sv[sv_elem<D, R>(sw_node<D>(c[0], c[1], c[2]), a, S::NNP)] = (R)din[g * D + a];
     }
     for (int k = threadIdx.x; k < S::STG; k += T::NT) stg[k] = R(0);
     __syncthreads();
