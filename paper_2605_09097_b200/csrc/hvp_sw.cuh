@@ -31,6 +31,9 @@ namespace osmpm {
 #endif
 
 template <int D, typename R> struct SWRec {
+    // G row a starts at GROW(a): 3D fp64 rows padded to 4 reals (16-B aligned: one 16-B + one 8-B load
+    // per row; the 30-real record has exactly the room), otherwise packed
+    static constexpr int GP = (D == 3 && sizeof(R) == 8) ? 4 : D;
     static constexpr bool RECOMPUTE = OSMPM_SW_RECOMPUTE != 0;
     static constexpr int F0 = 0;
     static constexpr int G0 = (D == 3) ? 4 : 2, GS = (D == 3) ? 4 : 2;  // G row a at G0 + GS a
@@ -331,7 +334,8 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                         }
                     const R ltr = ll * tr;
 #pragma unroll
-                    for (int a = 0; a < D; ++a)
+                    for (int a = 0; a < D; ++a) {
+                        R Ga[D];
 #pragma unroll
                         for (int bb = 0; bb < D; ++bb) {
                             R s1 = R(0), s2 = R(0);
@@ -340,9 +344,23 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                                 s1 = fma(gd[a * D + k], Sv[sym_idx<D>(k, bb)], s1);
                                 s2 = fma(M2[a * D + k], A[k * D + bb], s2);
                             }
-                            *r.at((SR::RECOMPUTE ? SR::G0 + SR::GS * a : Rec<D>::G + a * D) + bb) =
-                                fma(cc, s2, fma(ltr, A[a * D + bb], s1));
+                            Ga[bb] = fma(cc, s2, fma(ltr, A[a * D + bb], s1));
                         }
+                        if constexpr (SR::RECOMPUTE) {
+#pragma unroll
+                            for (int bb = 0; bb < D; ++bb) *r.at(SR::G0 + SR::GS * a + bb) = Ga[bb];
+                        } else if constexpr (SR::GP == 4) {
+                            using V2 = typename Vec2<R>::type;
+                            V2 g01;
+                            g01.x = Ga[0];
+                            g01.y = Ga[1];
+                            *reinterpret_cast<V2*>(r.at(Rec<D>::G + 4 * a)) = g01;
+                            *r.at(Rec<D>::G + 4 * a + 2) = Ga[D - 1];
+                        } else {
+#pragma unroll
+                            for (int bb = 0; bb < D; ++bb) *r.at(Rec<D>::G + a * D + bb) = Ga[bb];
+                        }
+                    }
                 }
                 __syncthreads();  // records ready; the streamed buffer is free
                 if (from_pf) {
@@ -389,7 +407,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                         } else {
                             W.load(r, ii);
 #pragma unroll
-                            for (int bb = 0; bb < D; ++bb) s[bb] = *r.at(Rec<D>::G + icomp * D + bb);
+                            for (int bb = 0; bb < D; ++bb) s[bb] = *r.at(Rec<D>::G + icomp * SR::GP + bb);
                         }
                         item_linear<D, R>(s, W, acc);
                     }
