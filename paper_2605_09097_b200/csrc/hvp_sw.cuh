@@ -165,13 +165,13 @@ __device__ __forceinline__ void sw_emit(int cellL, int a, int i, R* acc, R* stg)
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
             const int nxy = (cx + i) * T::N1 + (cy + j);
-            stg[(nxy * 3 + a) * 9 + i * 3 + j] = acc[j * 3 + 0];
+            stg[(i * 3 + j) * SW<D>::NITEM + nxy * 3 + a] = acc[j * 3 + 0];  // slot-major
             acc[j * 3 + 0] = acc[j * 3 + 1];
             acc[j * 3 + 1] = acc[j * 3 + 2];
             acc[j * 3 + 2] = R(0);
         }
     } else {
-        stg[((cellL + i) * 2 + a) * 3 + i] = acc[0];
+        stg[i * SW<D>::NITEM + (cellL + i) * 2 + a] = acc[0];
         acc[0] = acc[1];
         acc[1] = acc[2];
         acc[2] = R(0);
@@ -185,10 +185,10 @@ __device__ __forceinline__ void sw_flush(const BoxDev& b, const int* t, int plan
 {
     using T = Tile<D>;
     for (int it = threadIdx.x; it < SW<D>::NITEM; it += T::NT) {
-        const R* p = stg + it * SW<D>::NSLOT;
-        R s = p[0];
+        // slot-major staging: consecutive threads read consecutive reals (conflict-free)
+        R s = stg[it];
 #pragma unroll
-        for (int k = 1; k < SW<D>::NSLOT; ++k) s += p[k];
+        for (int k = 1; k < SW<D>::NSLOT; ++k) s += stg[k * SW<D>::NITEM + it];
         if (s != R(0)) {
             const int a = it % D, nxy = it / D;
             int64_t g;
