@@ -41,6 +41,12 @@ template <int D, typename R> struct SWRec {
                                          : (sizeof(R) == 8 ? ((D == 3) ? 18 : 6) : ((D == 3) ? 20 : 12));
 };
 
+// OSMPM_SW_L2PF: stream the next layer's particle inputs into L2 (cp.async.bulk.prefetch.L2) instead
+// of shared memory, and read them with global loads (no staging buffer, no mbarrier)
+#ifndef OSMPM_SW_L2PF
+#define OSMPM_SW_L2PF 0
+#endif
+
 #ifndef OSMPM_SW_SPLIT
 #define OSMPM_SW_SPLIT 1
 #endif
@@ -89,7 +95,8 @@ template <int D, typename R>
 constexpr size_t hvp_sw_smem_bytes()
 {
     using T = Tile<D>;
-    return 16 + ((size_t)SW<D>::NNP * SVS<D, R>::S + SW<D>::STG + (size_t)HvpIn<D, R>::NF * HvpIn<D, R>::PFS +
+    return 16 + ((size_t)SW<D>::NNP * SVS<D, R>::S + SW<D>::STG +
+                 (OSMPM_SW_L2PF ? (size_t)0 : (size_t)HvpIn<D, R>::NF * HvpIn<D, R>::PFS) +
                  (size_t)SWRec<D, R>::RS * T::NT) *
                     sizeof(R);
 }
@@ -212,6 +219,13 @@ __device__ __forceinline__ void sw_prefetch(const R* __restrict__ P, const R* __
     const int lb0 = lb & ~(In::UE - 1);                       // 16-B aligned start
     const int cnt = min(le, lb + Tile<D>::NT) - lb0;
     const uint32_t bytes = (uint32_t)((cnt + In::UE - 1) & ~(In::UE - 1)) * sizeof(R);
+    if constexpr (OSMPM_SW_L2PF) {
+        if (lane < In::NF) {
+            const R* src = (lane < D) ? P + (int64_t)(PL<D>::X + lane) * cap + lb0 : cache + (int64_t)(lane - D) * cap + lb0;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+        }
+        return;
+    }
     fence_async_smem();
     if (lane == 0) mbar_expect_tx(bar, bytes * In::NF);
     __syncwarp();
@@ -237,7 +251,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
     R* sv = reinterpret_cast<R*>(smem_raw + 16);
     R* stg = sv + S::NNP * SVS<D, R>::S;
     R* pf = stg + S::STG;
-    R* rec = pf + In::NF * In::PFS;
+    R* rec = pf + (OSMPM_SW_L2PF ? 0 : In::NF * In::PFS);
     const int tile = blockIdx.x;
     const int64_t kt = (int64_t)tile * T::NC;
     __shared__ int scs[T::NC + 1];  // the tile's cell ranges
@@ -283,7 +297,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
             for (int sb = lb; sb < le; sb += T::NT) {
                 const int se = min(sb + T::NT, le);
                 const int q = threadIdx.x, p = sb + q;
-                const bool from_pf = (sb == lb);
+                const bool from_pf = !OSMPM_SW_L2PF && (sb == lb);
                 if (sb != lb) __syncthreads();  // previous chunk's records consumed
                 if (from_pf) mbar_wait(bar, parity);
                 if (p < se) {
@@ -363,8 +377,8 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                     }
                 }
                 __syncthreads();  // records ready; the streamed buffer is free
-                if (from_pf) {
-                    parity ^= 1u;
+                if (sb == lb) {
+                    if (from_pf) parity ^= 1u;
                     if (threadIdx.x < 32 && next < T::NL)
                         sw_prefetch<D, R>(P, cache, cap, scs[next * T::LC], scs[(next + 1) * T::LC], pf, bar,
                                           threadIdx.x);
