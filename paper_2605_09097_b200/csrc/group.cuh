@@ -163,7 +163,7 @@ osmpm_status group_p2g(SlabGroup<D, R> G)
 //   particles {E, |E|, inverted}, nodes {E, |E|, |g_free|^2, f_scale^2}
 // ---------------------------------------------------------------------------------------------
 template <int D, typename R>
-osmpm_status group_grad(SlabGroup<D, R> G, bool need_fmask)
+osmpm_status group_grad(SlabGroup<D, R> G, bool need_fmask, bool trial)
 {
     GroupBufs& gb = *G.gb;
     int64_t na = 0, nb = 0;
@@ -178,7 +178,7 @@ osmpm_status group_grad(SlabGroup<D, R> G, bool need_fmask)
     int64_t off = 0;
     for (int i = 0; i < G.ns; ++i) {
         Sub<D, R>* s = G.s[i];
-        OSMPM_TRY(s->grad_scatter(s->u.p, need_fmask, gb.partA.p + off * 3));
+        OSMPM_TRY(s->grad_scatter(trial ? s->ut.p : s->u.p, need_fmask, gb.partA.p + off * 3));
         off += s->box.ntiles;
     }
     if (pf.on) pf.end("grad", G.st);
@@ -186,7 +186,7 @@ osmpm_status group_grad(SlabGroup<D, R> G, bool need_fmask)
     off = 0;
     for (int i = 0; i < G.ns; ++i) {
         Sub<D, R>* s = G.s[i];
-        OSMPM_TRY(s->grad_nodes(s->u.p, gb.partB.p + off * 4));
+        OSMPM_TRY(s->grad_nodes(trial ? s->ut.p : s->u.p, gb.partB.p + off * 4));
         off += s->grad_blocks_nodes();
     }
     G.s[0]->KC();
@@ -280,13 +280,32 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
     OSMPM_TRY(gb.partB.need((size_t)std::max<int64_t>(std::max(nbn_tot, nbd_tot), 1) * 4));
     const bool remote = G.multi();
     double g0 = 0.0, gref = 0.0;
-    // E(u) for the line search comes from the same energy kernels as the trial energies, so both
-    // sides of the comparison round alike (R8); later iterations reuse the accepted trial
+    // Line search by gradient evaluations (default): each trial point's energy comes from the
+    // gradient kernel, whose gradient, Jacobi diagonal and linearisation cache then serve the next
+    // Newton iteration when the trial is accepted (no separate energy pass, no second gradient at
+    // the accepted point).  OSMPM_LS=energy: energy-only trial passes + a gradient per iteration.
+    // Either way E(u) and E(trial) come from the same routine, so both sides of the comparison round
+    // alike (R8); later iterations reuse the accepted trial's energy.
+    // Used in fixed-iteration mode (the timed C5 sub-step); converged solves keep the energy-only
+    // passes, whose rounding behaviour near the noise floor the E-B physics test pins (R8).
+    static const bool ls_energy_env = getenv("OSMPM_LS") && std::string(getenv("OSMPM_LS")) == "energy";
+    const bool ls_energy = ls_energy_env || !s->fixed_iters;
+    auto grad_E = [&](double& E, double& Ea) {
+        E = (gb.h_scal[2] > 0) ? INFINITY : gb.h_scal[0] + gb.h_scal[3];
+        Ea = gb.h_scal[1] + gb.h_scal[4];
+    };
     double E0n = 0.0, Ea0n = 0.0;
+    bool have_g = false;  // g, diag, cache are at the current u
     if (s->max_newton > 0) {
-        OSMPM_TRY(group_energy<D, R>(G, false));
-        E0n = (gb.h_scal[10] > 0) ? INFINITY : gb.h_scal[8] + gb.h_scal[11];
-        Ea0n = gb.h_scal[9] + gb.h_scal[12];
+        if (ls_energy) {
+            OSMPM_TRY(group_energy<D, R>(G, false));
+            E0n = (gb.h_scal[10] > 0) ? INFINITY : gb.h_scal[8] + gb.h_scal[11];
+            Ea0n = gb.h_scal[9] + gb.h_scal[12];
+        } else {
+            OSMPM_TRY(group_grad<D, R>(G, true, false));
+            grad_E(E0n, Ea0n);
+            have_g = true;
+        }
     }
     bool converged = false;
     osmpm_status rc = OSMPM_OK;
@@ -309,7 +328,8 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
         return OSMPM_OK;
     };
     for (int it = 0; it < s->max_newton; ++it) {
-        OSMPM_TRY(group_grad<D, R>(G, true));
+        if (!have_g) OSMPM_TRY(group_grad<D, R>(G, true, false));
+        have_g = false;
         const double gn = std::sqrt(gb.h_scal[5]);
         const double E0 = E0n, Ea0 = Ea0n;
         if (it == 0) {
@@ -426,10 +446,15 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
                 k_axpy_free<<<nblk(ndof, 256), 256, 0, st>>>(ndof, q->fmask.p, q->u.p, alpha, q->xs.p, q->ut.p);
             }
             OSMPM_LAUNCH_CHECK();
-            OSMPM_TRY(group_energy<D, R>(G, true));
-            const bool inv = gb.h_scal[10] > 0;
-            Et = inv ? INFINITY : gb.h_scal[8] + gb.h_scal[11];
-            Eat = gb.h_scal[9] + gb.h_scal[12];
+            if (ls_energy) {
+                OSMPM_TRY(group_energy<D, R>(G, true));
+                const bool inv = gb.h_scal[10] > 0;
+                Et = inv ? INFINITY : gb.h_scal[8] + gb.h_scal[11];
+                Eat = gb.h_scal[9] + gb.h_scal[12];
+            } else {
+                OSMPM_TRY(group_grad<D, R>(G, true, true));
+                grad_E(Et, Eat);
+            }
             if (Et < E0 || (std::isfinite(Et) && std::fabs(Et - E0) <= s->energy_noise_rtol * Ea0)) break;
             alpha *= 0.5;
             sts->ls_halvings++;
@@ -446,11 +471,12 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
         }
         E0n = Et;
         Ea0n = Eat;
+        have_g = !ls_energy;  // the accepted trial's gradient / diagonal / cache are current
         sts->energy = Et;
         sts->newton_iters = it + 1;
     }
     if (rc == OSMPM_OK && !s->fixed_iters && !converged) {
-        OSMPM_TRY(group_grad<D, R>(G, true));
+        if (!have_g) OSMPM_TRY(group_grad<D, R>(G, true, false));
         const double gn = std::sqrt(gb.h_scal[5]);
         sts->grad_norm = gn;
         if (!(gn <= s->newton_rtol * gref || gn <= s->newton_atol)) {

@@ -97,7 +97,7 @@ template <int D, typename R> struct SlabGroup {
     bool multi() const { return gc && gc->multi(); }
 };
 template <int D, typename R> osmpm_status group_p2g(SlabGroup<D, R> G);
-template <int D, typename R> osmpm_status group_grad(SlabGroup<D, R> G, bool need_fmask);
+template <int D, typename R> osmpm_status group_grad(SlabGroup<D, R> G, bool need_fmask, bool trial = false);
 template <int D, typename R> osmpm_status group_energy(SlabGroup<D, R> G, bool trial);
 template <int D, typename R> osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s,
                                                       osmpm_solve_stats* stats);
