@@ -415,7 +415,7 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
                     Sub<D, R>* q = G.s[i];
                     const int64_t ndof = q->box.nnodes * D;
                     q->KC();
-                    k_cg_p<<<nblk(ndof, 256), 256, 0, st>>>(ndof, q->z.p, q->p.p, q->y.p, gb.cgs.p);
+                    k_cg_p<<<nblk(ndof, 256), 256, 0, st>>>(ndof, q->fmask.p, q->z.p, q->p.p, q->y.p, gb.cgs.p);
                 }
                 if (pf.on) pf.end("cg", st);
                 OSMPM_LAUNCH_CHECK();

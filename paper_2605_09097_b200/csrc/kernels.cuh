@@ -516,11 +516,13 @@ __global__ void k_cg_q(int64_t nn, int64_t nown, const uint8_t* __restrict__ fm,
     double red[1] = {0.0};
     if (!s->done) {
         for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
-            const double mi = m[i] * idt2;
 #pragma unroll
             for (int a = 0; a < D; ++a) {
                 const int64_t k = i * D + a;
-                const double q = fm[k] ? y[k] + mi * p[k] : 0.0;
+                // non-free DOFs (inactive, Dirichlet) are skipped without touching memory: their p is
+                // 0 and y there is never read (k_cg_update skips them too; k_cg_p re-zeroes y)
+                if (!fm[k]) continue;
+                const double q = y[k] + m[i] * idt2 * p[k];
                 y[k] = q;
                 if (i < nown) red[0] += p[k] * q;
             }
@@ -566,13 +568,14 @@ __global__ void k_cg_update(int64_t ndof, int64_t nown_dof, const uint8_t* __res
     if (!s->done) {
         const double al = s->alpha;
         for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ndof; k += (int64_t)gridDim.x * blockDim.x) {
+            if (!fm[k]) continue;  // x, r, z stay 0 on non-free DOFs (k_cg_init)
             const double xk = x[k] + al * p[k];
             const double rk = r[k] - al * q[k];
-            const double zk = fm[k] ? rk / dg[k] : 0.0;
+            const double zk = rk / dg[k];
             x[k] = xk;
             r[k] = rk;
             z[k] = zk;
-            if (fm[k] && k < nown_dof) {
+            if (k < nown_dof) {
                 red[0] += rk * zk;
                 red[1] += rk * rk;
             }
@@ -611,13 +614,13 @@ __global__ void k_final_sum_cg(const double* partials, int nb, const CGScalars* 
 }
 
 // p = z + beta p ; y = 0
-__global__ void k_cg_p(int64_t ndof, const double* __restrict__ z, double* __restrict__ p, double* __restrict__ y,
-                       const CGScalars* s)
+__global__ void k_cg_p(int64_t ndof, const uint8_t* __restrict__ fm, const double* __restrict__ z,
+                       double* __restrict__ p, double* __restrict__ y, const CGScalars* s)
 {
     if (s->done) return;
     const double be = s->beta;
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ndof; k += (int64_t)gridDim.x * blockDim.x) {
-        p[k] = z[k] + be * p[k];
+        if (fm[k]) p[k] = z[k] + be * p[k];  // p stays 0 on non-free DOFs
         y[k] = 0.0;
     }
 }
