@@ -112,8 +112,9 @@ struct Dist : public osmpm_subdomain {
     int64_t gdims[3] = {1, 1, 1};
     int64_t n_total = 0;
     DBuf<double> dense_io;          // dense node / creation-order particle staging
-    DBuf<unsigned char> mig_send[2], mig_recv[2];
+    DBuf<unsigned char> mig_recv[2];  // migration payload from the left / right rank
     DBuf<unsigned long long> mig_cnt;
+    std::vector<std::unique_ptr<DBuf<unsigned char>>> sendL, sendR;  // per local slab
     unsigned long long* h_cnt = nullptr;
 
     ~Dist() override
@@ -423,12 +424,13 @@ struct Dist : public osmpm_subdomain {
                 std::swap(s->pid.cap, s->pid2.cap);
             }
         }
-        // pack every slab's movers (per direction) into its send buffers
-        std::vector<std::unique_ptr<DBuf<unsigned char>>> sendL(ns), sendR(ns);
+        // pack every slab's movers (per direction) into its send buffers (grow-only members)
+        while ((int)sendL.size() < ns) {
+            sendL.push_back(std::make_unique<DBuf<unsigned char>>());
+            sendR.push_back(std::make_unique<DBuf<unsigned char>>());
+        }
         for (int i = 0; i < ns; ++i) {
             Sub<D, R>* s = sp[i];
-            sendL[i] = std::make_unique<DBuf<unsigned char>>();
-            sendR[i] = std::make_unique<DBuf<unsigned char>>();
             const int64_t c2[2] = {nl[i], nr[i]};
             const int64_t o2[2] = {nstay[i], nstay[i] + nl[i]};
             DBuf<unsigned char>* b2[2] = {sendL[i].get(), sendR[i].get()};
@@ -504,8 +506,6 @@ struct Dist : public osmpm_subdomain {
             if (r > 0) OSMPM_TRY(append(sp[0], mig_recv[0].p, from_left));
             if (r + 1 < gc->nranks) OSMPM_TRY(append(sp[ns - 1], mig_recv[1].p, from_right));
         }
-        // the send buffers are freed at scope exit: make sure the copies consumed them
-        OSMPM_CU(cudaStreamSynchronize(st()));
         return OSMPM_OK;
     }
 
