@@ -235,8 +235,11 @@ __device__ __forceinline__ void sw_prefetch(const R* __restrict__ P, const R* __
     }
 }
 
+#ifndef OSMPM_SW_MINB
+#define OSMPM_SW_MINB 3
+#endif
 template <int D, typename R>
-__global__ void __launch_bounds__(Tile<D>::NT, 3)
+__global__ void __launch_bounds__(Tile<D>::NT, OSMPM_SW_MINB)
 k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, const int* __restrict__ cell_start,
          BoxDev b, const double* __restrict__ din, double* __restrict__ yout)
 {
