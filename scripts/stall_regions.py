@@ -20,7 +20,7 @@ def region(fn, ln, src_lines):
     if fn is None:
         return "?"
     text = src_lines.get(fn, {}).get(ln, "")
-    if fn == "tiled.cuh" and 240 <= ln <= 290:
+    if fn == "tiled.cuh" and TILED_ITEM[0] <= ln <= TILED_ITEM[1]:
         return "phase2 item (weights load + FMA)"
     if fn == "hvp_sw.cuh":
         for lo, hi, name in REGIONS_SW:
@@ -34,6 +34,7 @@ def region(fn, ln, src_lines):
 
 
 REGIONS_SW = []
+TILED_ITEM = [0, 0]
 
 
 def main():
@@ -44,6 +45,10 @@ def main():
     src = {}
     for f in os.listdir(csrc):
         src[f] = {i + 1: t for i, t in enumerate(open(os.path.join(csrc, f)).read().splitlines())}
+    # phase-2 item helpers of tiled.cuh: from `struct ItemW` to `item_quadratic`
+    tl = src["tiled.cuh"]
+    TILED_ITEM[0] = next(i for i, t in tl.items() if "struct ItemW" in t)
+    TILED_ITEM[1] = next(i for i, t in tl.items() if "item_quadratic(" in t)
     # regions of hvp_sw.cuh by marker comments / function names
     lines = src["hvp_sw.cuh"]
 
