@@ -84,13 +84,7 @@ k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int
     }
     int t[3];
     tile_coords<D>(b, tile, t);
-    for (int idx = threadIdx.x; idx < T::NN * D; idx += T::NT) {
-        const int a = idx % D, l = idx / D;
-        int c[3];
-        tnode_coords<D>(l, c);
-        const int64_t g = box_node<D>(b, t[0] * T::T0 + c[0], t[1] * T::T1 + c[1], t[2] * T::T2 + c[2]);
-        sv[sv_elem<D, Rd>(sw_node<D>(c[0], c[1], c[2]), a, S::NNP)] = uin[g * D + a];
-    }
+    sw_stage_tile<D, Rd, T::NT>(b, t, uin, sv);
     for (int k = threadIdx.x; k < 2 * S::STG; k += T::NT) stg[k] = 0.0;
     __syncthreads();
     const int it = threadIdx.x;
@@ -252,13 +246,7 @@ k_energy_tiled(const R* __restrict__ P, int64_t cap, const int* __restrict__ mat
     }
     int t[3];
     tile_coords<D>(b, tile, t);
-    for (int idx = threadIdx.x; idx < T::NN * D; idx += T::NT) {
-        const int a = idx % D, l = idx / D;
-        int c[3];
-        tnode_coords<D>(l, c);
-        const int64_t g = box_node<D>(b, t[0] * T::T0 + c[0], t[1] * T::T1 + c[1], t[2] * T::T2 + c[2]);
-        sv[sv_elem<D, double>(sw_node<D>(c[0], c[1], c[2]), a, SW<D>::NNP)] = u[g * D + a];
-    }
+    sw_stage_tile<D, double, T::NT>(b, t, u, sv);
     __syncthreads();
     for (int p = p_lo + threadIdx.x; p < p_hi; p += T::NT) {
         double x[3], w[3][3], dw[3][3], Mx[D * D];

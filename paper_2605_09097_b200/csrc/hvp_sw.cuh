@@ -91,6 +91,32 @@ __device__ __forceinline__ int sw_node(int l0, int l1, int l2)
     return (D == 3) ? (l0 * T::N1 + l1) * SW<D>::NZP + l2 : l0 * T::N1 + l1;
 }
 
+// node values of a node vector (fp64, components innermost) on the tile's nodes -> the node tile.
+// fp64 tiles: cp.async (LDGSTS) so every thread's loads are in flight at once instead of one
+// load-store round trip each (the tile prologue is latency-bound); the caller's barrier follows
+// cp.async.wait_all.  fp32 tiles convert through registers.
+__device__ __forceinline__ void cp_async_8(void* sdst, const void* gsrc)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+template <int D, typename R, int NTHR>
+__device__ __forceinline__ void sw_stage_tile(const BoxDev& b, const int* t, const double* __restrict__ src, R* sv)
+{
+    using T = Tile<D>;
+    for (int idx = threadIdx.x; idx < T::NN * D; idx += NTHR) {
+        const int a = idx % D, l = idx / D;
+        int c[3];
+        tnode_coords<D>(l, c);
+        const int64_t g = box_node<D>(b, t[0] * T::T0 + c[0], t[1] * T::T1 + c[1], t[2] * T::T2 + c[2]);
+        R* dst = sv + sv_elem<D, R>(sw_node<D>(c[0], c[1], c[2]), a, SW<D>::NNP);
+        if constexpr (sizeof(R) == 8)
+            cp_async_8(dst, src + g * D + a);
+        else
+            *dst = (R)src[g * D + a];
+    }
+    if constexpr (sizeof(R) == 8) asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 template <int D, typename R>
 constexpr size_t hvp_sw_smem_bytes()
 {
@@ -273,13 +299,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
     tile_coords<D>(b, tile, t);
     // node tile of d (padded rows) and the staging slots (zero once: slots of cells outside the
     // tile are never written)
-    for (int idx = threadIdx.x; idx < T::NN * D; idx += T::NT) {
-        const int a = idx % D, l = idx / D;
-        int c[3];
-        tnode_coords<D>(l, c);
-        const int64_t g = box_node<D>(b, t[0] * T::T0 + c[0], t[1] * T::T1 + c[1], t[2] * T::T2 + c[2]);
-        sv[sv_elem<D, R>(sw_node<D>(c[0], c[1], c[2]), a, S::NNP)] = (R)din[g * D + a];
-    }
+    sw_stage_tile<D, R, T::NT>(b, t, din, sv);
     for (int k = threadIdx.x; k < S::STG; k += T::NT) stg[k] = R(0);
     __syncthreads();
     const int it = threadIdx.x;
