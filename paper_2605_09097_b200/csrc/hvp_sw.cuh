@@ -99,7 +99,7 @@ __device__ __forceinline__ void cp_async_8(void* sdst, const void* gsrc)
 {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
 }
-template <int D, typename R, int NTHR>
+template <int D, typename R, int NTHR, bool WAIT = true>
 __device__ __forceinline__ void sw_stage_tile(const BoxDev& b, const int* t, const double* __restrict__ src, R* sv)
 {
     using T = Tile<D>;
@@ -114,7 +114,8 @@ __device__ __forceinline__ void sw_stage_tile(const BoxDev& b, const int* t, con
         else
             *dst = (R)src[g * D + a];
     }
-    if constexpr (sizeof(R) == 8) asm volatile("cp.async.wait_all;" ::: "memory");
+    if constexpr (sizeof(R) == 8)
+        if (WAIT) asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 template <int D, typename R>
@@ -284,9 +285,19 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
     const int tile = blockIdx.x;
     const int64_t kt = (int64_t)tile * T::NC;
     __shared__ int scs[T::NC + 1];  // the tile's cell ranges
+    int t[3];
+    tile_coords<D>(b, tile, t);
+    // the node tile of d (fp64: asynchronous, in flight while the cell ranges load) and the staging
+    // slots (zeroed once: slots of cells outside the tile are never written)
+    constexpr bool ASYNC = sizeof(R) == 8;
+    if constexpr (ASYNC) sw_stage_tile<D, R, T::NT, false>(b, t, din, sv);
     for (int i = threadIdx.x; i <= T::NC; i += T::NT) scs[i] = cell_start[kt + i];
+    for (int k = threadIdx.x; k < S::STG; k += T::NT) stg[k] = R(0);
     __syncthreads();
-    if (scs[0] == scs[T::NC]) return;
+    if (scs[0] == scs[T::NC]) {
+        if constexpr (ASYNC) asm volatile("cp.async.wait_all;" ::: "memory");
+        return;
+    }
     auto layer_empty = [&](int l) { return scs[l * T::LC] == scs[(l + 1) * T::LC]; };
     int first = 0;
     while (layer_empty(first)) ++first;
@@ -295,12 +306,10 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
         __syncwarp();
         sw_prefetch<D, R>(P, cache, cap, scs[first * T::LC], scs[(first + 1) * T::LC], pf, bar, threadIdx.x);
     }
-    int t[3];
-    tile_coords<D>(b, tile, t);
-    // node tile of d (padded rows) and the staging slots (zero once: slots of cells outside the
-    // tile are never written)
-    sw_stage_tile<D, R, T::NT>(b, t, din, sv);
-    for (int k = threadIdx.x; k < S::STG; k += T::NT) stg[k] = R(0);
+    if constexpr (ASYNC)
+        asm volatile("cp.async.wait_all;" ::: "memory");
+    else
+        sw_stage_tile<D, R, T::NT>(b, t, din, sv);
     __syncthreads();
     const int it = threadIdx.x;
     int icell, icomp, ii;
