@@ -290,6 +290,21 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
     // the node tile of d (fp64: asynchronous, in flight while the cell ranges load) and the staging
     // slots (zeroed once: slots of cells outside the tile are never written)
     constexpr bool ASYNC = sizeof(R) == 8;
+    // warp 0 starts the first non-empty layer's input copies straight from the layer boundaries in
+    // global memory, before the cell ranges reach shared memory
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const int v = lane <= T::NL ? cell_start[kt + lane * T::LC] : 0;
+        const int vn = __shfl_down_sync(0xffffffffu, v, 1);
+        const unsigned ne = __ballot_sync(0xffffffffu, lane < T::NL && vn > v);
+        if (lane == 0) mbar_init(bar, 1);
+        __syncwarp();
+        if (ne) {
+            const int f = __ffs(ne) - 1;
+            const int lb0 = __shfl_sync(0xffffffffu, v, f), le0 = __shfl_sync(0xffffffffu, v, f + 1);
+            sw_prefetch<D, R>(P, cache, cap, lb0, le0, pf, bar, lane);
+        }
+    }
     if constexpr (ASYNC) sw_stage_tile<D, R, T::NT, false>(b, t, din, sv);
     for (int i = threadIdx.x; i <= T::NC; i += T::NT) scs[i] = cell_start[kt + i];
     for (int k = threadIdx.x; k < S::STG; k += T::NT) stg[k] = R(0);
@@ -299,13 +314,6 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
         return;
     }
     auto layer_empty = [&](int l) { return scs[l * T::LC] == scs[(l + 1) * T::LC]; };
-    int first = 0;
-    while (layer_empty(first)) ++first;
-    if (threadIdx.x < 32) {
-        if (threadIdx.x == 0) mbar_init(bar, 1);
-        __syncwarp();
-        sw_prefetch<D, R>(P, cache, cap, scs[first * T::LC], scs[(first + 1) * T::LC], pf, bar, threadIdx.x);
-    }
     if constexpr (ASYNC)
         asm volatile("cp.async.wait_all;" ::: "memory");
     else
