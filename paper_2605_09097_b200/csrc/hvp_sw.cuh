@@ -19,6 +19,8 @@
 // Particle inputs (x + Newton cache) are streamed with TMA bulk copies (cp.async.bulk + mbarrier),
 // the next non-empty layer in flight while the current one computes.
 #pragma once
+#include <cuda.h>  // CUtensorMap (the encoder is fetched at run time: cudaGetDriverEntryPoint)
+
 #include "tiled.cuh"
 
 namespace osmpm {
@@ -118,12 +120,60 @@ __device__ __forceinline__ void sw_stage_tile(const BoxDev& b, const int* t, con
         if (WAIT) asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
+// host: tensor maps of the streamed HVP inputs (x of the particle SoA, the Newton cache) as 2-D
+// tensors [fields][cap] with one box of {PFS particles, all fields}
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static inline PFN_encodeTiled encode_tiled_fn()
+{
+    static PFN_encodeTiled fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(p);
+    }
+    return fn;
+}
+// Shared-memory block of one layer's streamed inputs: x (D fields) then the Newton cache (CL::NF
+// fields), PFS particles per field starting at the 16-B aligned particle lb0 = lb & ~(UE - 1) (<= UE - 1
+// slack + NT particles, rounded to 16 B).  The x block is padded to 128 B so that both blocks are
+// destinations of 2-D tensor copies (128-B aligned shared memory; the tensor start coordinate must
+// be 16-B aligned too: measured, scripts/tma_probe.cu).
+template <int D, typename R> struct SWIn {
+    static constexpr int NF = D + CL<D>::NF;
+    static constexpr int UE = 16 / sizeof(R);
+    static constexpr int PFS = Tile<D>::NT + UE;
+    static constexpr int XB = (int)(((D * PFS * sizeof(R) + 127) / 128 * 128) / sizeof(R));
+    static constexpr int TOT = XB + CL<D>::NF * PFS;
+    static __host__ __device__ constexpr int off(int f) { return f < D ? f * PFS : XB + (f - D) * PFS; }
+};
+static_assert(Tile<3>::NT % 4 == 0 && Tile<2>::NT % 4 == 0, "NT a multiple of the 16-B unit");
+
+template <typename R>
+static inline bool encode_fields_map(CUtensorMap* m, const R* base, int nfields, int64_t cap, int box_particles)
+{
+    PFN_encodeTiled fn = encode_tiled_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)cap, (cuuint64_t)nfields};
+    const cuuint64_t strides[1] = {(cuuint64_t)cap * sizeof(R)};
+    const cuuint32_t box[2] = {(cuuint32_t)box_particles, (cuuint32_t)nfields};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, sizeof(R) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+              const_cast<R*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int D, typename R>
 constexpr size_t hvp_sw_smem_bytes()
 {
     using T = Tile<D>;
-    return 16 + ((size_t)SW<D>::NNP * SVS<D, R>::S + SW<D>::STG +
-                 (OSMPM_SW_L2PF ? (size_t)0 : (size_t)HvpIn<D, R>::NF * HvpIn<D, R>::PFS) +
+    return 16 + 128 /* alignment of the streamed-input block */ + ((size_t)SW<D>::NNP * SVS<D, R>::S + SW<D>::STG +
+                 (OSMPM_SW_L2PF ? (size_t)0 : (size_t)SWIn<D, R>::TOT) +
                  (size_t)SWRec<D, R>::RS * T::NT) *
                     sizeof(R);
 }
@@ -241,7 +291,7 @@ template <int D, typename R>
 __device__ __forceinline__ void sw_prefetch(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, int lb,
                                             int le, R* pf, uint64_t* bar, int lane)
 {
-    using In = HvpIn<D, R>;
+    using In = SWIn<D, R>;
     static_assert(In::NF <= 32, "one field per lane");
     const int lb0 = lb & ~(In::UE - 1);                       // 16-B aligned start
     const int cnt = min(le, lb + Tile<D>::NT) - lb0;
@@ -258,7 +308,38 @@ __device__ __forceinline__ void sw_prefetch(const R* __restrict__ P, const R* __
     __syncwarp();
     if (lane < In::NF) {
         const R* src = (lane < D) ? P + (int64_t)(PL<D>::X + lane) * cap + lb0 : cache + (int64_t)(lane - D) * cap + lb0;
-        bulk_g2s(pf + lane * In::PFS, src, bytes, bar);
+        bulk_g2s(pf + In::off(lane), src, bytes, bar);
+    }
+}
+
+// Two 2-D TMA tensor copies per layer instead of one bulk copy per field: the streamed inputs are the
+// field-major SoA arrays seen as 2-D tensors [fields][particles] (x: 3 fields of the particle SoA,
+// the Newton cache: 17 fields), and one box of {PFS particles, fields} lands exactly in the pf
+// layout (field f at pf + f * PFS).  OSMPM_SW_TMAP=0 selects the per-field bulk copies.
+#ifndef OSMPM_SW_TMAP
+#define OSMPM_SW_TMAP 1
+#endif
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+// boxes of {PFS particles, fields} at the 16-B aligned particle lb0 into the SWIn layout (the tail
+// beyond the particle count reads zeros)
+template <int D, typename R>
+__device__ __forceinline__ void sw_prefetch_tmap(const CUtensorMap* mx, const CUtensorMap* mc, int lb, R* pf,
+                                                 uint64_t* bar, int lane)
+{
+    using In = SWIn<D, R>;
+    if (lane == 0) {
+        const int lb0 = lb & ~(In::UE - 1);
+        fence_async_smem();
+        mbar_expect_tx(bar, (uint32_t)(In::PFS * In::NF * sizeof(R)));
+        tma_2d(pf, mx, lb0, 0, bar);
+        tma_2d(pf + In::XB, mc, lb0, 0, bar);
     }
 }
 
@@ -268,7 +349,8 @@ __device__ __forceinline__ void sw_prefetch(const R* __restrict__ P, const R* __
 template <int D, typename R>
 __global__ void __launch_bounds__(Tile<D>::NT, OSMPM_SW_MINB)
 k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, const int* __restrict__ cell_start,
-         BoxDev b, const double* __restrict__ din, double* __restrict__ yout)
+         BoxDev b, const double* __restrict__ din, double* __restrict__ yout, const __grid_constant__ CUtensorMap tmx,
+         const __grid_constant__ CUtensorMap tmc, int use_tmap)
 {
     using T = Tile<D>;
     using C = CL<D>;
@@ -280,8 +362,15 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
     R* sv = reinterpret_cast<R*>(smem_raw + 16);
     R* stg = sv + S::NNP * SVS<D, R>::S;
-    R* pf = stg + S::STG;
-    R* rec = pf + (OSMPM_SW_L2PF ? 0 : In::NF * In::PFS);
+    // streamed-input block, 128-B aligned for the tensor copies
+    R* pf;
+    {
+        const uint32_t base = smem_u32(smem_raw);
+        const uint32_t off = 16 + (uint32_t)((S::NNP * SVS<D, R>::S + S::STG) * sizeof(R));
+        pf = reinterpret_cast<R*>(smem_raw + (((base + off + 127u) & ~127u) - base));
+    }
+    const bool tmap = OSMPM_SW_TMAP && use_tmap;
+    R* rec = pf + (OSMPM_SW_L2PF ? 0 : SWIn<D, R>::TOT);
     const int tile = blockIdx.x;
     const int64_t kt = (int64_t)tile * T::NC;
     __shared__ int scs[T::NC + 1];  // the tile's cell ranges
@@ -302,7 +391,10 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
         if (ne) {
             const int f = __ffs(ne) - 1;
             const int lb0 = __shfl_sync(0xffffffffu, v, f), le0 = __shfl_sync(0xffffffffu, v, f + 1);
-            sw_prefetch<D, R>(P, cache, cap, lb0, le0, pf, bar, lane);
+            if (tmap)
+                sw_prefetch_tmap<D, R>(&tmx, &tmc, lb0, pf, bar, lane);
+            else
+                sw_prefetch<D, R>(P, cache, cap, lb0, le0, pf, bar, lane);
         }
     }
     if constexpr (ASYNC) sw_stage_tile<D, R, T::NT, false>(b, t, din, sv);
@@ -346,7 +438,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                     // weights and gather temporaries are dead by then).
                     const R* s = pf + (p - pf_base);
                     auto in = [&](int f) -> R {
-                        return from_pf ? s[f * In::PFS]
+                        return from_pf ? s[SWIn<D, R>::off(f)]
                                        : (f < D ? P[(int64_t)(PL<D>::X + f) * cap + p] : cache[(int64_t)(f - D) * cap + p]);
                     };
                     R x[3];
@@ -419,9 +511,13 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                 __syncthreads();  // records ready; the streamed buffer is free
                 if (sb == lb) {
                     if (from_pf) parity ^= 1u;
-                    if (threadIdx.x < 32 && next < T::NL)
-                        sw_prefetch<D, R>(P, cache, cap, scs[next * T::LC], scs[(next + 1) * T::LC], pf, bar,
-                                          threadIdx.x);
+                    if (threadIdx.x < 32 && next < T::NL) {
+                        if (tmap)
+                            sw_prefetch_tmap<D, R>(&tmx, &tmc, scs[next * T::LC], pf, bar, threadIdx.x);
+                        else
+                            sw_prefetch<D, R>(P, cache, cap, scs[next * T::LC], scs[(next + 1) * T::LC], pf, bar,
+                                              threadIdx.x);
+                    }
                 }
                 if (it < T::ITEMS) {
                     const int p0 = max(ks, sb), p1 = min(ke, se);

@@ -148,6 +148,11 @@ struct Sub : public osmpm_subdomain {
     DBuf<int> bounds;
     int* h_bounds = nullptr;
     int part_off = 0;  // this slab's block-partial offset inside its group's partial buffers
+    CUtensorMap tm_x{}, tm_c{};  // HVP streamed-input tensor maps (hvp_sw.cuh) and what they describe
+    const void* tm_P = nullptr;
+    const void* tm_C = nullptr;
+    int64_t tm_cap = -1;
+    bool tm_ok = false;
 
     // ---- slab decomposition --------------------------------------------------
     // cells [cut_lo, cut_hi) along x (INT32_MIN / INT32_MAX: open end).  A slab with a right
@@ -691,8 +696,20 @@ struct Sub : public osmpm_subdomain {
                                      (int)hvp_sw_smem_bytes<D, R>());
                 attr3 = true;
             }
-            KC(); k_hvp_sw<D, R><<<box.ntiles, T::NT, hvp_sw_smem_bytes<D, R>(), st()>>>(P.p, cache.p, cap,
-                                                                                         cell_start.p, box, din, yout);
+            // tensor maps of the streamed inputs, re-encoded when a buffer moves (the sort swaps P)
+            if (tm_P != P.p || tm_C != cache.p || tm_cap != cap) {
+                tm_ok = !(getenv("OSMPM_HVP_TMA") && std::string(getenv("OSMPM_HVP_TMA")) == "0") &&
+                        encode_fields_map<R>(&tm_x, P.p + (size_t)PL<D>::X * cap, D, cap, SWIn<D, R>::PFS) &&
+                        encode_fields_map<R>(&tm_c, cache.p, C::NF, cap, SWIn<D, R>::PFS);
+                tm_P = P.p;
+                tm_C = cache.p;
+                tm_cap = cap;
+                if (getenv("OSMPM_DEBUG_TMA"))
+                    fprintf(stderr, "[osmpm] hvp tensor maps: cap=%lld P=%p cache=%p ok=%d ntiles=%d\n", (long long)cap,
+                            (const void*)P.p, (const void*)cache.p, (int)tm_ok, (int)box.ntiles);
+            }
+            KC(); k_hvp_sw<D, R><<<box.ntiles, T::NT, hvp_sw_smem_bytes<D, R>(), st()>>>(
+                P.p, cache.p, cap, cell_start.p, box, din, yout, tm_x, tm_c, tm_ok ? 1 : 0);
         }
         OSMPM_LAUNCH_CHECK();
         if (pf.on) pf.end("hvp", st());
