@@ -4,6 +4,7 @@ the oracle's static solution at the coarsest resolution."""
 import os
 import sys
 
+import numpy as np
 import pytest
 
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
@@ -27,3 +28,37 @@ def test_gpu_cantilever_equals_oracle():
     tg, _, _ = eb.run_gpu(0.05)
     to, _, _ = eb.run_oracle(0.05)
     assert tg == pytest.approx(to, rel=1e-8)
+
+
+# Hertz line contact (§4.2; G7) through the C ABI: the same static unilateral-contact
+# driver as the oracle pin (scripts/hertz.py), refined to dx = 1/256 (103k particles; the paper refines
+# h_S to 5e-3).  Beyond that the nodal gap contact of DESIGN.md R19 breaks down (measured at 1/512: the
+# gap at the contact edge exceeds a cell and the edge nodes carry only the tail of the B-spline
+# support; the pressure profile oscillates there), which is a limit of that reading, not of the path.
+import hertz as hz  # noqa: E402
+
+
+def test_gpu_hertz_contact_converges_to_closed_form():
+    b_ref, p_ref = hz.hertz()
+    ns = (64, 128, 256)
+    res = {n: hz.run_gpu(n) for n in ns}
+    for r in res.values():
+        assert r["F"] == pytest.approx(hz.F_LINE, rel=1e-5)
+    eb_ = [res[n]["b"] / b_ref - 1 for n in ns]
+    ep_ = [res[n]["p0"] / p_ref - 1 for n in ns]
+    assert all(e > 0 for e in eb_) and all(e < 0 for e in ep_)
+    assert all(1.8 < a / b < 2.5 for a, b in zip(eb_, eb_[1:]))     # first order in dx
+    assert all(1.8 < a / b < 2.5 for a, b in zip(ep_, ep_[1:]))
+    assert eb_[-1] < 0.06 and ep_[-1] > -0.04
+    # Richardson extrapolation of the finest pair lands on Hertz
+    assert (2 * res[256]["b"] - res[128]["b"]) / b_ref == pytest.approx(1, abs=0.01)
+    assert (2 * res[256]["p0"] - res[128]["p0"]) / p_ref == pytest.approx(1, abs=0.01)
+
+
+def test_gpu_hertz_equals_oracle():
+    g = hz.run_gpu(64)
+    o = hz.run_oracle(64)
+    assert g["rounds"] == o["rounds"]
+    np.testing.assert_array_equal(g["xc"], o["xc"])
+    assert np.abs(g["p"] - o["p"]).max() <= 1e-7 * np.abs(o["p"]).max()
+    assert g["b"] == pytest.approx(o["b"], rel=1e-8) and g["p0"] == pytest.approx(o["p0"], rel=1e-8)

@@ -53,3 +53,36 @@ def test_oracle_cantilever_quasi_static():
     act = gs.active.astype(bool)
     t20 = eb.tip_deflection(sc.particles.x, oracle.g2p(sc, np.where(act[:, None], u / sc.dt, 0.0)).x)
     assert abs(t20 - t10) / t10 < 0.01
+
+
+# --------------------------------------------------------------------------------------------------
+# Hertz line contact (§4.2; tests/golden/g7_hertz.txt), scripts/hertz.py: a
+# semi-circular cylinder on a rigid frictionless plane under a body load of resultant F, static
+# single-domain MPM with unilateral gap contact at the plane nodes.  The paper reports that the
+# profile converges to the Hertz semi-ellipse "with the error reducing approximately linearly with
+# mesh element size"; the oracle must do the same and its Richardson extrapolation
+# must land on the closed-form half-width and peak pressure.
+import hertz as hz  # noqa: E402
+
+
+def test_hertz_golden_matches_closed_form():
+    R, E, nu, F, b, pmax = read_golden("g7_hertz.txt")[0]
+    assert (hz.R, hz.E, hz.NU, hz.F_LINE) == (R, E, nu, F)
+    bb, pp = hz.hertz(F)
+    assert bb == pytest.approx(b, rel=1e-6) and pp == pytest.approx(pmax, rel=1e-6)
+
+
+def test_oracle_hertz_contact_converges_to_closed_form():
+    b_ref, p_ref = hz.hertz()
+    res = {n: hz.run_oracle(n) for n in (32, 64)}
+    for r in res.values():
+        assert r["F"] == pytest.approx(hz.F_LINE, rel=1e-5)        # plane reactions balance the load
+        assert r["stats"].status == 0
+    err_b = {n: r["b"] / b_ref - 1 for n, r in res.items()}
+    err_p = {n: r["p0"] / p_ref - 1 for n, r in res.items()}
+    # too wide and too low (diffuse MPM boundary), first order in dx
+    assert 0 < err_b[64] < err_b[32] < 0.6 and err_p[32] < err_p[64] < 0
+    assert 1.8 < err_b[32] / err_b[64] < 2.6 and 1.8 < err_p[32] / err_p[64] < 2.3
+    # Richardson extrapolation of the first-order sequence lands on Hertz
+    assert (2 * res[64]["b"] - res[32]["b"]) / b_ref == pytest.approx(1, abs=0.06)
+    assert (2 * res[64]["p0"] - res[32]["p0"]) / p_ref == pytest.approx(1, abs=0.02)
