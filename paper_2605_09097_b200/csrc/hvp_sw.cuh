@@ -105,16 +105,42 @@ template <int D, typename R, int NTHR, bool WAIT = true>
 __device__ __forceinline__ void sw_stage_tile(const BoxDev& b, const int* t, const double* __restrict__ src, R* sv)
 {
     using T = Tile<D>;
-    for (int idx = threadIdx.x; idx < T::NN * D; idx += NTHR) {
-        const int a = idx % D, l = idx / D;
-        int c[3];
-        tnode_coords<D>(l, c);
-        const int64_t g = box_node<D>(b, t[0] * T::T0 + c[0], t[1] * T::T1 + c[1], t[2] * T::T2 + c[2]);
-        R* dst = sv + sv_elem<D, R>(sw_node<D>(c[0], c[1], c[2]), a, SW<D>::NNP);
-        if constexpr (sizeof(R) == 8)
-            cp_async_8(dst, src + g * D + a);
-        else
-            *dst = (R)src[g * D + a];
+    constexpr int ROWS = T::N0 * T::N1, RL = T::N2 * D;  // 3D: rows along z are contiguous in global memory
+    if constexpr (D == 3 && NTHR % ROWS == 0) {
+        // thread -> (row, part): one row base address per thread, then every TPR-th element of the row
+        // with its (node, component) advanced incrementally (no per-element index divisions)
+        constexpr int TPR = NTHR / ROWS;
+        const int row = threadIdx.x / TPR, part = threadIdx.x % TPR;
+        const int c0 = row / T::N1, c1 = row % T::N1;
+        const double* gs = src + box_node<D>(b, t[0] * T::T0 + c0, t[1] * T::T1 + c1, t[2] * T::T2) * D;
+        const int n0 = sw_node<D>(c0, c1, 0);
+        int z = part / D, a = part % D;
+#pragma unroll
+        for (int e = part; e < RL; e += TPR) {
+            R* dst = sv + sv_elem<D, R>(n0 + z, a, SW<D>::NNP);
+            if constexpr (sizeof(R) == 8)
+                cp_async_8(dst, gs + e);
+            else
+                *dst = (R)gs[e];
+            a += TPR % D;
+            z += TPR / D;
+            if (a >= D) {
+                a -= D;
+                z += 1;
+            }
+        }
+    } else {
+        for (int idx = threadIdx.x; idx < T::NN * D; idx += NTHR) {
+            const int a = idx % D, l = idx / D;
+            int c[3];
+            tnode_coords<D>(l, c);
+            const int64_t g = box_node<D>(b, t[0] * T::T0 + c[0], t[1] * T::T1 + c[1], t[2] * T::T2 + c[2]);
+            R* dst = sv + sv_elem<D, R>(sw_node<D>(c[0], c[1], c[2]), a, SW<D>::NNP);
+            if constexpr (sizeof(R) == 8)
+                cp_async_8(dst, src + g * D + a);
+            else
+                *dst = (R)src[g * D + a];
+        }
     }
     if constexpr (sizeof(R) == 8)
         if (WAIT) asm volatile("cp.async.wait_all;" ::: "memory");
@@ -240,6 +266,11 @@ __device__ __forceinline__ void sw_gather(const R* sv, const int* lc, const R (*
 }
 
 // item (cell, a, i): emit the completed kk = 0 plane into the staging slots, shift the window
+template <int V> struct ICst { static constexpr int value = V; };
+#ifndef OSMPM_SW_P1SPLIT
+#define OSMPM_SW_P1SPLIT 1
+#endif
+
 template <int D, typename R>
 __device__ __forceinline__ void sw_emit(int cellL, int a, int i, R* acc, R* stg)
 {
@@ -346,8 +377,13 @@ __device__ __forceinline__ void sw_prefetch_tmap(const CUtensorMap* mx, const CU
 #ifndef OSMPM_SW_MINB
 #define OSMPM_SW_MINB 3
 #endif
+// fp32 variant: half the shared memory (records, streamed inputs, node tile and staging in fp32) and
+// fewer live registers, so more CTAs fit per SM
+#ifndef OSMPM_SW_MINB_F32
+#define OSMPM_SW_MINB_F32 5
+#endif
 template <int D, typename R>
-__global__ void __launch_bounds__(Tile<D>::NT, OSMPM_SW_MINB)
+__global__ void __launch_bounds__(Tile<D>::NT, sizeof(R) == 8 ? OSMPM_SW_MINB : OSMPM_SW_MINB_F32)
 k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, const int* __restrict__ cell_start,
          BoxDev b, const double* __restrict__ din, double* __restrict__ yout, const __grid_constant__ CUtensorMap tmx,
          const __grid_constant__ CUtensorMap tmc, int use_tmap)
@@ -432,14 +468,23 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                 const bool from_pf = !OSMPM_SW_L2PF && (sb == lb);
                 if (sb != lb) __syncthreads();  // previous chunk's records consumed
                 if (from_pf) mbar_wait(bar, parity);
-                if (p < se) {
-                    // streamed field f of particle p: the smem copy (first chunk) or global memory.
-                    // The Newton cache is read only after the gather (register pressure: the
-                    // weights and gather temporaries are dead by then).
+                // phase 1, instantiated for the two sources of the streamed fields (the shared-memory copy
+                // of the first chunk; global memory for the rare further chunks of a layer holding more
+                // than NT particles) so that the common path carries no predicated global loads
+                auto phase1 = [&](auto fromc) {
+                    constexpr int FROM = decltype(fromc)::value;  // 1 smem, 0 global, 2 either (runtime)
+                    // streamed field f of particle p.  The Newton cache is read only after the gather
+                    // (register pressure: the weights and gather temporaries are dead by then).
                     const R* s = pf + (p - pf_base);
                     auto in = [&](int f) -> R {
-                        return from_pf ? s[SWIn<D, R>::off(f)]
-                                       : (f < D ? P[(int64_t)(PL<D>::X + f) * cap + p] : cache[(int64_t)(f - D) * cap + p]);
+                        if constexpr (FROM == 1)
+                            return s[SWIn<D, R>::off(f)];
+                        else if constexpr (FROM == 0)
+                            return f < D ? P[(int64_t)(PL<D>::X + f) * cap + p] : cache[(int64_t)(f - D) * cap + p];
+                        else
+                            return from_pf ? s[SWIn<D, R>::off(f)]
+                                           : (f < D ? P[(int64_t)(PL<D>::X + f) * cap + p]
+                                                    : cache[(int64_t)(f - D) * cap + p]);
                     };
                     R x[3];
 #pragma unroll
@@ -507,6 +552,14 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                             for (int bb = 0; bb < D; ++bb) *r.at(Rec<D>::G + a * D + bb) = Ga[bb];
                         }
                     }
+                };
+                if (p < se) {
+                    if (!OSMPM_SW_P1SPLIT)
+                        phase1(ICst<2>{});
+                    else if (from_pf)
+                        phase1(ICst<1>{});
+                    else
+                        phase1(ICst<0>{});
                 }
                 __syncthreads();  // records ready; the streamed buffer is free
                 if (sb == lb) {
