@@ -405,7 +405,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
         const uint32_t off = 16 + (uint32_t)((S::NNP * SVS<D, R>::S + S::STG) * sizeof(R));
         pf = reinterpret_cast<R*>(smem_raw + (((base + off + 127u) & ~127u) - base));
     }
-    const bool tmap = OSMPM_SW_TMAP && use_tmap;
+    const bool tmap = OSMPM_SW_TMAP && !OSMPM_SW_L2PF && use_tmap;  // L2PF has no shared-memory input block
     R* rec = pf + (OSMPM_SW_L2PF ? 0 : SWIn<D, R>::TOT);
     const int tile = blockIdx.x;
     const int64_t kt = (int64_t)tile * T::NC;
