@@ -147,6 +147,33 @@ def hvp_algorithmic_bytes(n_particles, n_active_nodes, word):
     return n_particles * 20 * word + n_active_nodes * 6 * 8
 
 
+def transfer_rooflines(fam, n_particles, n_active_nodes, word, peak):
+    """Algorithmic HBM GB/s of the per-step transfer kernels (BASELINE.json metric "HVP/P2G HBM GB/s"),
+    from the event-timed scopes (the sort runs inside the P2G scope).  Bytes per unit:
+      sort  keys (read x: 3 words, write key + index: 8 B) + permute (read and write the 26-word SoA
+            plus material, flag and id: 9 B) per particle;
+      p2g   read the sorted 26-word SoA per particle, write m, mv, f^sigma (7 fp64) per active node;
+      g2p   read x, F (12 words) and write x, v, F, B (24 words) per particle, read v (3 fp64) per
+            active node."""
+    out = {}
+    per_launch = {
+        "sort": n_particles * (3 * word + 8 + 2 * (26 * word + 9)),
+        "p2g": n_particles * 26 * word + n_active_nodes * 7 * 8,
+        "g2p": n_particles * 36 * word + n_active_nodes * 3 * 8,
+    }
+    s_n, s_ms = fam.get("sort", (0, 0.0))
+    for k, by in per_launch.items():
+        n, ms = fam.get(k, (0, 0.0))
+        if k == "p2g":
+            ms -= s_ms
+        if not n or ms <= 0:
+            continue
+        gbs = by / (ms / n * 1e-3) / 1e9
+        out[k] = {"achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                  "algorithmic_bytes_per_launch": by, "avg_launch_ms": ms / n}
+    return out
+
+
 def load_traffic(prec):
     path = os.path.join(ROOT, "profiles", f"ncu_hvp_{prec}.json")
     if os.path.exists(path):
@@ -452,6 +479,7 @@ def main():
                                   "flops_per_particle": HVP_FLOPS_PER_PARTICLE, "peak_kind": "derived (DESIGN.md §5)"}
                                  if hv_n else None)},
         "kernel_ms_per_step": {f: v[1] / args.steps for f, v in fam.items()},
+        "transfer_rooflines": transfer_rooflines(fam, n_local, n_active, word, peak),
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches_timed,

@@ -348,8 +348,11 @@ __global__ void k_energy(const R* __restrict__ P, int64_t cap, int64_t n, const 
 // =============================================================================================
 // a8: G2P + F update + advection, per particle
 // =============================================================================================
+#ifndef OSMPM_G2P_MINB
+#define OSMPM_G2P_MINB 4
+#endif
 template <int D, typename R>
-__global__ void k_g2p(R* __restrict__ P, int64_t cap, int64_t n, const int* __restrict__ pid, BoxDev b,
+__global__ void __launch_bounds__(128, OSMPM_G2P_MINB) k_g2p(R* __restrict__ P, int64_t cap, int64_t n, const int* __restrict__ pid, BoxDev b,
                       const double* __restrict__ vg, double dt, ErrLatch* err)
 {
     using L = PL<D>;
@@ -363,43 +366,86 @@ __global__ void k_g2p(R* __restrict__ P, int64_t cap, int64_t n, const int* __re
         c[a] = base_of<R>(P[(L::X + a) * cap + p], b.o[a], b.inv_dx, &f[a]) - b.lo[a];
         bspline<R>(f[a], inv_dx, w[a], dw[a]);
     }
+    // tensor-product gather (contract the last axis first): per component a the seven sums
+    //   N v, dN/dx_b v (b < D), N v (l_b - f_b) (b < D)
+    // with per-axis weight sets w, dw and wo = w (l - f) (the node offset taken per node, so
+    // B_p = dx sum N v (l - f)^T carries no cancellation), 147 FMA per component in 3D instead of the
+    // per-node products of N, grad N and the offsets
+    R wo[3][3];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int l = 0; l < 3; ++l) wo[a][l] = w[a][l] * (R(l) - f[a]);
     R vp[D], Bp[D * D], gv[D * D];
 #pragma unroll
-    for (int a = 0; a < D; ++a) vp[a] = 0;
+    for (int a = 0; a < D; ++a) {
+        vp[a] = 0;
 #pragma unroll
-    for (int k = 0; k < D * D; ++k) Bp[k] = gv[k] = 0;
+        for (int bb = 0; bb < D; ++bb) Bp[a * D + bb] = gv[a * D + bb] = 0;
+    }
+    if (D == 3) {
 #pragma unroll
-    for (int i = 0; i < 3; ++i)
+        for (int i = 0; i < 3; ++i) {
+            R Yww[3] = {0, 0, 0}, Ydw[3] = {0, 0, 0}, Yow[3] = {0, 0, 0}, Ywd[3] = {0, 0, 0}, Ywo[3] = {0, 0, 0};
 #pragma unroll
-        for (int j = 0; j < 3; ++j)
+            for (int j = 0; j < 3; ++j) {
+                const double* vv = vg + box_node<D>(b, c[0] + i, c[1] + j, c[2]) * D;
+                R Zw[3] = {0, 0, 0}, Zd[3] = {0, 0, 0}, Zo[3] = {0, 0, 0};
 #pragma unroll
-            for (int k = 0; k < Tile<D>::K3; ++k) {
-                R N, gN[3], off[3];
-                off[0] = dx * (R(i) - f[0]);
-                off[1] = dx * (R(j) - f[1]);
-                if (D == 3) {
-                    off[2] = dx * (R(k) - f[2]);
-                    N = w[0][i] * w[1][j] * w[2][k];
-                    gN[0] = dw[0][i] * w[1][j] * w[2][k];
-                    gN[1] = w[0][i] * dw[1][j] * w[2][k];
-                    gN[2] = w[0][i] * w[1][j] * dw[2][k];
-                } else {
-                    N = w[0][i] * w[1][j];
-                    gN[0] = dw[0][i] * w[1][j];
-                    gN[1] = w[0][i] * dw[1][j];
-                }
-                const double* vv = vg + box_node<D>(b, c[0] + i, c[1] + j, c[2] + k) * D;
+                for (int k = 0; k < 3; ++k)
 #pragma unroll
-                for (int a = 0; a < D; ++a) {
-                    const R va = (R)vv[a];
-                    vp[a] += N * va;
-#pragma unroll
-                    for (int bb = 0; bb < D; ++bb) {
-                        Bp[a * D + bb] += N * va * off[bb];
-                        gv[a * D + bb] += va * gN[bb];
+                    for (int a = 0; a < 3; ++a) {
+                        const R va = (R)vv[k * 3 + a];
+                        Zw[a] = fma(w[2][k], va, Zw[a]);
+                        Zd[a] = fma(dw[2][k], va, Zd[a]);
+                        Zo[a] = fma(wo[2][k], va, Zo[a]);
                     }
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    Yww[a] = fma(w[1][j], Zw[a], Yww[a]);
+                    Ydw[a] = fma(dw[1][j], Zw[a], Ydw[a]);
+                    Yow[a] = fma(wo[1][j], Zw[a], Yow[a]);
+                    Ywd[a] = fma(w[1][j], Zd[a], Ywd[a]);
+                    Ywo[a] = fma(w[1][j], Zo[a], Ywo[a]);
                 }
             }
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                vp[a] = fma(w[0][i], Yww[a], vp[a]);
+                gv[a * 3 + 0] = fma(dw[0][i], Yww[a], gv[a * 3 + 0]);
+                gv[a * 3 + 1] = fma(w[0][i], Ydw[a], gv[a * 3 + 1]);
+                gv[a * 3 + 2] = fma(w[0][i], Ywd[a], gv[a * 3 + 2]);
+                Bp[a * 3 + 0] = fma(wo[0][i], Yww[a], Bp[a * 3 + 0]);
+                Bp[a * 3 + 1] = fma(w[0][i], Yow[a], Bp[a * 3 + 1]);
+                Bp[a * 3 + 2] = fma(w[0][i], Ywo[a], Bp[a * 3 + 2]);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const double* vv = vg + box_node<D>(b, c[0] + i, c[1], 0) * D;
+            R Yw[2] = {0, 0}, Yd[2] = {0, 0}, Yo[2] = {0, 0};
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+                for (int a = 0; a < 2; ++a) {
+                    const R va = (R)vv[j * 2 + a];
+                    Yw[a] = fma(w[1][j], va, Yw[a]);
+                    Yd[a] = fma(dw[1][j], va, Yd[a]);
+                    Yo[a] = fma(wo[1][j], va, Yo[a]);
+                }
+#pragma unroll
+            for (int a = 0; a < 2; ++a) {
+                vp[a] = fma(w[0][i], Yw[a], vp[a]);
+                gv[a * 2 + 0] = fma(dw[0][i], Yw[a], gv[a * 2 + 0]);
+                gv[a * 2 + 1] = fma(w[0][i], Yd[a], gv[a * 2 + 1]);
+                Bp[a * 2 + 0] = fma(wo[0][i], Yw[a], Bp[a * 2 + 0]);
+                Bp[a * 2 + 1] = fma(w[0][i], Yo[a], Bp[a * 2 + 1]);
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) Bp[k] *= dx;
     R F[D * D], Fn[D * D];
 #pragma unroll
     for (int k = 0; k < D * D; ++k) F[k] = P[(L::F + k) * cap + p];
