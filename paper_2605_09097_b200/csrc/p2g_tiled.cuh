@@ -84,17 +84,27 @@ __device__ __forceinline__ void p2g_tile_flush(const BoxDev& b, const int* t, co
     }
 }
 
+// the three fields (momentum, stress force, mass) are staged together, one zero / stage / flush
+// sequence (three barriers) per layer instead of one per field (nine)
+template <int D> struct P2GStageAll {
+    static constexpr int SP = P2GStage<D, D>::SIZE, SM1 = P2GStage<D, 1>::SIZE;
+    static constexpr int SIZE = 2 * SP + SM1;
+};
+
 template <int D, typename R>
 constexpr size_t p2g_tiled_smem_bytes()
 {
     using T = Tile<D>;
     constexpr size_t rec = (size_t)P2GRec<D>::RS * T::NT;
-    constexpr size_t stg = (size_t)P2GStage<D, D>::SIZE;
+    constexpr size_t stg = ((size_t)P2GStageAll<D>::SIZE + 1) / 2 * 2;  // 16-B multiple for the zeroing
     return ((size_t)T::NN * (1 + 2 * D) + (rec > stg ? rec : stg)) * sizeof(R);
 }
 
+#ifndef OSMPM_P2G_MINB
+#define OSMPM_P2G_MINB 2
+#endif
 template <int D, typename R>
-__global__ void __launch_bounds__(Tile<D>::NT)
+__global__ void __launch_bounds__(Tile<D>::NT, OSMPM_P2G_MINB)
 k_p2g_tiled(const R* __restrict__ P, int64_t cap, const int* __restrict__ mat, const int* __restrict__ cell_start,
             BoxDev b, MatTable mt, double* __restrict__ m, double* __restrict__ mom, double* __restrict__ fsig)
 {
@@ -180,7 +190,8 @@ k_p2g_tiled(const R* __restrict__ P, int64_t cap, const int* __restrict__ mat, c
             __syncthreads();  // records ready
             if (it < T::ITEMS) {
                 const int p0 = max(ks, sb), p1 = min(ke, se);
-                const int len = p1 - p0, rot = len > 0 ? (icell & 7) % len : 0;
+                const int len = p1 - p0, r7 = icell & 7;
+                const int rot = r7 < len ? r7 : (len > 0 ? r7 % len : 0);
                 for (int k = 0; k < len; ++k) {
                     const RecPtr<R> r(rec, rotated(p0, len, k, rot) - sb, RS);
                     ItemW<D, R> W;
@@ -218,18 +229,26 @@ k_p2g_tiled(const R* __restrict__ P, int64_t cap, const int* __restrict__ mat, c
             __syncthreads();  // records consumed
         }
         // momentum, stress force, mass: stage -> fixed-order slot sums -> node tiles
-        for (int fld = 0; fld < 3; ++fld) {
-            stage_zero<D, R>(stg);
-            __syncthreads();
-            if (it < T::ITEMS) {
-                if (fld == 0) p2g_stage<D, R, D>(icell, icomp, ii, accp, stg);
-                if (fld == 1) p2g_stage<D, R, D>(icell, icomp, ii, accf, stg);
-                if (fld == 2 && icomp == 0) p2g_stage<D, R, 1>(icell, 0, ii, accm, stg);
+        {
+            using SA = P2GStageAll<D>;
+            R* stgp = stg;
+            R* stgf = stg + SA::SP;
+            R* stgm = stg + 2 * SA::SP;
+            {
+                constexpr int UE = 16 / sizeof(R);
+                const int4 z = make_int4(0, 0, 0, 0);
+                for (int u = threadIdx.x; u < (SA::SIZE + UE - 1) / UE; u += T::NT) reinterpret_cast<int4*>(stg)[u] = z;
             }
             __syncthreads();
-            if (fld == 0) p2g_layer_flush<D, R, D>(layer, stg, sp);
-            if (fld == 1) p2g_layer_flush<D, R, D>(layer, stg, sf);
-            if (fld == 2) p2g_layer_flush<D, R, 1>(layer, stg, sm);
+            if (it < T::ITEMS) {
+                p2g_stage<D, R, D>(icell, icomp, ii, accp, stgp);
+                p2g_stage<D, R, D>(icell, icomp, ii, accf, stgf);
+                if (icomp == 0) p2g_stage<D, R, 1>(icell, 0, ii, accm, stgm);
+            }
+            __syncthreads();
+            p2g_layer_flush<D, R, D>(layer, stgp, sp);
+            p2g_layer_flush<D, R, D>(layer, stgf, sf);
+            p2g_layer_flush<D, R, 1>(layer, stgm, sm);
             __syncthreads();
         }
     }
