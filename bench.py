@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--cg", type=int, default=50)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip the fp32-variant sub-run that a 1-GPU f64 run reports under `variants`")
     ap.add_argument("--no-prof", action="store_true", help="skip the per-kernel event timing (A/B of its overhead)")
     ap.add_argument("--cpu-cells", type=int, default=14, help="oracle sample cube side (cells)")
     ap.add_argument("--slabs", type=int, default=1,
@@ -145,6 +147,24 @@ def hvp_algorithmic_bytes(n_particles, n_active_nodes, word):
     # per particle: x (3) + Newton cache S' (6) + Ah (9) + c' + l' (2) = 20 words of the particle
     # precision; per active node: read d (3) + write y (3) fp64 words
     return n_particles * 20 * word + n_active_nodes * 6 * 8
+
+
+def fp32_variant(args):
+    """The same C5 sub-step with the fp32 HVP variant (BASELINE.json configs[4] names fp32 and fp64;
+    DESIGN.md R14: particle storage and HVP arithmetic fp32, node vectors and the gradient fp64),
+    measured device-only in a child process of this bench (same steps / warm-up)."""
+    import subprocess
+    cmd = [sys.executable, os.path.abspath(__file__), "--precision", "f32", "--steps", str(args.steps), "--warmup",
+           str(args.warmup), "--cells", str(args.cells), "--newton", str(args.newton), "--cg", str(args.cg),
+           "--no-e2e", "--no-cpu-baseline", "--no-variants"]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        d = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as e:  # reported, not fatal: the f64 line stands on its own
+        return {"unavailable": f"{type(e).__name__}: {e}"[:200]}
+    return {"value": d["value"], "unit": d["unit"], "ms_per_step": d["ms_per_step"], "dtype": d["dtype"],
+            "roofline": {k: d["roofline"].get(k) for k in ("achieved", "peak", "frac", "avg_launch_ms", "traffic")},
+            "kernel_ms_per_step": d["kernel_ms_per_step"], "clocks": d.get("clocks")}
 
 
 def transfer_rooflines(fam, n_particles, n_active_nodes, word, peak):
@@ -485,6 +505,8 @@ def main():
         "gpu_launches": launches_timed,
         "clocks": ck,
     }
+    if world == 1 and args.precision == "f64" and not args.no_variants and args.slabs == 1:
+        line["variants"] = {"f32": fp32_variant(args)}
     print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
