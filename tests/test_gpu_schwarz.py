@@ -94,3 +94,23 @@ def test_substep_contract(ctx):
     for m in range(1, 5):
         st = cpl.substep(m)
         assert st.status == 0
+
+
+@pytest.mark.parametrize("M", [2, 4])
+def test_free_fall_is_the_converged_frame(ctx, M):
+    """The GPU frame converges to backward-Euler free fall on both grids (the fixed point exists only
+    with alpha = m / M in the temporal interpolation; tests/test_oracle_schwarz.py)."""
+    from paper_2605_09097_b200 import osmpm
+    import test_oracle_schwarz as TOS
+    coarse, fine, c, g = TOS._falling_pair(M)
+    sb = make_sub(ctx, coarse)
+    ss = make_sub(ctx, fine)
+    st = osmpm.schwarz_settings(M=M, eps_conv=1e-10, k_max=200, eps_tol=-1.0,
+                                coarse=osmpm.newton_settings(**TIGHT), fine=osmpm.newton_settings(**TIGHT))
+    rep = osmpm.Coupler(sb, ss, st).step()
+    assert rep.iters < 60
+    for sub, sc, n in ((ss, fine, M), (sb, coarse, 1)):
+        out = sub.read_particles()
+        x, v = TOS.free_fall_closed_form(sc.particles.x, c, g, sc.dt, n)
+        np.testing.assert_allclose(out["v"], np.tile(v, (sc.particles.n, 1)), rtol=0, atol=1e-8)
+        np.testing.assert_allclose(out["x"], x, rtol=0, atol=1e-10)

@@ -1,5 +1,6 @@
 """Pins of the oracle's Schwarz frame (O11-O12): arbitration rules, exact reproduction of uniform
-translation for any M and resolution ratio, contraction of the interface residuals, parity mode
+translation for any M and resolution ratio, free fall as the converged frame (pins the temporal
+interpolation alpha = m / M), contraction of the interface residuals, parity mode
 (PAPER.md:294-301, 436-501)."""
 import numpy as np
 import pytest
@@ -67,6 +68,41 @@ def test_uniform_translation_is_reproduced_exactly(M):
         np.testing.assert_allclose(pt.x, x0 + coarse.dt * c, rtol=0, atol=1e-12)
         np.testing.assert_allclose(pt.F, np.broadcast_to(np.eye(2), pt.F.shape), rtol=0, atol=1e-10)
     assert res.r_B[-1] < 1e-10 and res.r_S[-1] < 1e-10
+
+
+def _falling_pair(M, c=(0.3, -0.2), g=(0.5, -9.81)):
+    coarse, fine = synth.c1_cantilever(g=0.0)
+    for sc in (coarse, fine):
+        sc.particles.v[:] = np.asarray(c)
+        sc.gravity = (g[0], g[1], 0.0)
+    fine.dt = coarse.dt / M
+    return coarse, fine, np.asarray(c), np.asarray(g)
+
+
+def free_fall_closed_form(x0, c, g, dt, n):
+    """n backward-Euler steps of free fall: v_m = c + m dt g, x_m = x_{m-1} + dt v_m."""
+    return x0 + n * dt * c + dt * dt * g * n * (n + 1) / 2, c + n * dt * g
+
+
+@pytest.mark.parametrize("M", [2, 4])
+def test_free_fall_is_the_converged_frame(M):
+    # Uniform free fall is a fixed point of the whole frame only if the fine receivers get the
+    # coarse velocity at the sub-step's own time, (1 - alpha) v_B^n + alpha v_B^(n+1) with alpha = m/M
+    # (PAPER.md:349-354, Eq. temporal_interp): backward Euler then gives every fine particle
+    # v = c + m dt g after sub-step m.  The iteration starts from Pi(v_S^n) = c on the coarse receivers
+    # (R16), so it converges to that closed form instead of reproducing it at k = 1.
+    coarse, fine, c, g = _falling_pair(M)
+    x0c, x0f = coarse.particles.x.copy(), fine.particles.x.copy()
+    res = S.schwarz_step(coarse, fine, M, eps_conv=1e-10, k_max=200)
+    assert res.converged and res.iters < 60
+    xf, vf = free_fall_closed_form(x0f, c, g, fine.dt, M)
+    xc, vc = free_fall_closed_form(x0c, c, g, coarse.dt, 1)
+    np.testing.assert_allclose(res.fine_particles.v, np.tile(vf, (fine.particles.n, 1)), rtol=0, atol=1e-8)
+    np.testing.assert_allclose(res.coarse_particles.v, np.tile(vc, (coarse.particles.n, 1)), rtol=0, atol=1e-8)
+    np.testing.assert_allclose(res.fine_particles.x, xf, rtol=0, atol=1e-10)
+    np.testing.assert_allclose(res.coarse_particles.x, xc, rtol=0, atol=1e-10)
+    np.testing.assert_allclose(res.fine_particles.F, np.broadcast_to(np.eye(2), res.fine_particles.F.shape),
+                               rtol=0, atol=1e-9)
 
 
 def test_cantilever_frame_converges_with_contracting_residuals():
