@@ -62,3 +62,28 @@ def test_gpu_hertz_equals_oracle():
     np.testing.assert_array_equal(g["xc"], o["xc"])
     assert np.abs(g["p"] - o["p"]).max() <= 1e-7 * np.abs(o["p"]).max()
     assert g["b"] == pytest.approx(o["b"], rel=1e-8) and g["p0"] == pytest.approx(o["p0"], rel=1e-8)
+
+
+# Eshelby misfit inclusion (§4.3; G8) through the C ABI, refined to dx = 1/512 (3.1 M
+# particles in the matrix disk) for the paper's three stiffness ratios.
+import eshelby as es  # noqa: E402
+
+
+@pytest.mark.parametrize("ratio", [1.0, 2.0, 5.0])
+def test_gpu_eshelby_converges_to_lame(ratio):
+    ns = (64, 128, 256, 512)
+    res = {n: es.run_gpu(n, ratio) for n in ns}
+    err_o = [res[n]["err_out"] for n in ns]
+    err_p = [abs(res[n]["p_in"] / res[n]["p_ref"] - 1) for n in ns]
+    assert err_o[-1] < 0.006 and err_p[-1] < 0.007
+    if ratio > 1:
+        # first order in dx once the interface is resolved (ratio 1 reaches the O(delta) floor first)
+        assert all(a > b for a, b in zip(err_o, err_o[1:]))
+        assert all(a / b > 1.4 for a, b in zip(err_p[1:], err_p[2:]))
+
+
+def test_gpu_eshelby_equals_oracle():
+    g = es.run_gpu(64, 5.0)
+    o = es.run_oracle(64, 5.0)
+    assert np.abs(g["F"] - o["F"]).max() <= 1e-8 * np.abs(o["F"] - np.eye(2)).max()
+    assert g["p_in"] == pytest.approx(o["p_in"], rel=1e-8) and g["err_out"] == pytest.approx(o["err_out"], rel=1e-6)

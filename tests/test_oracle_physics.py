@@ -86,3 +86,40 @@ def test_oracle_hertz_contact_converges_to_closed_form():
     # Richardson extrapolation of the first-order sequence lands on Hertz
     assert (2 * res[64]["b"] - res[32]["b"]) / b_ref == pytest.approx(1, abs=0.06)
     assert (2 * res[64]["p0"] - res[32]["p0"]) / p_ref == pytest.approx(1, abs=0.02)
+
+
+# --------------------------------------------------------------------------------------------------
+# Eshelby misfit inclusion (§4.3; tests/golden/g8_eshelby.txt), scripts/eshelby.py:
+# particles of a circular inclusion start at F0 = (1 - delta) I inside a traction-free matrix disk,
+# static single-domain MPM (plane strain, two materials, mirror-symmetry constraints on the centre
+# lines).  Reference: the paper's Lame solution, kept with the finite outer radius (the composite disk).
+import eshelby as es  # noqa: E402
+
+
+def test_eshelby_golden_and_reference_solution():
+    for E_out, nu, ratio, delta, P in read_golden("g8_eshelby.txt"):
+        assert (E_out, nu, delta) == (es.E_OUT, es.NU, es.DELTA)
+        # the paper's compliances in E and nu: C_out = (1 + nu)/E_out, C_in = (1 - 2 nu)(1 + nu)/E_in
+        assert P == pytest.approx(delta / ((1 + nu) / E_out + (1 - 2 * nu) * (1 + nu) / (E_out * ratio)), rel=1e-6)
+        assert es.paper_pressure(ratio) == pytest.approx(P, rel=1e-6)
+        # the finite composite disk: traction free at b, displacement and traction continuous at R ...
+        A, B, C, (li, Gi, lo, Go) = es.lame_finite(ratio)
+        srr, stt = es.reference_stress(ratio, [es.B_OUT, es.R_INC * (1 - 1e-12), es.R_INC])
+        assert abs(srr[0]) < 1e-9 * P and srr[1] == pytest.approx(srr[2], rel=1e-9)
+        assert A * es.R_INC == pytest.approx(B * es.R_INC + C / es.R_INC, rel=1e-12)
+        # ... uniform hydrostatic inside, and the paper's unbounded solution as b -> infinity
+        srr_u, stt_u = es.reference_stress(ratio, [0.5 * es.R_INC, 2 * es.R_INC, 3 * es.R_INC], b=1e5)
+        np.testing.assert_allclose(srr_u, [-P, -P / 4, -P / 9], rtol=1e-6)
+        np.testing.assert_allclose(stt_u, [-P, P / 4, P / 9], rtol=1e-6)
+
+
+@pytest.mark.parametrize("ratio", [1.0, 5.0])
+def test_oracle_eshelby_converges_to_lame(ratio):
+    res = {n: es.run_oracle(n, ratio) for n in (32, 64, 128)}
+    err_p = {n: abs(r["p_in"] / r["p_ref"] - 1) for n, r in res.items()}
+    err_o = {n: r["err_out"] for n, r in res.items()}
+    assert err_o[32] > err_o[64] > err_o[128]                       # monotone under refinement
+    assert err_o[32] / err_o[64] > 1.5 and err_o[64] / err_o[128] > 1.5
+    assert err_o[128] < (0.005 if ratio == 1 else 0.025)
+    assert err_p[128] < (0.005 if ratio == 1 else 0.03)
+    assert all(r["stats"].status == 0 for r in res.values())
