@@ -380,7 +380,7 @@ __device__ __forceinline__ void sw_prefetch_tmap(const CUtensorMap* mx, const CU
 // fp32 variant: half the shared memory (records, streamed inputs, node tile and staging in fp32) and
 // fewer live registers, so more CTAs fit per SM
 #ifndef OSMPM_SW_MINB_F32
-#define OSMPM_SW_MINB_F32 5
+#define OSMPM_SW_MINB_F32 4
 #endif
 template <int D, typename R>
 __global__ void __launch_bounds__(Tile<D>::NT, sizeof(R) == 8 ? OSMPM_SW_MINB : OSMPM_SW_MINB_F32)
