@@ -48,7 +48,8 @@ template <int D, typename R>
 __global__ void __launch_bounds__(Tile<D>::NT, 2)
 k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int* __restrict__ mat,
           const int* __restrict__ cell_start, BoxDev b, MatTable mt, const double* __restrict__ uin,
-          double* __restrict__ gout, double* __restrict__ dout, double* __restrict__ partials)
+          double* __restrict__ gout, double* __restrict__ dout, double* __restrict__ partials,
+          double* __restrict__ tbg, double* __restrict__ tbd)
 {
     using T = Tile<D>;
     using GR = GradRec<D>;
@@ -214,8 +215,8 @@ k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int
             sw_emit<D, Rd>(icell, icomp, ii, accd, stgd);
         }
         __syncthreads();
-        sw_flush<D, Rd>(b, t, layer, stg, gout);
-        sw_flush<D, Rd>(b, t, layer, stgd, dout);
+        sw_flush<D, Rd>(b, t, layer, stg, gout, tbg ? tbg + (int64_t)tile * T::NN * D : nullptr);
+        sw_flush<D, Rd>(b, t, layer, stgd, dout, tbd ? tbd + (int64_t)tile * T::NN * D : nullptr);
         if (layer + 1 >= T::NL || layer_empty(layer + 1)) __syncthreads();
     }
     block_reduce_store<3>(red, partials);

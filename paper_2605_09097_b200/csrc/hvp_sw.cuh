@@ -294,9 +294,14 @@ __device__ __forceinline__ void sw_emit(int cellL, int a, int i, R* acc, R* stg)
 }
 
 // fixed-order NSLOT-term sums of plane `plane` (tile-local last-axis node index) -> one RED each
+//
+// Deterministic mode (tb != nullptr, OSMPM_DETERMINISTIC=1): instead of the RED, every sum (zeros
+// included) is stored to the tile's own block of node values tb[tile-local node][component]; the node
+// pass k_det_gather then adds the <= 2^D tile blocks covering each node in a fixed tile order, so the
+// result does not depend on the order in which tiles finish (bitwise reproducible).
 template <int D, typename R>
 __device__ __forceinline__ void sw_flush(const BoxDev& b, const int* t, int plane, const R* stg,
-                                         double* __restrict__ out)
+                                         double* __restrict__ out, double* __restrict__ tb = nullptr)
 {
     using T = Tile<D>;
     for (int it = threadIdx.x; it < SW<D>::NITEM; it += T::NT) {
@@ -304,7 +309,10 @@ __device__ __forceinline__ void sw_flush(const BoxDev& b, const int* t, int plan
         R s = stg[it];
 #pragma unroll
         for (int k = 1; k < SW<D>::NSLOT; ++k) s += stg[k * SW<D>::NITEM + it];
-        if (s != R(0)) {
+        if (tb) {
+            const int a = it % D, nxy = it / D;
+            tb[((D == 3) ? nxy * T::N2 + plane : nxy * T::N1 + plane) * D + a] = (double)s;
+        } else if (s != R(0)) {
             const int a = it % D, nxy = it / D;
             int64_t g;
             if (D == 3)
@@ -314,6 +322,60 @@ __device__ __forceinline__ void sw_flush(const BoxDev& b, const int* t, int plan
             atomicAdd(&out[g * D + a], (double)s);
         }
     }
+}
+
+// out[node] = sum over the non-empty tiles covering the node, in increasing tile order per axis, of
+// the tile blocks written by sw_flush in deterministic mode (all nodes of the box, plain stores)
+template <int D, int NC = D>
+__global__ void k_det_gather(BoxDev b, const int* __restrict__ cell_start, const double* __restrict__ tb,
+                             double* __restrict__ out)
+{
+    using T = Tile<D>;
+    const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (n >= b.nnodes) return;
+    const int tt[3] = {T::T0, T::T1, T::T2};
+    int ix[3] = {0, 0, 0};
+    if (D == 3) {
+        ix[2] = (int)(n % b.nn[2]);
+        ix[1] = (int)((n / b.nn[2]) % b.nn[1]);
+        ix[0] = (int)(n / ((int64_t)b.nn[2] * b.nn[1]));
+    } else {
+        ix[1] = (int)(n % b.nn[1]);
+        ix[0] = (int)(n / b.nn[1]);
+    }
+    // per axis: the tiles t with t T <= i <= t T + T + 1 (one or two), lowest first
+    int tl[3][2], nt[3] = {1, 1, 1};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (a >= D) {
+            tl[a][0] = 0;
+            continue;
+        }
+        const int t1 = min(ix[a] / tt[a], b.nt[a] - 1);
+        if (t1 > 0 && ix[a] - t1 * tt[a] <= 1) {
+            tl[a][0] = t1 - 1;
+            tl[a][1] = t1;
+            nt[a] = 2;
+        } else {
+            tl[a][0] = t1;
+        }
+    }
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int u = 0; u < nt[0]; ++u)
+        for (int v = 0; v < nt[1]; ++v)
+            for (int w = 0; w < nt[2]; ++w) {
+                const int tx = tl[0][u], ty = tl[1][v], tz = tl[2][w];
+                const int tile = (D == 3) ? (tx * b.nt[1] + ty) * b.nt[2] + tz : tx * b.nt[1] + ty;
+                const int64_t kt = (int64_t)tile * T::NC;
+                if (cell_start[kt] == cell_start[kt + T::NC]) continue;  // empty tile: block not written
+                const int lx = ix[0] - tx * T::T0, ly = ix[1] - ty * T::T1, lz = ix[2] - tz * T::T2;
+                const int ln = (D == 3) ? (lx * T::N1 + ly) * T::N2 + lz : lx * T::N1 + ly;
+                const double* p = tb + ((int64_t)tile * T::NN + ln) * NC;
+#pragma unroll
+                for (int a = 0; a < NC; ++a) acc[a] += p[a];
+            }
+#pragma unroll
+    for (int a = 0; a < NC; ++a) out[n * NC + a] = acc[a];
 }
 
 // TMA bulk copies of the first min(NT, le - lb) particles of a layer, one field per lane of warp 0
@@ -386,7 +448,7 @@ template <int D, typename R>
 __global__ void __launch_bounds__(Tile<D>::NT, sizeof(R) == 8 ? OSMPM_SW_MINB : OSMPM_SW_MINB_F32)
 k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, const int* __restrict__ cell_start,
          BoxDev b, const double* __restrict__ din, double* __restrict__ yout, const __grid_constant__ CUtensorMap tmx,
-         const __grid_constant__ CUtensorMap tmc, int use_tmap)
+         const __grid_constant__ CUtensorMap tmc, int use_tmap, double* __restrict__ tbuf)
 {
     using T = Tile<D>;
     using C = CL<D>;
@@ -622,7 +684,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
         // node plane `layer` is complete: stage it, then sum the slots and RED
         if (it < T::ITEMS) sw_emit<D, R>(icell, icomp, ii, acc, stg);
         __syncthreads();
-        sw_flush<D, R>(b, t, layer, stg, yout);
+        sw_flush<D, R>(b, t, layer, stg, yout, tbuf ? tbuf + (int64_t)tile * T::NN * D : nullptr);
         // the next emit must not overwrite slots still being summed: a non-empty next layer has its
         // records barrier in between; otherwise synchronise here
         if (layer + 1 >= T::NL || layer_empty(layer + 1)) __syncthreads();

@@ -68,13 +68,18 @@ __device__ __forceinline__ void p2g_layer_flush(int layer, const R* stg, R* sy)
     }
 }
 
+// tb != nullptr: deterministic mode (hvp_sw.cuh sw_flush): the tile's node block is stored whole
+// (tile-local node order, zeros included) for k_det_gather instead of RED-ed
 template <int D, typename R, int NC>
-__device__ __forceinline__ void p2g_tile_flush(const BoxDev& b, const int* t, const R* sy, double* __restrict__ out)
+__device__ __forceinline__ void p2g_tile_flush(const BoxDev& b, const int* t, const R* sy, double* __restrict__ out,
+                                               double* __restrict__ tb = nullptr)
 {
     using T = Tile<D>;
     for (int idx = threadIdx.x; idx < T::NN * NC; idx += T::NT) {
         const R s = sy[idx];
-        if (s != R(0)) {
+        if (tb) {
+            tb[idx] = (double)s;
+        } else if (s != R(0)) {
             const int a = idx % NC, l = idx / NC;
             int c[3];
             tnode_coords<D>(l, c);
@@ -106,7 +111,8 @@ constexpr size_t p2g_tiled_smem_bytes()
 template <int D, typename R>
 __global__ void __launch_bounds__(Tile<D>::NT, OSMPM_P2G_MINB)
 k_p2g_tiled(const R* __restrict__ P, int64_t cap, const int* __restrict__ mat, const int* __restrict__ cell_start,
-            BoxDev b, MatTable mt, double* __restrict__ m, double* __restrict__ mom, double* __restrict__ fsig)
+            BoxDev b, MatTable mt, double* __restrict__ m, double* __restrict__ mom, double* __restrict__ fsig,
+            double* __restrict__ tbm, double* __restrict__ tbp, double* __restrict__ tbf)
 {
     using T = Tile<D>;
     using L = PL<D>;
@@ -252,9 +258,10 @@ k_p2g_tiled(const R* __restrict__ P, int64_t cap, const int* __restrict__ mat, c
             __syncthreads();
         }
     }
-    p2g_tile_flush<D, R, 1>(b, t, sm, m);
-    p2g_tile_flush<D, R, D>(b, t, sp, mom);
-    p2g_tile_flush<D, R, D>(b, t, sf, fsig);
+    const int64_t tn = (int64_t)tile * T::NN;
+    p2g_tile_flush<D, R, 1>(b, t, sm, m, tbm ? tbm + tn : nullptr);
+    p2g_tile_flush<D, R, D>(b, t, sp, mom, tbp ? tbp + tn * D : nullptr);
+    p2g_tile_flush<D, R, D>(b, t, sf, fsig, tbf ? tbf + tn * D : nullptr);
 }
 
 }  // namespace osmpm

@@ -141,6 +141,22 @@ struct Sub : public osmpm_subdomain {
     DBuf<uint8_t> act, dmask, fmask;
     DirList dir_user, dir_cpl;
     DBuf<double> stage_io;  // persistent host-I/O staging buffer
+    DBuf<double> det_a, det_b, det_c;  // per-tile node blocks of the deterministic scatter mode (hvp_sw.cuh)
+
+    // OSMPM_DETERMINISTIC=1: the sliding-window gradient and HVP store per-tile node blocks that a
+    // node pass sums in a fixed tile order instead of RED-ing into the node arrays (bitwise
+    // reproducible Newton-PCG; read at every launch so a process can switch)
+    static bool det_mode()
+    {
+        const char* e = getenv("OSMPM_DETERMINISTIC");
+        return e && e[0] == '1';
+    }
+    osmpm_status det_gather(const double* tb, double* out)
+    {
+        KC(); k_det_gather<D><<<nblk_all(box.nnodes, 256), 256, 0, st()>>>(box, cell_start.p, tb, out);
+        OSMPM_LAUNCH_CHECK();
+        return OSMPM_OK;
+    }
 
     // ---- reductions / scalars ---------------------------------------------------------------
     GroupBufs gbself;  // used when the subdomain is standalone (a group of one slab)
@@ -496,8 +512,21 @@ struct Sub : public osmpm_subdomain {
                                          (int)p2g_tiled_smem_bytes<D, R>());
                     attr = true;
                 }
+                const bool det = det_mode();
+                if (det) {
+                    OSMPM_TRY(det_a.need((size_t)box.ntiles * T::NN * D));
+                    OSMPM_TRY(det_b.need((size_t)box.ntiles * T::NN * D));
+                    OSMPM_TRY(det_c.need((size_t)box.ntiles * T::NN));
+                }
                 KC(); k_p2g_tiled<D, R><<<box.ntiles, T::NT, p2g_tiled_smem_bytes<D, R>(), st()>>>(
-                    P.p, cap, mat.p, cell_start.p, box, mats, m.p, mom.p, fsig.p);
+                    P.p, cap, mat.p, cell_start.p, box, mats, m.p, mom.p, fsig.p, det ? det_c.p : nullptr,
+                    det ? det_a.p : nullptr, det ? det_b.p : nullptr);
+                if (det) {
+                    OSMPM_LAUNCH_CHECK();
+                    KC(); k_det_gather<D, 1><<<nblk_all(box.nnodes, 256), 256, 0, st()>>>(box, cell_start.p, det_c.p, m.p);
+                    OSMPM_TRY(det_gather(det_a.p, mom.p));
+                    OSMPM_TRY(det_gather(det_b.p, fsig.p));
+                }
             }
             OSMPM_LAUNCH_CHECK();
         }
@@ -635,8 +664,19 @@ struct Sub : public osmpm_subdomain {
                                      (int)grad_sw_smem_bytes<D, R>());
                 attr_sw = true;
             }
+            const bool det = det_mode();
+            if (det) {
+                OSMPM_TRY(det_a.need((size_t)box.ntiles * T::NN * D));
+                OSMPM_TRY(det_b.need((size_t)box.ntiles * T::NN * D));
+            }
             KC(); k_grad_sw<D, R><<<box.ntiles, T::NT, grad_sw_smem_bytes<D, R>(), st()>>>(
-                P.p, cache.p, cap, mat.p, cell_start.p, box, mats, uu, g.p, dg.p, partA);
+                P.p, cache.p, cap, mat.p, cell_start.p, box, mats, uu, g.p, dg.p, partA, det ? det_a.p : nullptr,
+                det ? det_b.p : nullptr);
+            OSMPM_LAUNCH_CHECK();
+            if (det) {
+                OSMPM_TRY(det_gather(det_a.p, g.p));
+                OSMPM_TRY(det_gather(det_b.p, dg.p));
+            }
         }
         OSMPM_LAUNCH_CHECK();
         return OSMPM_OK;
@@ -708,8 +748,14 @@ struct Sub : public osmpm_subdomain {
                     fprintf(stderr, "[osmpm] hvp tensor maps: cap=%lld P=%p cache=%p ok=%d ntiles=%d\n", (long long)cap,
                             (const void*)P.p, (const void*)cache.p, (int)tm_ok, (int)box.ntiles);
             }
+            const bool det = det_mode();
+            if (det) OSMPM_TRY(det_a.need((size_t)box.ntiles * T::NN * D));
             KC(); k_hvp_sw<D, R><<<box.ntiles, T::NT, hvp_sw_smem_bytes<D, R>(), st()>>>(
-                P.p, cache.p, cap, cell_start.p, box, din, yout, tm_x, tm_c, tm_ok ? 1 : 0);
+                P.p, cache.p, cap, cell_start.p, box, din, yout, tm_x, tm_c, tm_ok ? 1 : 0, det ? det_a.p : nullptr);
+            if (det) {
+                OSMPM_LAUNCH_CHECK();
+                OSMPM_TRY(det_gather(det_a.p, yout));
+            }
         }
         OSMPM_LAUNCH_CHECK();
         if (pf.on) pf.end("hvp", st());
