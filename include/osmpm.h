@@ -32,6 +32,10 @@
  *     osmpm_implicit_solve, osmpm_schwarz_substep, osmpm_schwarz_step, osmpm_p2g (which read back
  *     a few scalars) and any call given host buffers.  Device-side errors (out-of-domain particle,
  *     inverted F) are latched and surface at the next synchronising call or osmpm_sync().
+ *   * Reproducibility: node sums that several tiles contribute to meet in fp64 atomics, so results
+ *     may differ run to run in the last bits.  With the environment variable OSMPM_DETERMINISTIC=1
+ *     (read at every launch) the P2G, Newton-gradient / Jacobi-diagonal and HVP scatters store
+ *     per-tile node blocks summed in a fixed tile order instead: bitwise reproducible, ~4 % slower.
  */
 #ifndef OSMPM_H
 #define OSMPM_H
