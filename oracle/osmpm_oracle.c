@@ -614,6 +614,7 @@ int orc_implicit_solve(const orc_grid* g, int64_t np, const double* x, const dou
         rc = orc_energy(g, np, x, F, V0, mat, E, nu, dt, mi, vn, fext, u, &E0, &Ea0);
         if (rc) goto done;
         double alpha = 1.0;
+        int at_floor = 0;
         for (;;) {
             for (int64_t k = 0; k < nd; ++k) ut[k] = free_mask[k] ? u[k] + alpha * xs[k] : u[k];
             rc = orc_energy(g, np, x, F, V0, mat, E, nu, dt, mi, vn, fext, ut, &Et, &Eat);
@@ -622,9 +623,20 @@ int orc_implicit_solve(const orc_grid* g, int64_t np, const double* x, const dou
             alpha *= 0.5;
             stats->ls_halvings++;
             if (alpha < st->ls_min_alpha) {
+                /* no decrease of E_h is resolvable any more: once |g| has dropped below
+                 * sqrt(rtol) * gref the iterate is accepted as converged at the roundoff floor of
+                 * E_h (R8), otherwise the stagnation is an error */
+                if (!st->fixed_iters && gn <= sqrt(st->newton_rtol) * gref) {
+                    at_floor = 1;
+                    break;
+                }
                 rc = ORC_LS_STAGNATION;
                 goto done;
             }
+        }
+        if (at_floor) {
+            converged = 1;
+            break;
         }
         memcpy(u, ut, sizeof(double) * (size_t)nd);
         stats->energy = Et;

@@ -438,6 +438,7 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
             }
         // backtracking line search (R8)
         double alpha = 1.0, Et = 0.0, Eat = 0.0;
+        bool at_floor = false;
         for (;;) {
             for (int i = 0; i < G.ns; ++i) {
                 Sub<D, R>* q = G.s[i];
@@ -459,12 +460,22 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
             alpha *= 0.5;
             sts->ls_halvings++;
             if (alpha < s->ls_min_alpha) {
+                // no decrease of E_h is resolvable any more: once |g| has dropped below sqrt(rtol) * gref
+                // the iterate is accepted as converged at the roundoff floor of E_h (R8)
+                if (!s->fixed_iters && gn <= std::sqrt(s->newton_rtol) * gref) {
+                    at_floor = true;
+                    break;
+                }
                 set_error("line search stagnated at Newton iteration %d (alpha < %g)", it, s->ls_min_alpha);
                 rc = OSMPM_E_LINESEARCH_STAGNATION;
                 break;
             }
         }
         if (rc != OSMPM_OK) break;
+        if (at_floor) {
+            converged = true;
+            break;
+        }
         for (int i = 0; i < G.ns; ++i) {
             std::swap(G.s[i]->u.p, G.s[i]->ut.p);
             std::swap(G.s[i]->u.cap, G.s[i]->ut.cap);

@@ -229,3 +229,29 @@ def test_newton_fixed_iterations_runs_exact_count():
     st_set = oracle.default_settings(max_newton=3, max_cg=7, fixed_iters=1)
     u, st = oracle.implicit_solve(sc, gs, st_set)
     assert st.newton_iters == 3 and st.cg_iters == 21
+
+
+def test_newton_accepts_the_energy_roundoff_floor():
+    """R8: near the static limit (dt = 10 s, Dirichlet band, tiny load) the backtracking line search can
+    no longer resolve a decrease of E_h; once |g| <= sqrt(rtol) * max(|g0|, f_s) the iterate is accepted as
+    converged instead of failing with LINESEARCH_STAGNATION (this coarse solve of the quasi-static
+    cantilever frame stalls at |g| / |g0| ~ 1.3e-6 with rtol = 1e-8)."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
+    import eb_cantilever as eb
+    from oracle import schwarz as OS
+    D = eb.E * eb.H ** 3 / (12 * (1 - eb.NU ** 2))
+    g = 0.05 * D / (eb.RHO * eb.H * eb.L ** 3)
+    coarse, fine = synth.c1_cantilever(g=g)
+    coarse.dt, fine.dt = 1.0, 0.25
+    gsB, gsS = oracle.p2g(coarse), oracle.p2g(fine)
+    hatB, _ = OS.receivers(coarse, fine, gsB, gsS, 1e-6)
+    nn = gsB.m.shape[0]
+    mask = np.zeros((nn, 2), np.uint8)
+    mask[hatB] = 1
+    st = oracle.default_settings(newton_rtol=1e-8, cg_rtol=1e-10, max_cg=20000, max_newton=40)
+    u, s = oracle.implicit_solve(coarse, gsB, st, dirichlet_mask=mask, dirichlet_v=np.zeros((nn, 2)),
+                                 raise_on_error=False)
+    assert s.status == 0 and s.ls_halvings > 0
+    assert s.grad_norm <= 1e-4 * s.grad_norm0 and s.grad_norm > 1e-8 * s.grad_norm0
