@@ -270,7 +270,11 @@ osmpm_status osmpm_subdomain_info(osmpm_subdomain* sub, int64_t* n_particles, in
  *   with v_B^n from src's last P2G and v_B^{n+1} its solved / set grid velocity; alpha in [0,1].
  * targets: n_targets linear node indices of dst's dense box (NULL: all nodes of dst's box,
  *   n_targets must then equal dst's node count); v_out: n_targets*d.  eps_tol only for Pi.
- * Coarse stencil nodes outside the coarse box contribute / receive nothing (R9). */
+ * Coarse stencil nodes outside the coarse box contribute / receive nothing (R9).
+ * Environment OSMPM_PI=affine (here and in the coupler; NOT the paper's operator, R21):
+ *   Pi returns instead the value at x_I of the weighted least-squares affine fit of the fine
+ *   velocities over the same weights m_S,j N_B,I(x_S,j) -- exact for affine fields under any masses
+ *   (nodes whose fine support is too thin to fit keep the mean above). */
 osmpm_status osmpm_transmit(osmpm_subdomain* src, osmpm_subdomain* dst, osmpm_direction dir,
                             double alpha, double eps_tol, int64_t n_targets, const int64_t* targets,
                             double* v_out, osmpm_memspace space);

@@ -744,6 +744,120 @@ int orc_project(const orc_grid* gs, const double* ms, const double* vs, const ui
     return ORC_OK;
 }
 
+/* O9b (NOT the paper's operator; R21): affine projection.  Same weights w_j = m_j N_B,I(x_j)
+ * over the active fine nodes of the coarse node's support as Pi, but v_B,I is the value
+ * at x_I of the weighted least-squares affine fit
+ *     min_{a,B} sum_j w_j |v_j - a - B (x_j - x_I)/dx_B|^2 ,
+ * i.e. the (1+d)x(1+d) normal equations [S0 S1^T; S1 S2] [a; B^T] = [T0; T1] with S0 = sum w (+ eps_tol),
+ * S1 = sum w xi, S2 = sum w xi xi^T, T0 = sum w v^T, T1 = sum w xi v^T, xi = (x_j - x_I)/dx_B.  It
+ * reproduces affine fields exactly for ANY masses (Pi only for uniform ones).  A node whose fine
+ * support does not span d dimensions well (a pivot below 1e-4 of S0 after elimination: the support's spread
+ * in some direction under 1 % of a coarse cell, where the fit amplifies rounding) keeps Pi's value.
+ * Solved by Gaussian elimination with partial pivoting, the d components as d right-hand sides. */
+int orc_project_affine(const orc_grid* gs, const double* ms, const double* vs, const uint8_t* act_s,
+                       const orc_grid* gb, double eps_tol, double* vb)
+{
+    int d = gs->d, K = 1 + d;
+    int64_t nns = n_nodes(gs), nnb = n_nodes(gb);
+    double* A = (double*)calloc((size_t)nnb * K * K, sizeof(double));
+    double* R = (double*)calloc((size_t)nnb * K * d, sizeof(double));
+    if (!A || !R) {
+        free(A);
+        free(R);
+        return -1;
+    }
+    int64_t idx[27];
+    double N[27];
+    for (int64_t j = 0; j < nns; ++j) {
+        if (!act_s[j]) continue;
+        int64_t k[3];
+        if (d == 3) {
+            k[0] = j / (gs->n[1] * gs->n[2]);
+            k[1] = (j / gs->n[2]) % gs->n[1];
+            k[2] = j % gs->n[2];
+        } else {
+            k[0] = j / gs->n[1];
+            k[1] = j % gs->n[1];
+            k[2] = 0;
+        }
+        double xj[3];
+        for (int a = 0; a < d; ++a) xj[a] = gs->o[a] + gs->dx * (double)k[a];
+        int c = stencil_partial(gb, xj, idx, N);
+        for (int s = 0; s < c; ++s) {
+            int64_t I = idx[s];
+            if (I < 0) continue;
+            int64_t kI[3];
+            if (d == 3) {
+                kI[0] = I / (gb->n[1] * gb->n[2]);
+                kI[1] = (I / gb->n[2]) % gb->n[1];
+                kI[2] = I % gb->n[2];
+            } else {
+                kI[0] = I / gb->n[1];
+                kI[1] = I % gb->n[1];
+                kI[2] = 0;
+            }
+            double phi[4] = {1.0, 0.0, 0.0, 0.0};  /* (1, xi) */
+            for (int a = 0; a < d; ++a) phi[1 + a] = (xj[a] - (gb->o[a] + gb->dx * (double)kI[a])) / gb->dx;
+            double w = ms[j] * N[s];
+            for (int r = 0; r < K; ++r) {
+                for (int q = 0; q < K; ++q) A[(I * K + r) * K + q] += w * phi[r] * phi[q];
+                for (int a = 0; a < d; ++a) R[(I * K + r) * d + a] += w * phi[r] * vs[j * d + a];
+            }
+        }
+    }
+    for (int64_t I = 0; I < nnb; ++I) {
+        double M[4][4], rhs[4][3];
+        for (int r = 0; r < K; ++r) {
+            for (int q = 0; q < K; ++q) M[r][q] = A[(I * K + r) * K + q];
+            for (int a = 0; a < d; ++a) rhs[r][a] = R[(I * K + r) * d + a];
+        }
+        double s0 = M[0][0];
+        M[0][0] += eps_tol;
+        /* Pi as the fallback */
+        for (int a = 0; a < d; ++a) vb[I * d + a] = rhs[0][a] / (s0 + eps_tol);
+        if (!(s0 > 0.0)) continue;
+        int ok = 1;
+        for (int col = 0; col < K && ok; ++col) {
+            int piv = col;
+            for (int r = col + 1; r < K; ++r)
+                if (fabs(M[r][col]) > fabs(M[piv][col])) piv = r;
+            if (!(fabs(M[piv][col]) > 1e-4 * s0)) {
+                ok = 0;
+                break;
+            }
+            if (piv != col) {
+                for (int q = 0; q < K; ++q) {
+                    double t = M[col][q];
+                    M[col][q] = M[piv][q];
+                    M[piv][q] = t;
+                }
+                for (int a = 0; a < d; ++a) {
+                    double t = rhs[col][a];
+                    rhs[col][a] = rhs[piv][a];
+                    rhs[piv][a] = t;
+                }
+            }
+            for (int r = col + 1; r < K; ++r) {
+                double f = M[r][col] / M[col][col];
+                for (int q = col; q < K; ++q) M[r][q] -= f * M[col][q];
+                for (int a = 0; a < d; ++a) rhs[r][a] -= f * rhs[col][a];
+            }
+        }
+        if (!ok) continue;
+        double sol[4][3];
+        for (int r = K - 1; r >= 0; --r)
+            for (int a = 0; a < d; ++a) {
+                double t = rhs[r][a];
+                for (int q = r + 1; q < K; ++q) t -= M[r][q] * sol[q][a];
+                sol[r][a] = t / M[r][r];
+            }
+        for (int a = 0; a < d; ++a) vb[I * d + a] = sol[0][a];
+    }
+    free(A);
+    free(R);
+    return ORC_OK;
+}
+
 /* O10: I_{B->S} (Eq. interp_BtoS) at the fine node positions `targets`, applied
  * to both endpoint fields (Eq. spatial_interp_n), then T_m with weight alpha
  * (Eq. temporal_interp): v = (1 - alpha) I(v_B^n) + alpha I(v_B^{n+1}). */

@@ -213,9 +213,7 @@ struct Coupler : public osmpm_coupler {
         // v_GammaB^(0) = Pi(v_S^n) on the coarse receivers (R16)
         eps_tol = set.eps_tol >= 0 ? set.eps_tol : 1e-12 * S->total_mass;
         if (nB) {
-            B->KC();
-            k_project_out<D><<<nblk_all(nB, 256), 256, 0, st()>>>(nB, dB.p, num.p, den.p, eps_tol, vGB.p);
-            OSMPM_LAUNCH_CHECK();
+            OSMPM_TRY(project_out<D, R>(st(), B, nB, dB.p, num.p, den.p, eps_tol, vGB.p));
         }
         // v_GammaS^(0) = I(v_B^n) (R15: r_S at k = 0 compares I(v_B^(1)) with I(v_B^n))
         if (nS) {
@@ -278,9 +276,7 @@ struct Coupler : public osmpm_coupler {
             OSMPM_TRY(project_accumulate(S, B, true, num, den));
             const int64_t nB = recvB.size();
             if (nB) {
-                B->KC();
-                k_project_out<D><<<nblk_all(nB, 256), 256, 0, st()>>>(nB, dB.p, num.p, den.p, eps_tol, vGBnew.p);
-                OSMPM_LAUNCH_CHECK();
+                OSMPM_TRY(project_out<D, R>(st(), B, nB, dB.p, num.p, den.p, eps_tol, vGBnew.p));
             }
         }
         return S->g2p();

@@ -141,6 +141,7 @@ struct Sub : public osmpm_subdomain {
     DBuf<uint8_t> act, dmask, fmask;
     DirList dir_user, dir_cpl;
     DBuf<double> stage_io;  // persistent host-I/O staging buffer
+    DBuf<double> pi_mom;  // affine-Pi moments when this subdomain is the coarse side (transmit.cuh)
     DBuf<double> det_a, det_b, det_c;  // per-tile node blocks of the deterministic scatter mode (hvp_sw.cuh)
 
     // OSMPM_DETERMINISTIC=1: the sliding-window gradient and HVP store per-tile node blocks that a

@@ -81,6 +81,127 @@ __global__ void k_project_out(int64_t nt, const int64_t* __restrict__ targets, c
     for (int a = 0; a < D; ++a) out[t * D + a] = num[I * D + a] / (den[I] + eps);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Affine variant of Pi (OSMPM_PI=affine; R21, NOT the paper's operator): the same weights
+// w_j = m_j N_B,I(x_j) feed the normal equations of the weighted least-squares affine fit
+// v ~ a + B xi, xi = (x_j - x_I)/dx_B, and the coarse value is a -- exact for affine fields under any
+// fine masses (the paper's support-wide mean is exact only for uniform masses, which biases the
+// rotation a bending section transmits).  Moments per coarse node: the symmetric (1+D)^2 matrix
+// (upper triangle, AF<D>::NA) and the (1+D) x D right-hand sides.
+template <int D> struct AF {
+    static constexpr int K = 1 + D, NA = K * (K + 1) / 2, NM = NA + K * D;
+    static __host__ __device__ constexpr int ai(int r, int q) { return r * K - r * (r - 1) / 2 + (q - r); }  // r <= q
+};
+static inline bool pi_affine()
+{
+    const char* e = getenv("OSMPM_PI");
+    return e && std::string(e) == "affine";
+}
+template <int D>
+__global__ void k_project_affine(BoxDev fb, int64_t nown, const uint8_t* __restrict__ act, const double* __restrict__ m,
+                                 const double* __restrict__ v, GridGeo cg, double* __restrict__ mom)
+{
+    using A = AF<D>;
+    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= nown || !act[j]) return;
+    int i2 = (D == 3) ? (int)(j % fb.nn[2]) : 0;
+    int i1 = (D == 3) ? (int)((j / fb.nn[2]) % fb.nn[1]) : (int)(j % fb.nn[1]);
+    int i0 = (D == 3) ? (int)(j / ((int64_t)fb.nn[2] * fb.nn[1])) : (int)(j / fb.nn[1]);
+    const int gi[3] = {fb.lo[0] + i0, fb.lo[1] + i1, fb.lo[2] + i2};
+    double xj[3];
+#pragma unroll
+    for (int a = 0; a < D; ++a) xj[a] = fb.o[a] + fb.dx * (double)gi[a];
+    int64_t idx[27];
+    double N[27];
+    coarse_stencil<D>(xj, cg.o, cg.inv_dx, cg.gd, idx, N);
+    const double mj = m[j];
+    for (int s = 0; s < Tile<D>::NS; ++s) {
+        const int64_t I = idx[s];
+        if (I < 0) continue;
+        int kI[3] = {0, 0, 0};
+        if (D == 3) {
+            kI[2] = (int)(I % cg.gd[2]);
+            kI[1] = (int)((I / cg.gd[2]) % cg.gd[1]);
+            kI[0] = (int)(I / ((int64_t)cg.gd[2] * cg.gd[1]));
+        } else {
+            kI[1] = (int)(I % cg.gd[1]);
+            kI[0] = (int)(I / cg.gd[1]);
+        }
+        double phi[A::K];
+        phi[0] = 1.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) phi[1 + a] = (xj[a] - (cg.o[a] + cg.dx * (double)kI[a])) * cg.inv_dx;
+        const double w = mj * N[s];
+        double* mo = mom + I * A::NM;
+#pragma unroll
+        for (int r = 0; r < A::K; ++r) {
+#pragma unroll
+            for (int q = r; q < A::K; ++q) atomicAdd(&mo[A::ai(r, q)], w * phi[r] * phi[q]);
+#pragma unroll
+            for (int a = 0; a < D; ++a) atomicAdd(&mo[A::NA + r * D + a], w * phi[r] * v[j * D + a]);
+        }
+    }
+}
+
+// solve the normal equations of each target coarse node (Gaussian elimination with partial pivoting);
+// a node whose fine support does not span D dimensions keeps the mass-weighted mean num / (den + eps)
+template <int D>
+__global__ void k_project_out_affine(int64_t nt, const int64_t* __restrict__ targets, const double* __restrict__ num,
+                                     const double* __restrict__ den, const double* __restrict__ mom, double eps,
+                                     double* __restrict__ out)
+{
+    using A = AF<D>;
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    const int64_t I = targets ? targets[t] : t;
+    const double* mo = mom + I * A::NM;
+    double M[A::K][A::K], rhs[A::K][D];
+#pragma unroll
+    for (int r = 0; r < A::K; ++r) {
+#pragma unroll
+        for (int q = 0; q < A::K; ++q) M[r][q] = mo[A::ai(r < q ? r : q, r < q ? q : r)];
+#pragma unroll
+        for (int a = 0; a < D; ++a) rhs[r][a] = mo[A::NA + r * D + a];
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) out[t * D + a] = num[I * D + a] / (den[I] + eps);
+    const double s0 = M[0][0];
+    if (!(s0 > 0.0)) return;
+    M[0][0] += eps;
+    for (int col = 0; col < A::K; ++col) {
+        int piv = col;
+        for (int r = col + 1; r < A::K; ++r)
+            if (fabs(M[r][col]) > fabs(M[piv][col])) piv = r;
+        if (!(fabs(M[piv][col]) > 1e-4 * s0)) return;  // the fit would amplify rounding: keep the mean
+        if (piv != col) {
+            for (int q = 0; q < A::K; ++q) {
+                const double tq = M[col][q];
+                M[col][q] = M[piv][q];
+                M[piv][q] = tq;
+            }
+            for (int a = 0; a < D; ++a) {
+                const double ta = rhs[col][a];
+                rhs[col][a] = rhs[piv][a];
+                rhs[piv][a] = ta;
+            }
+        }
+        for (int r = col + 1; r < A::K; ++r) {
+            const double f = M[r][col] / M[col][col];
+            for (int q = col; q < A::K; ++q) M[r][q] -= f * M[col][q];
+            for (int a = 0; a < D; ++a) rhs[r][a] -= f * rhs[col][a];
+        }
+    }
+    double sol[A::K][D];
+    for (int r = A::K - 1; r >= 0; --r)
+        for (int a = 0; a < D; ++a) {
+            double tv = rhs[r][a];
+            for (int q = r + 1; q < A::K; ++q) tv -= M[r][q] * sol[q][a];
+            sol[r][a] = tv / M[r][r];
+        }
+#pragma unroll
+    for (int a = 0; a < D; ++a) out[t * D + a] = sol[0][a];
+}
+
 // I + T: v_j = (1 - alpha) sum_I v0_I N_I(x_j) + alpha sum_I v1_I N_I(x_j); the coarse fields live
 // on the coarse subdomain's box (nodes outside the box carry zero velocity)
 template <int D>
@@ -155,7 +276,35 @@ osmpm_status project_accumulate_group(SlabGroup<D, R> F, Sub<D, R>* coarse, bool
         OSMPM_LAUNCH_CHECK();
     }
     OSMPM_TRY(group_allreduce<D, R>(F, num, (int)(nnb * (D + 1))));
+    if (pi_affine()) {
+        OSMPM_TRY(coarse->pi_mom.need((size_t)nnb * AF<D>::NM));
+        OSMPM_CU(cudaMemsetAsync(coarse->pi_mom.p, 0, nnb * AF<D>::NM * sizeof(double), st));
+        for (int i = 0; i < F.ns; ++i) {
+            Sub<D, R>* fine = F.s[i];
+            const double* v = use_solved ? fine->vnew.p : fine->vn.p;
+            fine->KC();
+            k_project_affine<D><<<nblk_all(fine->box.nnodes, 256), 256, 0, st>>>(
+                fine->box, fine->nown, fine->act.p, fine->m.p, v, geo_of(coarse), coarse->pi_mom.p);
+            OSMPM_LAUNCH_CHECK();
+        }
+        OSMPM_TRY(group_allreduce<D, R>(F, coarse->pi_mom.p, (int)(nnb * AF<D>::NM)));
+    }
     if (pf.on) pf.end("transmit", st);
+    return OSMPM_OK;
+}
+
+// the projected coarse values of nt target nodes (Pi, or its affine variant under OSMPM_PI=affine)
+template <int D, typename R>
+osmpm_status project_out(cudaStream_t st, Sub<D, R>* coarse, int64_t nt, const int64_t* targets, const double* num,
+                         const double* den, double eps, double* out)
+{
+    if (nt <= 0) return OSMPM_OK;
+    coarse->KC();
+    if (pi_affine())
+        k_project_out_affine<D><<<nblk_all(nt, 256), 256, 0, st>>>(nt, targets, num, den, coarse->pi_mom.p, eps, out);
+    else
+        k_project_out<D><<<nblk_all(nt, 256), 256, 0, st>>>(nt, targets, num, den, eps, out);
+    OSMPM_LAUNCH_CHECK();
     return OSMPM_OK;
 }
 template <int D, typename R>
@@ -224,12 +373,7 @@ osmpm_status transmit_impl(SlabGroup<D, R> SG, Sub<D, R>* src, Sub<D, R>* dstc, 
         double* num = (double*)cx->get_scratch(2, dstc->dense_nodes() * (D + 1) * sizeof(double));
         if (!num) return OSMPM_E_OOM;
         OSMPM_TRY(project_accumulate_group<D, R>(SG, dstc, alpha == 1.0, num));
-        if (nt > 0) {
-            SG.ctx->launches++;
-            k_project_out<D><<<nblk_all(nt, 256), 256, 0, st>>>(nt, tptr, num, num + dstc->dense_nodes() * D, eps,
-                                                               optr);
-            OSMPM_LAUNCH_CHECK();
-        }
+        OSMPM_TRY(project_out<D, R>(st, dstc, nt, tptr, num, num + dstc->dense_nodes() * D, eps, optr));
     } else {
         if (!src) {
             set_error("transmit COARSE_TO_FINE: the coarse subdomain must not be decomposed");

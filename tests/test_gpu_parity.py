@@ -247,3 +247,22 @@ def test_deterministic_mode_is_bitwise_reproducible(ctx, monkeypatch):
         sub.implicit_solve(osmpm.newton_settings(max_newton=3, max_cg=20, fixed_iters=1))
         vs.append(sub.read_grid_velocity())
     assert np.array_equal(vs[0], vs[1])
+
+
+def test_affine_projection_parity(ctx, monkeypatch):
+    """OSMPM_PI=affine (R21; not the paper's operator) against oracle.project_affine."""
+    from paper_2605_09097_b200 import osmpm
+    monkeypatch.setenv("OSMPM_PI", "affine")
+    fine = synth.random_fixture(dim=3, cells=(8, 8, 6), seed=106, dx=0.025)
+    coarse = synth.random_fixture(dim=3, cells=(6, 6, 5), seed=107, dx=0.1)
+    coarse.particles.x -= 0.1
+    coarse.grid = synth.grid_around(coarse.particles.x, 0.1, 4, 3)
+    rf = oracle.p2g(fine)
+    sf = make_sub(ctx, fine)
+    scs = make_sub(ctx, coarse)
+    sf.p2g()
+    scs.p2g()
+    out = osmpm.transmit(sf, scs, osmpm.FINE_TO_COARSE, alpha=0.0, eps_tol=1e-12)
+    ref = oracle.project_affine(fine.grid, rf, coarse.grid, eps_tol=1e-12)
+    assert rel_linf(out, ref) <= TOL
+    assert rel_linf(out, oracle.project(fine.grid, rf, coarse.grid, eps_tol=1e-12)[0]) > 1e-6  # it is a different operator
