@@ -459,6 +459,9 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
             if (Et < E0 || (std::isfinite(Et) && std::fabs(Et - E0) <= s->energy_noise_rtol * Ea0)) break;
             alpha *= 0.5;
             sts->ls_halvings++;
+            if (alpha < s->ls_min_alpha && getenv("OSMPM_DEBUG_LS"))
+                fprintf(stderr, "[osmpm] ls stall: it %d |g| %.3e gref %.3e E0 %.17g Et-E0 %.3e Ea0 %.3e\n", it, gn,
+                        gref, E0, Et - E0, Ea0);
             if (alpha < s->ls_min_alpha) {
                 // no decrease of E_h is resolvable any more: once |g| has dropped below sqrt(rtol) * gref
                 // the iterate is accepted as converged at the roundoff floor of E_h (R8)
