@@ -58,27 +58,7 @@ def parse():
 
 def build_workload(cells):
     import synth
-    fine = synth.c5_stress(n_cells=cells)
-    cgrid, cvel = synth.c5_coarse_field(fine.grid, n_cells=cells)
-    # passive coarse subdomain: 1 particle per coarse cell carrying the smooth field
-    # (its P2G gives v_B^n; v_B^{n+1} is the field shifted in time)
-    side = cells * fine.grid.dx
-    lo = 0.5 - side / 2
-    xb, vol = synth.lattice([lo] * 3, [lo + side] * 3, cgrid.dx, 1)
-    cpart = synth.make_particles(xb, vol, 1000.0)
-    idx = np.clip(np.round((xb - np.asarray(cgrid.origin)) / cgrid.dx).astype(int), 0, cgrid.dims[0] - 1)
-    cpart.v = np.ascontiguousarray(cvel[idx[:, 0], idx[:, 1], idx[:, 2]])
-    coarse = synth.Scene(cgrid, cpart, [(1.0e5, 0.3)], 4e-3, (0.0, 0.0, 0.0))
-    # fine receivers: fine nodes of the material footprint outside the cube shrunk by 2 cells
-    k0 = int(round((0.5 - side / 2) / fine.grid.dx))
-    n_nodes_side = cells + 3
-    kk = np.arange(k0 - 1, k0 - 1 + n_nodes_side)
-    K = np.stack(np.meshgrid(kk, kk, kk, indexing="ij"), -1).reshape(-1, 3)
-    inner = np.all((K >= k0 + 2) & (K <= k0 + cells - 2), axis=1)
-    R = K[~inner]
-    gd = fine.grid.dims
-    recv = (R[:, 0] * gd[1] + R[:, 1]) * gd[2] + R[:, 2]
-    return fine, coarse, cvel, np.ascontiguousarray(recv.astype(np.int64))
+    return synth.c5_bench_workload(cells)
 
 
 # ------------------------------------------------------------------------------------------------
@@ -323,7 +303,7 @@ def main():
     prec = osmpm.F64 if args.precision == "f64" else osmpm.F32
     word = 8 if args.precision == "f64" else 4
 
-    fine, coarse, cvel, recv = build_workload(args.cells)
+    fine, coarse, recv = build_workload(args.cells)
     n = fine.particles.n
     sub = osmpm.Subdomain(ctx, fine.grid, fine.dt, fine.particles, fine.materials, fine.gravity, precision=prec)
     # the small coarse overlap grid is replicated on every rank (decompose=False)
@@ -338,12 +318,22 @@ def main():
     settings = osmpm.newton_settings(max_newton=args.newton, max_cg=args.cg, fixed_iters=1)
     mask_all = torch.full((recv.shape[0],), 7, dtype=torch.uint8, device=dev)
 
-    def step():
+    # a11: the step's initial particle state, restored at the start of every step (warm-up and timed
+    # alike), as Alg. 1 restores the fine particles at every Schwarz iteration: every
+    # step then does the identical work on the identical state
+    sub.checkpoint()
+    last_stats = {}
+
+    def step(restore=True):
+        if restore:
+            sub.restore()
         sub.p2g()
         vb = osmpm.transmit(sub, csub, osmpm.FINE_TO_COARSE, alpha=0.0, eps_tol=1e-12, device=dev)
         vS = osmpm.transmit(csub, sub, osmpm.COARSE_TO_FINE, alpha=0.5, targets=recv_d, device=dev)
         sub.set_dirichlet_device(recv_d, mask_all, vS)
-        sub.implicit_solve(settings)
+        st = sub.implicit_solve(settings)
+        last_stats.update(newton_iters=st.newton_iters, cg_iters=st.cg_iters, ls_halvings=st.ls_halvings,
+                          ls_failures=st.ls_failures, negcurv=st.negcurv)
         sub.g2p()
         return vb
 
@@ -352,7 +342,8 @@ def main():
         ctx.profile(w == args.warmup - 1 and not args.no_prof)
         step()
     torch.cuda.synchronize(dev)
-    sub.p2g()  # (untimed) grid of the current state, for the active-node count of the roofline
+    sub.restore()
+    sub.p2g()  # (untimed) grid of the step's initial state, for the active-node count of the roofline
     _, _, box_dims = sub.info()
     g = sub.read_grid(device=dev)
     n_active = int(g["active"].sum().item())  # this rank's owned nodes (decomposed reads)
@@ -425,7 +416,7 @@ def main():
                 consumed[b].record(stream)
                 if k + 1 < steps:
                     upload(k + 1)
-                step()
+                step(restore=False)  # the upload replaces the restore
                 sub.read_particles_into(x=res[b]["x"], v=res[b]["v"])
                 done[b].record(stream)
                 with torch.cuda.stream(copy):
@@ -482,6 +473,9 @@ def main():
                    "particles": n, "particles_rank0": n_local, "cells": args.cells, "newton": args.newton,
                    "cg": args.cg, "active_nodes_rank0": n_active, "box_nodes_rank0": int(np.prod(box_dims)),
                    "receivers": int(recv.shape[0]),
+                   "state": "every step restores the checkpointed initial particle state (a11) first; "
+                            "the e2e leg uploads it from pinned host memory instead",
+                   "solve_stats_last_step": last_stats,
                    "parallelism": (f"x-slabs x{slabs_total} (NCCL over NVLink, {world} GPUs)" if world > 1
                                    else (f"x-slabs x{slabs_total} on one GPU" if slabs_total > 1 else "single GPU")),
                    "slab_cuts": cuts,

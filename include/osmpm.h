@@ -108,9 +108,20 @@ typedef struct {
     double newton_rtol, newton_atol, cg_rtol, ls_min_alpha, energy_noise_rtol;
 } osmpm_newton_settings;
 
+/* Outcome of one implicit solve.  Besides the counts, three events that change what the solve
+ * returns are reported (R7, R8), identically in the oracle:
+ *   negcurv       PCG solves stopped by non-positive curvature p^T H p <= 0 (the Newton step is the
+ *                 iterate reached, or -diag^-1 g if it was the first PCG iteration)
+ *   ls_failures   fixed_iters only: Newton iterations whose line search found no decrease down to
+ *                 ls_min_alpha; alpha = 0 is taken (u unchanged) and the solve goes on, so the work
+ *                 of a timed solve stays fixed
+ *   floor_accept  tolerance mode only: 1 if the solve was accepted as converged at the round-off
+ *                 floor of E_h (||g|| <= sqrt(newton_rtol) * g_ref while no decrease was resolvable)
+ *                 rather than at newton_rtol */
 typedef struct {
     int32_t newton_iters, cg_iters, ls_halvings, status;
     double grad_norm0, grad_norm, energy;
+    int32_t negcurv, ls_failures, floor_accept, reserved;
 } osmpm_solve_stats;
 
 /* Schwarz coupling settings (R10-R16).
@@ -271,10 +282,12 @@ osmpm_status osmpm_subdomain_info(osmpm_subdomain* sub, int64_t* n_particles, in
  * targets: n_targets linear node indices of dst's dense box (NULL: all nodes of dst's box,
  *   n_targets must then equal dst's node count); v_out: n_targets*d.  eps_tol only for Pi.
  * Coarse stencil nodes outside the coarse box contribute / receive nothing (R9).
- * Environment OSMPM_PI=affine (here and in the coupler; NOT the paper's operator, R21):
- *   Pi returns instead the value at x_I of the weighted least-squares affine fit of the fine
- *   velocities over the same weights m_S,j N_B,I(x_S,j) -- exact for affine fields under any masses
- *   (nodes whose fine support is too thin to fit keep the mean above). */
+ * Errors: INVALID_ARG for alpha outside [0, 1] (FINE_TO_COARSE: alpha not 0 or 1), n_targets < 0,
+ *   targets == NULL with n_targets != dst node count, or a HOST target outside dst's dense box (checked
+ *   before any work).  A DEVICE target outside the box is skipped (its output row is 0) and latched:
+ *   INVALID_ARG with its position in `targets` at the next synchronising call / osmpm_sync of the
+ *   coarse subdomain.  STATE if src has no grid (no osmpm_p2g) or alpha > 0 without a solved velocity.
+ * Pi is evaluated as a gather (fixed-order sums, no atomics): bitwise reproducible. */
 osmpm_status osmpm_transmit(osmpm_subdomain* src, osmpm_subdomain* dst, osmpm_direction dir,
                             double alpha, double eps_tol, int64_t n_targets, const int64_t* targets,
                             double* v_out, osmpm_memspace space);
@@ -294,6 +307,15 @@ osmpm_status osmpm_schwarz_prepare(osmpm_coupler* cpl);
 osmpm_status osmpm_schwarz_substep(osmpm_coupler* cpl, int32_t m, osmpm_solve_stats* stats);
 /* Whole frame t_n -> t_n+1 (Alg. 1). */
 osmpm_status osmpm_schwarz_step(osmpm_coupler* cpl, osmpm_schwarz_report* report);
+
+/* a11 (PAPER.md:376-379 Eq. store_states, 455 Alg. 1 "reset"): osmpm_checkpoint stores the whole
+ * particle state {x, v, F, B, m, V0, material, P^∂ flag, id} -- per slab, with its particle count,
+ * for a decomposed subdomain -- in library-owned device memory (one copy per subdomain; a second
+ * call overwrites it); osmpm_restore copies it back, so the next osmpm_p2g starts from exactly the
+ * stored state.  Device-to-device copies on the ctx stream, asynchronous.  Errors: STATE (restore
+ * without a checkpoint), OOM. */
+osmpm_status osmpm_checkpoint(osmpm_subdomain* sub);
+osmpm_status osmpm_restore(osmpm_subdomain* sub);
 
 /* Block until all work of the ctx is done; surfaces latched device errors. */
 osmpm_status osmpm_sync(osmpm_subdomain* sub);

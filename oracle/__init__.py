@@ -35,7 +35,8 @@ class OrcNewtonSettings(C.Structure):
 class OrcSolveStats(C.Structure):
     _fields_ = [("newton_iters", C.c_int32), ("cg_iters", C.c_int32), ("ls_halvings", C.c_int32),
                 ("status", C.c_int32), ("grad_norm0", C.c_double), ("grad_norm", C.c_double),
-                ("energy", C.c_double)]
+                ("energy", C.c_double), ("negcurv", C.c_int32), ("ls_failures", C.c_int32),
+                ("floor_accept", C.c_int32), ("reserved", C.c_int32)]
 
 
 def build(force: bool = False) -> str:
@@ -328,22 +329,6 @@ def project(grid_s, gs_fine: GridState, grid_b, eps_tol=0.0, v_fine=None, m_fine
                            C.c_double(eps_tol), _p(num), _p(den), _p(vb))
     check(rc, "project")
     return vb, num, den
-
-
-def project_affine(grid_s, gs_fine: GridState, grid_b, eps_tol=0.0, v_fine=None, m_fine=None, active_fine=None):
-    """Affine variant of Pi (R21; not the paper's operator): weighted least-squares affine
-    fit at each coarse node, exact for affine fields under any masses."""
-    gS = grid_struct(grid_s)
-    gB = grid_struct(grid_b)
-    d = grid_s.dim
-    vb = np.zeros((n_nodes(grid_b), d))
-    ms = _f64(gs_fine.m if m_fine is None else m_fine)
-    vs = _f64(gs_fine.v if v_fine is None else v_fine)
-    act = np.ascontiguousarray(gs_fine.active if active_fine is None else active_fine, dtype=np.uint8)
-    rc = lib().orc_project_affine(C.byref(gS), _p(ms), _p(vs), _p(act, np.uint8), C.byref(gB),
-                                  C.c_double(eps_tol), _p(vb))
-    check(rc, "project_affine")
-    return vb
 
 
 def interp(grid_b, vb0, vb1, alpha, grid_s, targets):

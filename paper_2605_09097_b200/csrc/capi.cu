@@ -340,6 +340,8 @@ osmpm_status osmpm_subdomain_info(osmpm_subdomain* sub, int64_t* n_particles, in
     SUB_CALL(sub, info(n_particles, box_lo, box_dims));
 }
 osmpm_status osmpm_sync(osmpm_subdomain* sub) { SUB_CALL(sub, sync()); }
+osmpm_status osmpm_checkpoint(osmpm_subdomain* sub) { SUB_CALL(sub, checkpoint()); }
+osmpm_status osmpm_restore(osmpm_subdomain* sub) { SUB_CALL(sub, restore()); }
 
 osmpm_status osmpm_subdomain_decomp(osmpm_subdomain* sub, int32_t* slabs_total, int32_t* slabs_local,
                                     int32_t* first_slab, int64_t* n_local, int32_t* cuts)
@@ -407,6 +409,7 @@ osmpm_status osmpm_coupler_create(osmpm_subdomain* coarse, osmpm_subdomain* fine
               "coupler: slab-decomposed subdomains are driven by the caller (osmpm_transmit / osmpm_implicit_solve), "
               "not by the coupler");
     CHECK_ARG(settings->M >= 1, "M must be >= 1");
+    CHECK_ARG(settings->k_max >= 1 || settings->parity_fixed_k >= 1, "k_max and parity_fixed_k both < 1: no Schwarz iteration");
     SET_DEVICE(coarse->ctx);
     return coupler_create(coarse, fine, settings, out);
 }

@@ -219,7 +219,7 @@ struct Coupler : public osmpm_coupler {
         if (nS) {
             B->KC();
             k_interp<D><<<nblk_all(nS, 256), 256, 0, st()>>>(nS, dS.p, geo_of(S), B->box, B->vn.p, nullptr, 0.0,
-                                                             vSprev.p);
+                                                             vSprev.p, B->err.p);
             OSMPM_LAUNCH_CHECK();
         }
         // the coarse subdomain's Schwarz Dirichlet data for the first coarse solve
@@ -235,10 +235,11 @@ struct Coupler : public osmpm_coupler {
         const int64_t nS = recvS.size();
         if (!nS) return OSMPM_OK;
         B->KC();
-        k_interp<D><<<nblk_all(nS, 256), 256, 0, st()>>>(nS, dS.p, geo_of(S), B->box, B->vn.p, nullptr, 0.0, vSn.p);
+        k_interp<D><<<nblk_all(nS, 256), 256, 0, st()>>>(nS, dS.p, geo_of(S), B->box, B->vn.p, nullptr, 0.0, vSn.p,
+                                                         B->err.p);
         B->KC();
         k_interp<D><<<nblk_all(nS, 256), 256, 0, st()>>>(nS, dS.p, geo_of(S), B->box, B->vnew.p, nullptr, 0.0,
-                                                         vSnp1.p);
+                                                         vSnp1.p, B->err.p);
         OSMPM_LAUNCH_CHECK();
         return OSMPM_OK;
     }

@@ -369,6 +369,18 @@ struct Dist : public osmpm_subdomain {
         return OSMPM_OK;
     }
 
+    // ---- a11: checkpoint / restore every slab (each slab keeps its own count) ---------------------
+    osmpm_status checkpoint() override
+    {
+        for (auto* s : sp) OSMPM_TRY(s->checkpoint());
+        return OSMPM_OK;
+    }
+    osmpm_status restore() override
+    {
+        for (auto* s : sp) OSMPM_TRY(s->restore());
+        return OSMPM_OK;
+    }
+
     // ---- a8: G2P on every slab, then migration across the cuts ---------------------------------
     osmpm_status g2p() override
     {

@@ -430,6 +430,7 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
         OSMPM_CU(cudaMemcpyAsync(gb.h_cgs, gb.cgs.p, sizeof(CGScalars), cudaMemcpyDeviceToHost, st));
         OSMPM_CU(cudaStreamSynchronize(st));
         sts->cg_iters += gb.h_cgs->it + (gb.h_cgs->done == 2 ? 1 : 0);
+        if (gb.h_cgs->done == 2) sts->negcurv++;
         if (gb.h_cgs->negcurv_first)
             for (int i = 0; i < G.ns; ++i) {
                 Sub<D, R>* q = G.s[i];
@@ -438,7 +439,7 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
             }
         // backtracking line search (R8)
         double alpha = 1.0, Et = 0.0, Eat = 0.0;
-        bool at_floor = false;
+        bool at_floor = false, ls_fail = false;
         for (;;) {
             for (int i = 0; i < G.ns; ++i) {
                 Sub<D, R>* q = G.s[i];
@@ -463,9 +464,15 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
                 fprintf(stderr, "[osmpm] ls stall: it %d |g| %.3e gref %.3e E0 %.17g Et-E0 %.3e Ea0 %.3e\n", it, gn,
                         gref, E0, Et - E0, Ea0);
             if (alpha < s->ls_min_alpha) {
+                // fixed-iteration mode (timing): no decrease found -> alpha = 0 (u unchanged), counted,
+                // and the solve goes on with the same work per iteration (R8)
+                if (s->fixed_iters) {
+                    ls_fail = true;
+                    break;
+                }
                 // no decrease of E_h is resolvable any more: once |g| has dropped below sqrt(rtol) * gref
                 // the iterate is accepted as converged at the roundoff floor of E_h (R8)
-                if (!s->fixed_iters && gn <= std::sqrt(s->newton_rtol) * gref) {
+                if (gn <= std::sqrt(s->newton_rtol) * gref) {
                     at_floor = true;
                     break;
                 }
@@ -476,8 +483,17 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
         }
         if (rc != OSMPM_OK) break;
         if (at_floor) {
+            sts->floor_accept = 1;
             converged = true;
             break;
+        }
+        if (ls_fail) {
+            // u stays; the last gradient pass ran at a trial point, so the next iteration recomputes
+            // g, the diagonal and the cache at u
+            sts->ls_failures++;
+            have_g = false;
+            sts->newton_iters = it + 1;
+            continue;
         }
         for (int i = 0; i < G.ns; ++i) {
             std::swap(G.s[i]->u.p, G.s[i]->ut.p);

@@ -582,11 +582,11 @@ __device__ __forceinline__ void cg_alpha(const double* v, CGScalars* s)
     {
         s->pq = v[0];
         if (!(v[0] > 0.0)) {
+            // non-positive curvature: stop, in fixed-iteration mode too (the remaining launches of a
+            // fixed solve then leave x unchanged; R7)
             s->alpha = 0.0;
-            if (!s->fixed) {
-                if (s->it == 0) s->negcurv_first = 1;
-                s->done = 2;  // negative curvature: stop (R7)
-            }
+            if (s->it == 0) s->negcurv_first = 1;
+            s->done = 2;
         } else {
             s->alpha = s->rz / v[0];
         }

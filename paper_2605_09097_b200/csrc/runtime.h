@@ -89,8 +89,8 @@ struct osmpm_ctx {
     osmpm::GroupComm gc;
     // grow-only device scratch of the per-call operators (transmit): no cudaMalloc / cudaFree (an
     // implicit device synchronisation) inside a time step
-    void* scratch[4] = {nullptr, nullptr, nullptr, nullptr};
-    size_t scratch_cap[4] = {0, 0, 0, 0};
+    void* scratch[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    size_t scratch_cap[6] = {0, 0, 0, 0, 0, 0};
     void* get_scratch(int k, size_t bytes)
     {
         if (scratch_cap[k] < bytes) {
@@ -129,4 +129,7 @@ struct osmpm_subdomain {
     virtual osmpm_status read_particles(double* x, double* v, double* F, double* B, osmpm_memspace sp) = 0;
     virtual osmpm_status info(int64_t* n, int64_t* lo, int64_t* dims) = 0;
     virtual osmpm_status sync() = 0;
+    // a11: store / restore the whole particle state on the device
+    virtual osmpm_status checkpoint() = 0;
+    virtual osmpm_status restore() = 0;
 };

@@ -141,7 +141,7 @@ struct Sub : public osmpm_subdomain {
     DBuf<uint8_t> act, dmask, fmask;
     DirList dir_user, dir_cpl;
     DBuf<double> stage_io;  // persistent host-I/O staging buffer
-    DBuf<double> pi_mom;  // affine-Pi moments when this subdomain is the coarse side (transmit.cuh)
+    DBuf<int> pi_gd;  // dense-box dims on the device when this subdomain is Pi's coarse side (transmit.cuh)
     DBuf<double> det_a, det_b, det_c;  // per-tile node blocks of the deterministic scatter mode (hvp_sw.cuh)
 
     // OSMPM_DETERMINISTIC=1: the sliding-window gradient and HVP store per-tile node blocks that a
@@ -337,7 +337,9 @@ struct Sub : public osmpm_subdomain {
         OSMPM_CU(cudaStreamSynchronize(st()));
         if (h.code) {
             OSMPM_CU(cudaMemsetAsync(err.p, 0, sizeof(ErrLatch), st()));
-            if (h.code == OSMPM_E_OUT_OF_DOMAIN)
+            if (h.code == OSMPM_E_INVALID_ARG)
+                set_error("transmit target %lld outside the destination node box", h.index);
+            else if (h.code == OSMPM_E_OUT_OF_DOMAIN)
                 set_error("particle %lld left the safe interior of the node box", h.index);
             else if (h.code == OSMPM_E_INVERTED_F)
                 set_error("particle %lld: det F <= 0 after G2P", h.index);
@@ -959,9 +961,12 @@ struct Sub : public osmpm_subdomain {
         return OSMPM_OK;
     }
 
-    // checkpoint / restore of the whole particle state (K11)
-    osmpm_status checkpoint()
+    // checkpoint / restore of the whole particle state (K11).  The slab's
+    // particle count is part of the state (migration changes it); the capacity never changes.
+    int64_t n_ck = 0;
+    osmpm_status checkpoint() override
     {
+        n_ck = n;
         OSMPM_TRY(Pck.need(L::NF * cap));
         OSMPM_TRY(matck.need(cap));
         OSMPM_TRY(pidck.need(cap));
@@ -973,12 +978,13 @@ struct Sub : public osmpm_subdomain {
         have_ck = true;
         return OSMPM_OK;
     }
-    osmpm_status restore()
+    osmpm_status restore() override
     {
         if (!have_ck) {
             set_error("restore without checkpoint");
             return OSMPM_E_STATE;
         }
+        n = n_ck;
         OSMPM_CU(cudaMemcpyAsync(P.p, Pck.p, (size_t)L::NF * cap * sizeof(R), cudaMemcpyDeviceToDevice, st()));
         OSMPM_CU(cudaMemcpyAsync(mat.p, matck.p, cap * sizeof(int), cudaMemcpyDeviceToDevice, st()));
         OSMPM_CU(cudaMemcpyAsync(pid.p, pidck.p, cap * sizeof(int), cudaMemcpyDeviceToDevice, st()));

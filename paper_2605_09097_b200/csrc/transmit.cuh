@@ -42,164 +42,165 @@ struct GridGeo {
     int gd[3];
 };
 
-// Pi numerator / denominator: every ACTIVE fine box node scatters m_j [v_j, 1] N_B,I(x_j)
-template <int D>
-__global__ void k_project(BoxDev fb, int64_t nown, const uint8_t* __restrict__ act, const double* __restrict__ m,
-                          const double* __restrict__ v, GridGeo cg, double* __restrict__ num, double* __restrict__ den)
-{
-    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= nown || !act[j]) return;  // ghost planes are projected by their owner
-    int i2 = (D == 3) ? (int)(j % fb.nn[2]) : 0;
-    int i1 = (D == 3) ? (int)((j / fb.nn[2]) % fb.nn[1]) : (int)(j % fb.nn[1]);
-    int i0 = (D == 3) ? (int)(j / ((int64_t)fb.nn[2] * fb.nn[1])) : (int)(j / fb.nn[1]);
-    const int gi[3] = {fb.lo[0] + i0, fb.lo[1] + i1, fb.lo[2] + i2};
-    double xj[3];
-#pragma unroll
-    for (int a = 0; a < D; ++a) xj[a] = fb.o[a] + fb.dx * (double)gi[a];
-    int64_t idx[27];
-    double N[27];
-    coarse_stencil<D>(xj, cg.o, cg.inv_dx, cg.gd, idx, N);
-    const double mj = m[j];
-#pragma unroll
-    for (int s = 0; s < Tile<D>::NS; ++s) {
-        if (idx[s] < 0) continue;
-        const double wgt = mj * N[s];
-        atomicAdd(&den[idx[s]], wgt);
-#pragma unroll
-        for (int a = 0; a < D; ++a) atomicAdd(&num[idx[s] * D + a], wgt * v[j * D + a]);
-    }
-}
-
-template <int D>
-__global__ void k_project_out(int64_t nt, const int64_t* __restrict__ targets, const double* __restrict__ num,
-                              const double* __restrict__ den, double eps, double* __restrict__ out)
-{
-    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= nt) return;
-    const int64_t I = targets ? targets[t] : t;
-#pragma unroll
-    for (int a = 0; a < D; ++a) out[t * D + a] = num[I * D + a] / (den[I] + eps);
-}
-
 // ---------------------------------------------------------------------------------------------
-// Affine variant of Pi (OSMPM_PI=affine; R21, NOT the paper's operator): the same weights
-// w_j = m_j N_B,I(x_j) feed the normal equations of the weighted least-squares affine fit
-// v ~ a + B xi, xi = (x_j - x_I)/dx_B, and the coarse value is a -- exact for affine fields under any
-// fine masses (the paper's support-wide mean is exact only for uniform masses, which biases the
-// rotation a bending section transmits).  Moments per coarse node: the symmetric (1+D)^2 matrix
-// (upper triangle, AF<D>::NA) and the (1+D) x D right-hand sides.
-template <int D> struct AF {
-    static constexpr int K = 1 + D, NA = K * (K + 1) / 2, NM = NA + K * D;
-    static __host__ __device__ constexpr int ai(int r, int q) { return r * K - r * (r - 1) / 2 + (q - r); }  // r <= q
-};
-static inline bool pi_affine()
+// Pi numerator / denominator (Eq. spatial_projection) as a GATHER:
+//   num_I = sum_j m_j v_j N_B,I(x_j),  den_I = sum_j m_j N_B,I(x_j)   over the active fine nodes j.
+// The coarse shape function is a tensor product, N_B,I(x_j) = prod_a N1((x_j,a - x_I,a)/dx_B), and the
+// fine nodes form a lattice, so the sum factorises into one 1-D pass per axis (last axis first):
+//   pass A  T1[i0][i1][c2] = sum_{i2} N1(.) f(i0,i1,i2),   f = act ? m [v, 1] : 0
+//   pass B  T2[i0][c1][c2] = sum_{i1} N1(.) T1[i0][i1][c2]                           (3D only)
+//   pass C  num/den[I0,I1,I2] += sum_{i0 owned} N1(.) T2[i0][c1][c2]
+// Every output is a fixed-order sum (no atomics: deterministic, and the fine box is read once);
+// c_a ranges over the coarse nodes whose support meets the fine box, clipped to the coarse dense box
+// (coarse nodes outside it receive nothing, R9).  Ghost planes (i0 >= n0own) belong to
+// the neighbour slab and are skipped in pass C.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ double bspline_kernel(double t)
 {
-    const char* e = getenv("OSMPM_PI");
-    return e && std::string(e) == "affine";
+    const double a = fabs(t);
+    if (a < 0.5) return 0.75 - a * a;
+    if (a < 1.5) return 0.5 * (1.5 - a) * (1.5 - a);
+    return 0.0;
 }
-template <int D>
-__global__ void k_project_affine(BoxDev fb, int64_t nown, const uint8_t* __restrict__ act, const double* __restrict__ m,
-                                 const double* __restrict__ v, GridGeo cg, double* __restrict__ mom)
+
+// one axis of the factorised sum: coarse node I (global index along the axis) against fine box nodes
+// l in [0, n): x_f(l) = xf0 + df l, x_I = oc + dc I
+struct PiAxis {
+    double xf0, df, oc, dc, inv_dc;
+    int n;       // fine box nodes along the axis
+    int clo, nc; // coarse range [clo, clo + nc)
+};
+__device__ __forceinline__ void pi_support(const PiAxis& ax, int I, int& l0, int& l1)
 {
-    using A = AF<D>;
-    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= nown || !act[j]) return;
-    int i2 = (D == 3) ? (int)(j % fb.nn[2]) : 0;
-    int i1 = (D == 3) ? (int)((j / fb.nn[2]) % fb.nn[1]) : (int)(j % fb.nn[1]);
-    int i0 = (D == 3) ? (int)(j / ((int64_t)fb.nn[2] * fb.nn[1])) : (int)(j / fb.nn[1]);
-    const int gi[3] = {fb.lo[0] + i0, fb.lo[1] + i1, fb.lo[2] + i2};
-    double xj[3];
+    const double xI = ax.oc + ax.dc * (double)I;
+    l0 = max(0, (int)ceil((xI - 1.5 * ax.dc - ax.xf0) / ax.df) - 1);
+    l1 = min(ax.n - 1, (int)floor((xI + 1.5 * ax.dc - ax.xf0) / ax.df) + 1);
+}
+__device__ __forceinline__ double pi_weight(const PiAxis& ax, int I, int l)
+{
+    return bspline_kernel((ax.xf0 + ax.df * (double)l - (ax.oc + ax.dc * (double)I)) * ax.inv_dc);
+}
+
+template <int D>
+struct PiGeo {
+    PiAxis ax[3];
+};
+
+// pass A: the last axis, from the fine node fields
+template <int D>
+__global__ void k_pi_pass_a(PiGeo<D> G, int64_t nout, const uint8_t* __restrict__ act, const double* __restrict__ m,
+                            const double* __restrict__ v, double* __restrict__ T1)
+{
+    constexpr int F = D + 1;
+    const PiAxis& A = G.ax[D - 1];
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < nout; o += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(o % A.nc);
+        const int64_t row = o / A.nc;  // (i0, i1) in 3D, i0 in 2D
+        const int I = A.clo + c;
+        int l0, l1;
+        pi_support(A, I, l0, l1);
+        double acc[F];
 #pragma unroll
-    for (int a = 0; a < D; ++a) xj[a] = fb.o[a] + fb.dx * (double)gi[a];
-    int64_t idx[27];
-    double N[27];
-    coarse_stencil<D>(xj, cg.o, cg.inv_dx, cg.gd, idx, N);
-    const double mj = m[j];
-    for (int s = 0; s < Tile<D>::NS; ++s) {
-        const int64_t I = idx[s];
-        if (I < 0) continue;
-        int kI[3] = {0, 0, 0};
-        if (D == 3) {
-            kI[2] = (int)(I % cg.gd[2]);
-            kI[1] = (int)((I / cg.gd[2]) % cg.gd[1]);
-            kI[0] = (int)(I / ((int64_t)cg.gd[2] * cg.gd[1]));
-        } else {
-            kI[1] = (int)(I % cg.gd[1]);
-            kI[0] = (int)(I / cg.gd[1]);
+        for (int k = 0; k < F; ++k) acc[k] = 0.0;
+        for (int l = l0; l <= l1; ++l) {
+            const int64_t j = row * A.n + l;
+            if (!act[j]) continue;
+            const double w = pi_weight(A, I, l);
+            if (w == 0.0) continue;
+            const double mw = m[j] * w;
+#pragma unroll
+            for (int a = 0; a < D; ++a) acc[a] += mw * v[j * D + a];
+            acc[D] += mw;
         }
-        double phi[A::K];
-        phi[0] = 1.0;
 #pragma unroll
-        for (int a = 0; a < D; ++a) phi[1 + a] = (xj[a] - (cg.o[a] + cg.dx * (double)kI[a])) * cg.inv_dx;
-        const double w = mj * N[s];
-        double* mo = mom + I * A::NM;
-#pragma unroll
-        for (int r = 0; r < A::K; ++r) {
-#pragma unroll
-            for (int q = r; q < A::K; ++q) atomicAdd(&mo[A::ai(r, q)], w * phi[r] * phi[q]);
-#pragma unroll
-            for (int a = 0; a < D; ++a) atomicAdd(&mo[A::NA + r * D + a], w * phi[r] * v[j * D + a]);
-        }
+        for (int k = 0; k < F; ++k) T1[o * F + k] = acc[k];
     }
 }
 
-// solve the normal equations of each target coarse node (Gaussian elimination with partial pivoting);
-// a node whose fine support does not span D dimensions keeps the mass-weighted mean num / (den + eps)
-template <int D>
-__global__ void k_project_out_affine(int64_t nt, const int64_t* __restrict__ targets, const double* __restrict__ num,
-                                     const double* __restrict__ den, const double* __restrict__ mom, double eps,
-                                     double* __restrict__ out)
+// pass B (3D): axis 1.  T1[i0][i1][c2][F] -> T2[i0][c1][c2][F]
+__global__ void k_pi_pass_b(PiGeo<3> G, int64_t nout, const double* __restrict__ T1, double* __restrict__ T2)
 {
-    using A = AF<D>;
+    constexpr int F = 4;
+    const PiAxis& A = G.ax[1];
+    const int nc2 = G.ax[2].nc;
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < nout; o += (int64_t)gridDim.x * blockDim.x) {
+        const int c2 = (int)(o % nc2);
+        const int c1 = (int)((o / nc2) % A.nc);
+        const int64_t i0 = o / ((int64_t)nc2 * A.nc);
+        const int I = A.clo + c1;
+        int l0, l1;
+        pi_support(A, I, l0, l1);
+        double acc[F] = {0.0, 0.0, 0.0, 0.0};
+        for (int l = l0; l <= l1; ++l) {
+            const double w = pi_weight(A, I, l);
+            if (w == 0.0) continue;
+            const double* t = T1 + ((i0 * A.n + l) * nc2 + c2) * F;
+#pragma unroll
+            for (int k = 0; k < F; ++k) acc[k] += w * t[k];
+        }
+#pragma unroll
+        for (int k = 0; k < F; ++k) T2[o * F + k] = acc[k];
+    }
+}
+
+// pass C: axis 0 over the owned planes, added into the coarse dense num (nnb*D) / den (nnb)
+template <int D>
+__global__ void k_pi_pass_c(PiGeo<D> G, int n0own, const int* __restrict__ gdc, const double* __restrict__ T,
+                            double* __restrict__ num, double* __restrict__ den)
+{
+    constexpr int F = D + 1;
+    const PiAxis& A = G.ax[0];
+    const int nc1 = G.ax[1].nc, nc2 = (D == 3) ? G.ax[2].nc : 1;
+    const int64_t nout = (int64_t)A.nc * nc1 * nc2;
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < nout; o += (int64_t)gridDim.x * blockDim.x) {
+        const int c2 = (int)(o % nc2);
+        const int c1 = (int)((o / nc2) % nc1);
+        const int c0 = (int)(o / ((int64_t)nc2 * nc1));
+        const int I0 = A.clo + c0;
+        int l0, l1;
+        pi_support(A, I0, l0, l1);
+        l1 = min(l1, n0own - 1);
+        double acc[F];
+#pragma unroll
+        for (int k = 0; k < F; ++k) acc[k] = 0.0;
+        for (int l = l0; l <= l1; ++l) {
+            const double w = pi_weight(A, I0, l);
+            if (w == 0.0) continue;
+            const double* t = T + (((int64_t)l * nc1 + c1) * nc2 + c2) * F;
+#pragma unroll
+            for (int k = 0; k < F; ++k) acc[k] += w * t[k];
+        }
+        const int I1 = G.ax[1].clo + c1;
+        const int64_t I = (D == 3) ? ((int64_t)I0 * gdc[1] + I1) * gdc[2] + (G.ax[2].clo + c2) : (int64_t)I0 * gdc[1] + I1;
+#pragma unroll
+        for (int a = 0; a < D; ++a) num[I * D + a] += acc[a];
+        den[I] += acc[D];
+    }
+}
+
+// targets of a transmit call must lie in the destination's dense node box; an index outside it is
+// skipped (output 0) and latched as INVALID_ARG with its position in the target list
+__device__ __forceinline__ bool target_ok(int64_t I, int64_t nmax, ErrLatch* err, int64_t t)
+{
+    if (I >= 0 && I < nmax) return true;
+    latch_error(err, OSMPM_E_INVALID_ARG, t);
+    return false;
+}
+
+template <int D>
+__global__ void k_project_out(int64_t nt, const int64_t* __restrict__ targets, int64_t nnb, const double* __restrict__ num,
+                              const double* __restrict__ den, double eps, double* __restrict__ out, ErrLatch* err)
+{
     int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= nt) return;
     const int64_t I = targets ? targets[t] : t;
-    const double* mo = mom + I * A::NM;
-    double M[A::K][A::K], rhs[A::K][D];
+    if (!target_ok(I, nnb, err, t)) {
 #pragma unroll
-    for (int r = 0; r < A::K; ++r) {
-#pragma unroll
-        for (int q = 0; q < A::K; ++q) M[r][q] = mo[A::ai(r < q ? r : q, r < q ? q : r)];
-#pragma unroll
-        for (int a = 0; a < D; ++a) rhs[r][a] = mo[A::NA + r * D + a];
+        for (int a = 0; a < D; ++a) out[t * D + a] = 0.0;
+        return;
     }
 #pragma unroll
     for (int a = 0; a < D; ++a) out[t * D + a] = num[I * D + a] / (den[I] + eps);
-    const double s0 = M[0][0];
-    if (!(s0 > 0.0)) return;
-    M[0][0] += eps;
-    for (int col = 0; col < A::K; ++col) {
-        int piv = col;
-        for (int r = col + 1; r < A::K; ++r)
-            if (fabs(M[r][col]) > fabs(M[piv][col])) piv = r;
-        if (!(fabs(M[piv][col]) > 1e-4 * s0)) return;  // the fit would amplify rounding: keep the mean
-        if (piv != col) {
-            for (int q = 0; q < A::K; ++q) {
-                const double tq = M[col][q];
-                M[col][q] = M[piv][q];
-                M[piv][q] = tq;
-            }
-            for (int a = 0; a < D; ++a) {
-                const double ta = rhs[col][a];
-                rhs[col][a] = rhs[piv][a];
-                rhs[piv][a] = ta;
-            }
-        }
-        for (int r = col + 1; r < A::K; ++r) {
-            const double f = M[r][col] / M[col][col];
-            for (int q = col; q < A::K; ++q) M[r][q] -= f * M[col][q];
-            for (int a = 0; a < D; ++a) rhs[r][a] -= f * rhs[col][a];
-        }
-    }
-    double sol[A::K][D];
-    for (int r = A::K - 1; r >= 0; --r)
-        for (int a = 0; a < D; ++a) {
-            double tv = rhs[r][a];
-            for (int q = r + 1; q < A::K; ++q) tv -= M[r][q] * sol[q][a];
-            sol[r][a] = tv / M[r][r];
-        }
-#pragma unroll
-    for (int a = 0; a < D; ++a) out[t * D + a] = sol[0][a];
 }
 
 // I + T: v_j = (1 - alpha) sum_I v0_I N_I(x_j) + alpha sum_I v1_I N_I(x_j); the coarse fields live
@@ -207,11 +208,17 @@ __global__ void k_project_out_affine(int64_t nt, const int64_t* __restrict__ tar
 template <int D>
 __global__ void k_interp(int64_t nt, const int64_t* __restrict__ targets, GridGeo fg, BoxDev cb,
                          const double* __restrict__ v0, const double* __restrict__ v1, double alpha,
-                         double* __restrict__ out)
+                         double* __restrict__ out, ErrLatch* err)
 {
     int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= nt) return;
     const int64_t j = targets ? targets[t] : t;
+    const int64_t nfine = (int64_t)fg.gd[0] * fg.gd[1] * (D == 3 ? fg.gd[2] : 1);
+    if (!target_ok(j, nfine, err, t)) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) out[t * D + a] = 0.0;
+        return;
+    }
     int g2 = (D == 3) ? (int)(j % fg.gd[2]) : 0;
     int g1 = (D == 3) ? (int)((j / fg.gd[2]) % fg.gd[1]) : (int)(j % fg.gd[1]);
     int g0 = (D == 3) ? (int)(j / ((int64_t)fg.gd[2] * fg.gd[1])) : (int)(j / fg.gd[1]);
@@ -257,7 +264,8 @@ static GridGeo geo_of(const S* s)
 }
 
 // Pi over ALL coarse dense nodes: num (nnB*D), den (nnB) device buffers of the coarse side.  The
-// fine side may be a group of slabs (each projects its owned nodes; sums all-reduced over ranks).
+// fine side may be a group of slabs (each projects its owned nodes, in slab order; sums all-reduced
+// over ranks).
 template <int D, typename R>
 osmpm_status project_accumulate_group(SlabGroup<D, R> F, Sub<D, R>* coarse, bool use_solved, double* num)
 {
@@ -267,43 +275,72 @@ osmpm_status project_accumulate_group(SlabGroup<D, R> F, Sub<D, R>* coarse, bool
     double* denp = num + nnb * D;  // num and den contiguous: one all-reduce
     auto& pf = F.ctx->prof;
     if (pf.on) pf.begin("transmit", st);
+    int* gdc = coarse->pi_gd.p;
+    if (!gdc) {
+        OSMPM_TRY(coarse->pi_gd.need(3));
+        int h[3] = {(int)coarse->gdims[0], (int)coarse->gdims[1], (int)coarse->gdims[2]};
+        OSMPM_CU(cudaMemcpy(coarse->pi_gd.p, h, sizeof(h), cudaMemcpyHostToDevice));
+        gdc = coarse->pi_gd.p;
+    }
     for (int i = 0; i < F.ns; ++i) {
         Sub<D, R>* fine = F.s[i];
+        if (fine->box.nnodes == 0 || fine->nown == 0) continue;
         const double* v = use_solved ? fine->vnew.p : fine->vn.p;
+        PiGeo<D> G{};
+        bool empty = false;
+        for (int a = 0; a < D; ++a) {
+            PiAxis& A = G.ax[a];
+            A.df = fine->box.dx;
+            A.xf0 = fine->box.o[a] + fine->box.dx * (double)fine->box.lo[a];
+            A.n = fine->box.nn[a];
+            A.oc = coarse->origin[a];
+            A.dc = coarse->dx;
+            A.inv_dc = 1.0 / coarse->dx;
+            const double xlo = A.xf0, xhi = A.xf0 + A.df * (A.n - 1);
+            const int lo = std::max<int>(0, (int)std::floor((xlo - 1.5 * A.dc - A.oc) / A.dc) - 1);
+            const int hi = std::min<int>((int)coarse->gdims[a] - 1, (int)std::ceil((xhi + 1.5 * A.dc - A.oc) / A.dc) + 1);
+            A.clo = lo;
+            A.nc = hi - lo + 1;
+            if (A.nc <= 0) empty = true;
+        }
+        if (empty) continue;
+        const int64_t plane = (D == 3) ? (int64_t)fine->box.nn[1] * fine->box.nn[2] : fine->box.nn[1];
+        const int n0own = (int)(fine->nown / plane);
+        const int64_t n_a = (D == 3) ? (int64_t)G.ax[0].n * G.ax[1].n * G.ax[2].nc : (int64_t)G.ax[0].n * G.ax[1].nc;
+        double* T1 = (double*)F.ctx->get_scratch(4, (size_t)n_a * (D + 1) * sizeof(double));
+        if (!T1) return OSMPM_E_OOM;
         fine->KC();
-        k_project<D><<<nblk_all(fine->box.nnodes, 256), 256, 0, st>>>(fine->box, fine->nown, fine->act.p, fine->m.p, v,
-                                                                      geo_of(coarse), num, denp);
+        k_pi_pass_a<D><<<nblk_all(n_a, 256), 256, 0, st>>>(G, n_a, fine->act.p, fine->m.p, v, T1);
+        OSMPM_LAUNCH_CHECK();
+        const double* Tc = T1;
+        if constexpr (D == 3) {
+            const int64_t n_b = (int64_t)G.ax[0].n * G.ax[1].nc * G.ax[2].nc;
+            double* T2 = (double*)F.ctx->get_scratch(5, (size_t)n_b * 4 * sizeof(double));
+            if (!T2) return OSMPM_E_OOM;
+            fine->KC();
+            k_pi_pass_b<<<nblk_all(n_b, 256), 256, 0, st>>>(G, n_b, T1, T2);
+            OSMPM_LAUNCH_CHECK();
+            Tc = T2;
+        }
+        const int64_t n_c = (int64_t)G.ax[0].nc * G.ax[1].nc * (D == 3 ? G.ax[2].nc : 1);
+        fine->KC();
+        k_pi_pass_c<D><<<nblk_all(n_c, 256), 256, 0, st>>>(G, n0own, gdc, Tc, num, denp);
         OSMPM_LAUNCH_CHECK();
     }
     OSMPM_TRY(group_allreduce<D, R>(F, num, (int)(nnb * (D + 1))));
-    if (pi_affine()) {
-        OSMPM_TRY(coarse->pi_mom.need((size_t)nnb * AF<D>::NM));
-        OSMPM_CU(cudaMemsetAsync(coarse->pi_mom.p, 0, nnb * AF<D>::NM * sizeof(double), st));
-        for (int i = 0; i < F.ns; ++i) {
-            Sub<D, R>* fine = F.s[i];
-            const double* v = use_solved ? fine->vnew.p : fine->vn.p;
-            fine->KC();
-            k_project_affine<D><<<nblk_all(fine->box.nnodes, 256), 256, 0, st>>>(
-                fine->box, fine->nown, fine->act.p, fine->m.p, v, geo_of(coarse), coarse->pi_mom.p);
-            OSMPM_LAUNCH_CHECK();
-        }
-        OSMPM_TRY(group_allreduce<D, R>(F, coarse->pi_mom.p, (int)(nnb * AF<D>::NM)));
-    }
     if (pf.on) pf.end("transmit", st);
     return OSMPM_OK;
 }
 
-// the projected coarse values of nt target nodes (Pi, or its affine variant under OSMPM_PI=affine)
+// the projected coarse values of nt target nodes
 template <int D, typename R>
 osmpm_status project_out(cudaStream_t st, Sub<D, R>* coarse, int64_t nt, const int64_t* targets, const double* num,
                          const double* den, double eps, double* out)
 {
     if (nt <= 0) return OSMPM_OK;
     coarse->KC();
-    if (pi_affine())
-        k_project_out_affine<D><<<nblk_all(nt, 256), 256, 0, st>>>(nt, targets, num, den, coarse->pi_mom.p, eps, out);
-    else
-        k_project_out<D><<<nblk_all(nt, 256), 256, 0, st>>>(nt, targets, num, den, eps, out);
+    k_project_out<D><<<nblk_all(nt, 256), 256, 0, st>>>(nt, targets, coarse->dense_nodes(), num, den, eps, out,
+                                                        coarse->err.p);
     OSMPM_LAUNCH_CHECK();
     return OSMPM_OK;
 }
@@ -351,6 +388,15 @@ osmpm_status transmit_impl(SlabGroup<D, R> SG, Sub<D, R>* src, Sub<D, R>* dstc, 
     osmpm_ctx* cx = SG.ctx;
     const int64_t* tptr = targets;
     if (targets && sp == OSMPM_HOST) {
+        // host targets are checked here; device targets in the kernels (latched, surfaced at the next
+        // synchronising call)
+        const int64_t nmax = (dir == OSMPM_FINE_TO_COARSE) ? (dstc ? dstc->dense_nodes() : 0) : dst_nodes;
+        for (int64_t t = 0; t < nt; ++t)
+            if (targets[t] < 0 || targets[t] >= nmax) {
+                set_error("transmit: target %lld = node %lld outside the destination node box (%lld nodes)",
+                          (long long)t, (long long)targets[t], (long long)nmax);
+                return OSMPM_E_INVALID_ARG;
+            }
         int64_t* tg = (int64_t*)cx->get_scratch(0, nt * sizeof(int64_t));
         if (!tg) return OSMPM_E_OOM;
         OSMPM_CU(cudaMemcpyAsync(tg, targets, nt * sizeof(int64_t), cudaMemcpyHostToDevice, st));
@@ -383,7 +429,8 @@ osmpm_status transmit_impl(SlabGroup<D, R> SG, Sub<D, R>* src, Sub<D, R>* dstc, 
             if (src->ctx->prof.on) src->ctx->prof.begin("transmit", st);
             src->KC();
             k_interp<D><<<nblk_all(nt, 256), 256, 0, st>>>(nt, tptr, dst_geo, src->box, src->vn.p,
-                                                           need_solved ? src->vnew.p : nullptr, alpha, optr);
+                                                           need_solved ? src->vnew.p : nullptr, alpha, optr,
+                                                           src->err.p);
             OSMPM_LAUNCH_CHECK();
             if (src->ctx->prof.on) src->ctx->prof.end("transmit", st);
         }

@@ -54,7 +54,8 @@ class NewtonSettings(C.Structure):
 class SolveStats(C.Structure):
     _fields_ = [("newton_iters", C.c_int32), ("cg_iters", C.c_int32), ("ls_halvings", C.c_int32),
                 ("status", C.c_int32), ("grad_norm0", C.c_double), ("grad_norm", C.c_double),
-                ("energy", C.c_double)]
+                ("energy", C.c_double), ("negcurv", C.c_int32), ("ls_failures", C.c_int32),
+                ("floor_accept", C.c_int32), ("reserved", C.c_int32)]
 
 
 class SchwarzSettings(C.Structure):
@@ -361,6 +362,12 @@ class Subdomain:
 
     def sync(self):
         _check(lib().osmpm_sync(self._h))
+
+    def checkpoint(self):
+        _check(lib().osmpm_checkpoint(self._h))
+
+    def restore(self):
+        _check(lib().osmpm_restore(self._h))
 
     def decomp(self):
         """(slabs_total, slabs_local, first_slab, n_local_particles, cuts)"""

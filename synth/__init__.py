@@ -319,3 +319,32 @@ def c5_coarse_field(grid_fine: Grid, n_cells=128, seed=5001, dx_coarse=1.0 / 128
         a = rng.normal(0.0, amp, size=3)
         v += np.cos(xn @ kv + ph)[:, None] * a[None, :]
     return grid, v.reshape(nn, nn, nn, 3)
+
+
+def c5_bench_workload(cells=128, full_box=True):
+    """The timed C5 workload of bench.py: the fine cube of c5_stress, a passive coarse
+    subdomain of one particle per coarse cell carrying the smooth field of c5_coarse_field (its P2G
+    gives v_B^n; bench.py sets v_B^{n+1} = 1.01 v_B^n), and the fine receivers: the fine nodes of the
+    cube's footprint outside the cube shrunk by 2 cells, as linear indices of the fine node box.
+    Returns (fine Scene, coarse Scene, receivers int64[])."""
+    fine = c5_stress(n_cells=cells, full_box=full_box)
+    cgrid, cvel = c5_coarse_field(fine.grid, n_cells=cells)
+    side = cells * fine.grid.dx
+    lo = 0.5 - side / 2
+    xb, vol = lattice([lo] * 3, [lo + side] * 3, cgrid.dx, 1)
+    cpart = make_particles(xb, vol, 1000.0)
+    idx = np.clip(np.round((xb - np.asarray(cgrid.origin)) / cgrid.dx).astype(int), 0, cgrid.dims[0] - 1)
+    cpart.v = np.ascontiguousarray(cvel[idx[:, 0], idx[:, 1], idx[:, 2]])
+    coarse = Scene(cgrid, cpart, [(1.0e5, 0.3)], 4e-3, (0.0, 0.0, 0.0))
+    # footprint nodes k0-1 .. k0+cells+1 (absolute node indices of the 1/512 lattice) minus the
+    # cube shrunk by 2 cells, as indices of this fine grid's box
+    dx = fine.grid.dx
+    k0 = int(round(lo / dx))
+    kk = np.arange(k0 - 1, k0 + cells + 2)
+    K = np.stack(np.meshgrid(kk, kk, kk, indexing="ij"), -1).reshape(-1, 3)
+    inner = np.all((K >= k0 + 2) & (K <= k0 + cells - 2), axis=1)
+    R = K[~inner] - np.round(np.asarray(fine.grid.origin) / dx).astype(np.int64)[None, :]
+    gd = fine.grid.dims
+    assert (R >= 0).all() and (R < np.asarray(gd)[None, :3]).all()
+    recv = (R[:, 0] * gd[1] + R[:, 1]) * gd[2] + R[:, 2]
+    return fine, coarse, np.ascontiguousarray(recv.astype(np.int64))

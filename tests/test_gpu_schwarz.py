@@ -114,29 +114,3 @@ def test_free_fall_is_the_converged_frame(ctx, M):
         x, v = TOS.free_fall_closed_form(sc.particles.x, c, g, sc.dt, n)
         np.testing.assert_allclose(out["v"], np.tile(v, (sc.particles.n, 1)), rtol=0, atol=1e-8)
         np.testing.assert_allclose(out["x"], x, rtol=0, atol=1e-10)
-
-
-def test_cantilever_frame_parity_affine_pi(ctx, monkeypatch):
-    """The C1 frame of test_cantilever_frame_parity with OSMPM_PI=affine (R21) against the
-    oracle frame run with oracle.project_affine in place of the paper's Pi."""
-    monkeypatch.setenv("OSMPM_PI", "affine")
-
-    def affine(grid_s, gs, grid_b, eps_tol=0.0, v_fine=None, m_fine=None, active_fine=None):
-        vb = oracle.project_affine(grid_s, gs, grid_b, eps_tol, v_fine, m_fine, active_fine)
-        _, num, den = oracle.project(grid_s, gs, grid_b, eps_tol, v_fine, m_fine, active_fine)
-        return vb, num, den
-
-    monkeypatch.setattr(OS, "project", affine)
-    coarse, fine = synth.c1_cantilever()
-    M, K = 4, 3
-    sel = _clamp(fine)
-    nn = oracle.n_nodes(fine.grid)
-    mask = np.zeros((nn, 2), np.uint8)
-    mask[sel] = 1
-    ref = OS.schwarz_step(coarse, fine, M, parity_fixed_k=K, user_S=OS.UserBC(mask, np.zeros((nn, 2))),
-                          newton_coarse=oracle.default_settings(**TIGHT), newton_fine=oracle.default_settings(**TIGHT))
-    sb, ss, rep, _ = _gpu_frame(ctx, coarse, fine, M, K, clamp_fine=sel)
-    fo, co = ss.read_particles(), sb.read_particles()
-    for out, r, x0 in ((fo, ref.fine_particles, fine.particles.x), (co, ref.coarse_particles, coarse.particles.x)):
-        assert rel_linf(out["x"] - x0, r.x - x0) <= 1e-8
-        assert rel_linf(out["v"], r.v) <= 1e-8

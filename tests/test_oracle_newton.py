@@ -255,3 +255,43 @@ def test_newton_accepts_the_energy_roundoff_floor():
                                  raise_on_error=False)
     assert s.status == 0 and s.ls_halvings > 0
     assert s.grad_norm <= 1e-4 * s.grad_norm0 and s.grad_norm > 1e-8 * s.grad_norm0
+    assert s.floor_accept == 1  # the loosened acceptance is reported, never silent
+    # a solve that reaches newton_rtol does not raise the flag
+    sc = synth.random_fixture(dim=2, seed=57, cells=(4, 3, 1))
+    _, s2 = oracle.implicit_solve(sc, oracle.p2g(sc), oracle.default_settings(newton_rtol=1e-10, cg_rtol=1e-12))
+    assert s2.status == 0 and s2.floor_accept == 0
+
+
+def test_fixed_mode_line_search_failure_takes_zero_step():
+    """R8 fixed-iteration policy: when no trial step decreases E_h (forced here by max_cg = 0, i.e. a
+    zero Newton direction, and a negative noise tolerance, so that no trial is ever accepted), the
+    solve neither errors nor moves: alpha = 0 is taken, every such iteration is counted, and u stays
+    at the initial guess x^ = x~ (u = dt v^n on free DOFs)."""
+    sc = synth.random_fixture(dim=3, seed=58, cells=(3, 2, 2))
+    gs = oracle.p2g(sc)
+    st = oracle.default_settings(max_newton=4, max_cg=0, fixed_iters=1, energy_noise_rtol=-1.0)
+    u, s = oracle.implicit_solve(sc, gs, st)
+    act = gs.active.astype(bool)
+    assert s.status == 0 and s.ls_failures == 4 and s.newton_iters == 4 and s.ls_halvings == 4 * 21
+    assert np.array_equal(u[act], sc.dt * gs.v[act])
+    # the same settings in tolerance mode are a LINESEARCH_STAGNATION error
+    _, s3 = oracle.implicit_solve(sc, gs, oracle.default_settings(max_cg=0, energy_noise_rtol=-1.0),
+                                  raise_on_error=False)
+    assert s3.status == oracle.LS_STAGNATION and s3.ls_failures == 0
+
+
+def test_fixed_mode_negative_curvature_stops_pcg():
+    """R7: p^T H p <= 0 stops PCG in both modes.  A strongly compressed state (F = 0.3 I, so that
+    mu - lambda ln J > mu s^2) makes the neo-Hookean tangent indefinite for rotation-like modes; from
+    u = 0 (guess 1) the Krylov directions meet it and the event is counted, in fixed mode as well, with
+    the PCG iterations cut short (fewer than the 2 x 30 a fixed solve would otherwise run)."""
+    sc = synth.random_fixture(dim=2, seed=59, cells=(4, 4, 1), F_sigma=0.0)
+    sc.particles.F[:] = np.diag([0.3, 0.3])
+    sc.dt = 1.0
+    gs = oracle.p2g(sc)
+    for fixed in (1, 0):
+        u, s = oracle.implicit_solve(sc, gs, oracle.default_settings(max_newton=2, max_cg=30, fixed_iters=fixed,
+                                                                     guess=1), raise_on_error=False)
+        assert s.negcurv >= 1 and s.cg_iters < 60
+        if fixed:
+            assert s.status == 0 and s.newton_iters == 2

@@ -223,34 +223,3 @@ def test_interp_time_reproduces_linear(dim):
     oh = oracle.interp(gB, w0, w1, 0.3, gS, targets)
     np.testing.assert_array_equal(o0, oracle.interp(gB, w0, w0, 0.7, gS, targets) * 0 + o0)
     np.testing.assert_allclose(oh, 0.7 * o0 + 0.3 * o1, rtol=0, atol=1e-14)
-
-
-@pytest.mark.parametrize("dim", [2, 3])
-def test_affine_projection_reproduces_affine_fields_under_any_mass(dim):
-    """R21 (not the paper's operator): the affine variant of Pi is exact for affine fields whatever the
-    fine masses, where the paper's mass-weighted Pi is exact only for uniform ones --
-    the bias that holds a quasi-static coupled cantilever at half its deflection."""
-    rng = np.random.default_rng(22)
-    for r, off in ((2, 0.0), (4, 0.37), (8, 0.0)):
-        gS, gB = _coarse_fine_pair(dim, r, off)
-        kS, xS = _nodes(gS)
-        kB, xB = _nodes(gB)
-        nS = xS.shape[0]
-        act = np.ones(nS, np.uint8)
-        m = rng.uniform(0.2, 3.0, nS)                   # strongly non-uniform fine masses
-        A = rng.normal(size=(dim, dim))
-        c = rng.normal(size=dim)
-        gsf = oracle.GridState(m, None, xS @ A.T + c, None, None, act)
-        lo = np.asarray(gS.origin[:dim]) + 1.5 * gB.dx
-        hi = np.asarray(gS.origin[:dim]) + (gS.dims[0] - 1) * gS.dx - 1.5 * gB.dx
-        full = np.all((xB >= lo - 1e-12) & (xB <= hi + 1e-12), axis=1)
-        assert full.sum() >= 1
-        va = oracle.project_affine(gS, gsf, gB, 0.0)
-        np.testing.assert_allclose(va[full], xB[full] @ A.T + c, rtol=0, atol=1e-11)
-        vp, _, den = oracle.project(gS, gsf, gB, 0.0)
-        assert np.abs(vp[full] - (xB[full] @ A.T + c)).max() > 1e-4   # the paper's Pi is biased here
-        # constants stay exact on every covered node (fallback nodes keep Pi's value)
-        gsc = oracle.GridState(m, None, np.tile(c, (nS, 1)), None, None, act)
-        vc = oracle.project_affine(gS, gsc, gB, 0.0)
-        cov = den > 0
-        np.testing.assert_allclose(vc[cov], np.tile(c, (cov.sum(), 1)), rtol=0, atol=1e-11)
