@@ -124,8 +124,16 @@ FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 
 
 def hvp_algorithmic_bytes(n_particles, n_active_nodes, word):
-    # per particle: x (3) + Newton cache S' (6) + Ah (9) + c' + l' (2) = 20 words of the particle
-    # precision; per active node: read d (3) + write y (3) fp64 words
+    """SURVEY.md §8(d) accounting of one HVP launch: 190 B per particle in fp64, 95 B in fp32 (App. C:
+    the particle's position, F^n-derived Newton cache and V^0 plus its share of the node vectors d and
+    y), times the particles the launch processes.  (The reformulated kernel reads only 20 particle
+    words + 48 B per active node -- `reformulated_bytes_per_launch` below.)"""
+    return n_particles * (190 if word == 8 else 95)
+
+
+def hvp_reformulated_bytes(n_particles, n_active_nodes, word):
+    # x (3) + Newton cache S' (6) + Ah (9) + c' + l' (2) = 20 words of the particle precision per particle;
+    # read d (3) + write y (3) fp64 words per active node (DESIGN.md §5)
     return n_particles * 20 * word + n_active_nodes * 6 * 8
 
 
@@ -481,8 +489,11 @@ def main():
                    "slab_cuts": cuts,
                    "l2": "working set (>3 GB) far larger than the 126 MB L2; no flush needed"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak if achieved else None,
-                     "traffic": traffic, "kernel": "k_hvp", "peak_kind": peak_kind,
+                     "traffic": traffic, "traffic_source": f"profiles/ncu_hvp_{args.precision}.json (ncu --set full)",
+                     "kernel": "k_hvp_sw", "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": hvp_bytes, "avg_launch_ms": hvp_avg_ms,
+                     "accounting": "SURVEY.md §8(d): 190 B/particle fp64 (95 fp32) x particles per launch",
+                     "reformulated_bytes_per_launch": hvp_reformulated_bytes(n_local, n_active, word),
                      "launches": hv_n,
                      # the same launches against the CUDA-core floating-point peak (the
                      # fp64 HVP's compute ceiling lies at 68 % of the HBM roofline)

@@ -716,6 +716,11 @@ int orc_g2p(const orc_grid* g, int64_t np, double* x, double* v, double* F, doub
             v[p * d + a] = vp[a];
             x[p * d + a] += dt * vp[a];
         }
+        /* the advected position must stay in the safe interior (SPEC.md:123 advect "errors") */
+        if (orc_stencil(g, x + p * d, idx, N, gN, xip) < 0) {
+            if (bad) *bad = p;
+            return ORC_OUT_OF_DOMAIN;
+        }
     }
     return ORC_OK;
 }

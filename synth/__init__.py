@@ -266,7 +266,7 @@ def c4_fold(seed_fine=4000, seed_coarse=4001, y_extent=0.5):
             Scene(grid_around(xs, dxs, 4, 3), ps, mats, 2.5e-3, (0.0, 0.0, -9.81), meta={"config": "C4", "M": 4}))
 
 
-def c5_stress(n_cells=128, seed=5000, dx=1.0 / 512, full_box=True):
+def c5_stress(n_cells=128, seed=5000, dx=1.0 / 512, full_box=True, pad=3):
     """C5: a random-density neo-Hookean cube of n_cells^3 cells at dx = 1/512 centred at
     (0.5, 0.5, 0.5) inside the 512^3 region, 8 ppc (2x2x2), rho ~ U(500, 1500),
     v ~ N(0, 0.1), F = I + N(0, 1e-3), B = 0, E = 1e5, nu = 0.3, dt = 1e-3.
@@ -296,7 +296,7 @@ def c5_stress(n_cells=128, seed=5000, dx=1.0 / 512, full_box=True):
     if full_box:
         grid = Grid(3, (0.0, 0.0, 0.0), dx, (513, 513, 513))
     else:
-        grid = grid_around(x, dx, 3, 3)
+        grid = grid_around(x, dx, pad, 3)
     return Scene(grid, p, [(1.0e5, 0.3)], 1e-3, (0.0, 0.0, 0.0),
                  meta={"config": "C5", "n_cells": n_cells})
 
@@ -321,13 +321,13 @@ def c5_coarse_field(grid_fine: Grid, n_cells=128, seed=5001, dx_coarse=1.0 / 128
     return grid, v.reshape(nn, nn, nn, 3)
 
 
-def c5_bench_workload(cells=128, full_box=True):
+def c5_bench_workload(cells=128, full_box=True, pad=3):
     """The timed C5 workload of bench.py: the fine cube of c5_stress, a passive coarse
     subdomain of one particle per coarse cell carrying the smooth field of c5_coarse_field (its P2G
     gives v_B^n; bench.py sets v_B^{n+1} = 1.01 v_B^n), and the fine receivers: the fine nodes of the
     cube's footprint outside the cube shrunk by 2 cells, as linear indices of the fine node box.
     Returns (fine Scene, coarse Scene, receivers int64[])."""
-    fine = c5_stress(n_cells=cells, full_box=full_box)
+    fine = c5_stress(n_cells=cells, full_box=full_box, pad=pad)
     cgrid, cvel = c5_coarse_field(fine.grid, n_cells=cells)
     side = cells * fine.grid.dx
     lo = 0.5 - side / 2

@@ -99,8 +99,10 @@ def test_bench_recipe_25_restored_steps(ctx):
 
 def test_bench_recipe_25_drifting_steps(ctx):
     """25 consecutive sub-steps WITHOUT restore (the state drifts, the receivers stay) on an 8^3-cell
-    cube, the oracle stepping alongside from its own state: displacement and v at 1e-9 every step."""
-    fine, coarse, recv = synth.c5_bench_workload(8, full_box=False)
+    cube, the oracle stepping alongside from its own state: displacement and v at 1e-9 every step.
+    The node box is padded by 14 cells: the receivers' coarse field (up to ~0.8 m/s) carries the
+    boundary layer ~0.4 cells per step."""
+    fine, coarse, recv = synth.c5_bench_workload(8, full_box=False, pad=14)
     sub, csub = gpu_setup(ctx, fine, coarse)
     pt = fine.particles.copy()
     for k in range(25):

@@ -19,6 +19,110 @@ def _translating_pair(dim, c, M=4):
     return coarse, fine
 
 
+# ---------------------------------------------------------------------------------------------
+# O11 Gamma selection (Eq. boundary_grid_set): pins of its own
+# ---------------------------------------------------------------------------------------------
+
+def _one_boundary_particle_scene(dim, x_p, m_p=2.0):
+    """A block of ordinary particles plus one marked boundary particle at x_p."""
+    sc = synth.random_fixture(dim=dim, cells=(4, 4, 3) if dim == 3 else (6, 5, 1), seed=71, dx=0.1)
+    pt = sc.particles
+    pt.boundary[:] = 0
+    pt.x[0] = x_p
+    pt.m[0] = m_p
+    pt.boundary[0] = 1
+    return sc
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_gamma_one_boundary_particle_touches_its_stencil_only(dim):
+    """One P^∂ particle sitting exactly on a grid node: its boundary mass lands on exactly its 3^d
+    stencil nodes with the knot weights (1/8, 3/4, 1/8) per axis (golden G1 at f = 1), so
+    m^∂ = m_p (3/4)^d at the node, m_p (3/4)^(d-1)/8 at face neighbours, ..., and sums to m_p."""
+    sc = _one_boundary_particle_scene(dim, None)
+    g = sc.grid
+    k = np.array([3, 3, 2][:dim])
+    sc.particles.x[0] = np.asarray(g.origin[:dim]) + g.dx * k
+    mb = oracle.boundary_mass(sc)
+    nz = np.flatnonzero(mb)
+    assert nz.size == 3 ** dim
+    knot = {-1: 1 / 8, 0: 3 / 4, 1: 1 / 8}
+    shp = oracle.node_shape(g)
+    for i in nz:
+        ki = np.array(np.unravel_index(i, shp))
+        off = ki - k
+        assert np.all(np.abs(off) <= 1)
+        assert mb[i] == pytest.approx(2.0 * np.prod([knot[int(o)] for o in off]), rel=1e-15)
+    assert mb.sum() == pytest.approx(2.0, rel=1e-15)
+    # Gamma (threshold 1e-6 x median mass): exactly those 3^d nodes
+    gs = oracle.p2g(sc)
+    gam, tau = S.gamma_set(sc, gs, 1e-6)
+    assert set(np.flatnonzero(gam)) == set(nz)
+
+
+def test_gamma_counts_only_marked_particles():
+    """m^∂ equals the P2G mass (pinned by golden G2 and conservation) of the marked subset alone: an
+    oracle that treated every particle as a boundary particle fails this."""
+    sc = synth.random_fixture(dim=2, cells=(8, 6, 1), seed=72, dx=0.1)
+    rng = np.random.default_rng(3)
+    sc.particles.boundary[:] = (rng.random(sc.particles.n) < 0.3).astype(np.uint8)
+    mb = oracle.boundary_mass(sc)
+    sub = synth.Scene(sc.grid, sc.particles.subset(sc.particles.boundary.astype(bool)), sc.materials, sc.dt)
+    np.testing.assert_allclose(mb, oracle.p2g(sub).m, rtol=1e-14, atol=0)
+    assert mb.sum() < 0.5 * oracle.p2g(sc).m.sum()
+
+
+def test_gamma_threshold_is_relative_to_the_median_mass():
+    """tau_Gamma = tau_rel x median particle mass (R11): a boundary particle whose stencil
+    weight at a corner node is w gives that node m_p w; the node is in Gamma iff m_p w > tau."""
+    sc = _one_boundary_particle_scene(2, None, m_p=1.0)
+    g = sc.grid
+    k = np.array([3, 3])
+    sc.particles.x[0] = np.asarray(g.origin[:2]) + g.dx * k
+    gs = oracle.p2g(sc)
+    med = oracle.median(sc.particles.m)
+    corner = 1 / 64  # (1/8)^2
+    for tau_rel, expect in ((0.999 * corner / med, 9), (1.001 * corner / med, 5)):
+        gam, tau = S.gamma_set(sc, gs, tau_rel)
+        assert tau == pytest.approx(tau_rel * med)
+        assert int(gam.sum()) == expect  # corners drop out first (faces carry 3/32)
+
+
+def test_receivers_hand_case_1d_overlap():
+    """A hand-computed pair: coarse dx = 0.2, fine dx = 0.1, both marked at their artificial cuts.
+    The fine nodes at x = 0.4 and the coarse node at x = 0.4 coincide; whichever carries the larger
+    raw nodal mass donates (tie -> B), the other side receives, never both."""
+    # fine block x in [0, 0.6], coarse block x in [0.3, 1.2] (2D strips, one row of cells)
+    fine = synth.random_fixture(dim=2, cells=(6, 2, 1), seed=73, dx=0.1, F_sigma=0.0, B_scale=0.0)
+    coarse = synth.random_fixture(dim=2, cells=(5, 1, 1), seed=74, dx=0.2, F_sigma=0.0, B_scale=0.0)
+    coarse.particles.x[:, 0] += 0.2
+    for sc, cut, side in ((fine, 0.6, -1), (coarse, 0.2 + 0.0, +1)):
+        x = sc.particles.x[:, 0]
+        sc.particles.boundary[:] = (np.abs(x - (x.max() if side < 0 else x.min())) < sc.grid.dx).astype(np.uint8)
+    lo = np.minimum(fine.particles.x.min(0), coarse.particles.x.min(0)) - 0.6
+    for sc in (fine, coarse):
+        sc.grid = synth.grid_around(np.vstack([fine.particles.x, coarse.particles.x]), sc.grid.dx, 4, 2,
+                                    align_origin=(0.0, 0.0))
+    gsB, gsS = oracle.p2g(coarse), oracle.p2g(fine)
+    hatB, hatS = S.receivers(coarse, fine, gsB, gsS, 1e-6)
+    gB, _ = S.gamma_set(coarse, gsB, 1e-6)
+    gS, _ = S.gamma_set(fine, gsS, 1e-6)
+    assert hatB.sum() > 0 and hatS.sum() > 0
+    xs, _ = S.node_positions(fine.grid)
+    cidx = S.coincident_coarse_index(coarse.grid, xs, 1e-9)
+    amb = np.flatnonzero(gS & (cidx >= 0) & gB[np.maximum(cidx, 0)])
+    assert amb.size > 0
+    for j in amb:
+        I = cidx[j]
+        assert not (hatB[I] and hatS[j])
+        if gsB.m[I] >= gsS.m[j]:
+            assert not hatB[I]
+        else:
+            assert not hatS[j]
+    # receivers are a subset of Gamma on each side
+    assert np.all(gB[hatB]) and np.all(gS[hatS])
+
+
 def test_receivers_disjoint_and_tie_to_B():
     coarse, fine = synth.c1_cantilever()
     gsB = oracle.p2g(coarse)

@@ -221,5 +221,11 @@ def test_interp_time_reproduces_linear(dim):
     o0 = oracle.interp(gB, w0, w1, 0.0, gS, targets)
     o1 = oracle.interp(gB, w0, w1, 1.0, gS, targets)
     oh = oracle.interp(gB, w0, w1, 0.3, gS, targets)
-    np.testing.assert_array_equal(o0, oracle.interp(gB, w0, w0, 0.7, gS, targets) * 0 + o0)
+    # endpoints (PAPER.md:352 with alpha = 0 / 1): T_0 = I(v^n) and T_1 = I(v^{n+1}) whatever the other
+    # field is -- compared with the single-field interpolation (both endpoints set to the same field)
+    np.testing.assert_array_equal(o0, oracle.interp(gB, w0, 100.0 * w1 + 7.0, 0.0, gS, targets))
+    np.testing.assert_allclose(o0, oracle.interp(gB, w0, w0, 0.5, gS, targets), rtol=0, atol=1e-14)
+    np.testing.assert_array_equal(o1, oracle.interp(gB, -3.0 * w0, w1, 1.0, gS, targets))
+    np.testing.assert_allclose(o1, oracle.interp(gB, w1, w1, 0.5, gS, targets), rtol=0, atol=1e-14)
+    assert np.abs(o0 - o1).max() > 0.1  # the two endpoints differ, so the checks above see alpha
     np.testing.assert_allclose(oh, 0.7 * o0 + 0.3 * o1, rtol=0, atol=1e-14)
