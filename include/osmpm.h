@@ -308,6 +308,14 @@ osmpm_status osmpm_schwarz_substep(osmpm_coupler* cpl, int32_t m, osmpm_solve_st
 /* Whole frame t_n -> t_n+1 (Alg. 1). */
 osmpm_status osmpm_schwarz_step(osmpm_coupler* cpl, osmpm_schwarz_report* report);
 
+/* a1 building block, exposed for testing: stable LSD radix sort (8 bits per pass) of n (key, value)
+ * pairs on the low nbits bits of the keys, in place; equal keys keep their input order.  This is the
+ * sort osmpm_p2g runs on the particles' tile-major cell keys every step (north_star: "block-level
+ * radix sort").  keys, vals: n entries each, host or device memory per `space`.  Synchronising.
+ * Errors: INVALID_ARG (n outside [0, 2^31), nbits outside [0, 32], NULL arrays), OOM. */
+osmpm_status osmpm_sort_pairs(osmpm_ctx* ctx, uint32_t* keys, int32_t* vals, int64_t n, int32_t nbits,
+                              osmpm_memspace space);
+
 /* a11 (PAPER.md:376-379 Eq. store_states, 455 Alg. 1 "reset"): osmpm_checkpoint stores the whole
  * particle state {x, v, F, B, m, V0, material, P^∂ flag, id} -- per slab, with its particle count,
  * for a decomposed subdomain -- in library-owned device memory (one copy per subdomain; a second

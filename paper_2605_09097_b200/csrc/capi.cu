@@ -340,6 +340,33 @@ osmpm_status osmpm_subdomain_info(osmpm_subdomain* sub, int64_t* n_particles, in
     SUB_CALL(sub, info(n_particles, box_lo, box_dims));
 }
 osmpm_status osmpm_sync(osmpm_subdomain* sub) { SUB_CALL(sub, sync()); }
+osmpm_status osmpm_sort_pairs(osmpm_ctx* ctx, uint32_t* keys, int32_t* vals, int64_t n, int32_t nbits,
+                              osmpm_memspace space)
+{
+    CHECK_ARG(ctx, "ctx is NULL");
+    CHECK_ARG(n >= 0 && n < (int64_t(1) << 31), "n outside [0, 2^31)");
+    CHECK_ARG(nbits >= 0 && nbits <= 32, "nbits outside [0, 32]");
+    CHECK_ARG(n == 0 || (keys && vals), "NULL keys / vals");
+    SET_DEVICE(ctx);
+    if (n == 0 || nbits == 0) return OSMPM_OK;
+    DBuf<uint32_t> k[2], h;
+    DBuf<int> v[2];
+    for (int i = 0; i < 2; ++i) {
+        OSMPM_TRY(k[i].need(n));
+        OSMPM_TRY(v[i].need(n));
+    }
+    OSMPM_TRY(h.need(radix_hist_words(n)));
+    const cudaMemcpyKind in = space == OSMPM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    const cudaMemcpyKind out = space == OSMPM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    OSMPM_CU(cudaMemcpyAsync(k[0].p, keys, n * 4, in, ctx->stream));
+    OSMPM_CU(cudaMemcpyAsync(v[0].p, vals, n * 4, in, ctx->stream));
+    const int r = radix_sort_pairs(k[0].p, v[0].p, k[1].p, v[1].p, n, nbits, h.p, ctx->stream, ctx->launches) ? 1 : 0;
+    OSMPM_LAUNCH_CHECK();
+    OSMPM_CU(cudaMemcpyAsync(keys, k[r].p, n * 4, out, ctx->stream));
+    OSMPM_CU(cudaMemcpyAsync(vals, v[r].p, n * 4, out, ctx->stream));
+    OSMPM_CU(cudaStreamSynchronize(ctx->stream));
+    return OSMPM_OK;
+}
 osmpm_status osmpm_checkpoint(osmpm_subdomain* sub) { SUB_CALL(sub, checkpoint()); }
 osmpm_status osmpm_restore(osmpm_subdomain* sub) { SUB_CALL(sub, restore()); }
 

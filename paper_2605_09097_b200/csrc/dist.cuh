@@ -415,12 +415,16 @@ struct Dist : public osmpm_subdomain {
             nl[i] = (int64_t)h_cnt[1];
             nr[i] = (int64_t)h_cnt[2];
             if (nl[i] + nr[i] > 0) {
-                size_t bytes = 0;
-                cub::DeviceRadixSort::SortPairs(nullptr, bytes, s->keys.p, s->keys2.p, s->vals.p, s->vals2.p, (int)s->n,
-                                                0, 2, st());
-                OSMPM_TRY(s->cub_tmp.need(bytes));
-                OSMPM_CU(cub::DeviceRadixSort::SortPairs(s->cub_tmp.p, bytes, s->keys.p, s->keys2.p, s->vals.p,
-                                                         s->vals2.p, (int)s->n, 0, 2, st()));
+                OSMPM_TRY(s->rs_hist.need(radix_hist_words(s->n)));
+                // 2-bit keys stay / left / right: one stable radix pass (radix_sort.cuh)
+                if (!radix_sort_pairs(s->keys.p, s->vals.p, s->keys2.p, s->vals2.p, s->n, 2, s->rs_hist.p, st(),
+                                      ctx->launches)) {
+                    std::swap(s->keys.p, s->keys2.p);
+                    std::swap(s->keys.cap, s->keys2.cap);
+                    std::swap(s->vals.p, s->vals2.p);
+                    std::swap(s->vals.cap, s->vals2.cap);
+                }
+                OSMPM_LAUNCH_CHECK();
                 KC();
                 k_permute<R><<<nblk_all(s->n, 256), 256, 0, st()>>>(s->P.p, s->P2.p, L::NF, s->cap, s->n, s->vals2.p,
                                                                     s->mat.p, s->mat2.p, s->bnd.p, s->bnd2.p, s->pid.p,

@@ -1,7 +1,6 @@
 // subdomain.cuh -- one MPM subdomain on one GPU (§3.1: its own grid dx, time step dt and
 // particle set), templated on dimension D and particle precision R.
 #pragma once
-#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <type_traits>
@@ -11,6 +10,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "radix_sort.cuh"
 #include "runtime.h"
 
 namespace osmpm {
@@ -131,7 +131,7 @@ struct Sub : public osmpm_subdomain {
     bool have_ck = false;
     DBuf<uint32_t> keys, keys2;
     DBuf<int> vals, vals2;
-    DBuf<unsigned char> cub_tmp;
+    DBuf<uint32_t> rs_hist;  // digit histograms of the radix sort (radix_sort.cuh)
 
     // ---- node box ---------------------------------------------------------------------------
     BoxDev box{};
@@ -456,11 +456,15 @@ struct Sub : public osmpm_subdomain {
         OSMPM_LAUNCH_CHECK();
         int nbits = 1;
         while ((int64_t(1) << nbits) < box.ncells) ++nbits;
-        size_t bytes = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, keys2.p, vals.p, vals2.p, (int)n, 0, nbits, st());
-        OSMPM_TRY(cub_tmp.need(bytes));
-        OSMPM_CU(cub::DeviceRadixSort::SortPairs(cub_tmp.p, bytes, keys.p, keys2.p, vals.p, vals2.p, (int)n, 0,
-                                                 nbits, st()));
+        OSMPM_TRY(rs_hist.need(radix_hist_words(n)));
+        // stable LSD radix sort of the cell keys (radix_sort.cuh); the sorted pairs end in keys2/vals2
+        if (!radix_sort_pairs(keys.p, vals.p, keys2.p, vals2.p, n, nbits, rs_hist.p, st(), ctx->launches)) {
+            std::swap(keys.p, keys2.p);
+            std::swap(keys.cap, keys2.cap);
+            std::swap(vals.p, vals2.p);
+            std::swap(vals.cap, vals2.cap);
+        }
+        OSMPM_LAUNCH_CHECK();
         KC(); k_permute<R><<<nblk_all(n, 256), 256, 0, st()>>>(P.p, P2.p, L::NF, cap, n, vals2.p, mat.p, mat2.p, bnd.p,
                                                          bnd2.p, pid.p, pid2.p);
         OSMPM_LAUNCH_CHECK();

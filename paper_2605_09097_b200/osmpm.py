@@ -99,6 +99,17 @@ def comm_unique_id() -> bytes:
     return bytes(buf)
 
 
+def sort_pairs(ctx, keys, vals, nbits):
+    """Stable radix sort of (uint32 key, int32 value) pairs on the low nbits bits, in place (numpy or
+    torch CUDA arrays)."""
+    if _is_torch(keys):
+        kp, vp, sp = C.c_void_p(keys.data_ptr()), C.c_void_p(vals.data_ptr()), DEVICE
+    else:
+        assert keys.dtype == np.uint32 and vals.dtype == np.int32 and keys.flags.c_contiguous and vals.flags.c_contiguous
+        kp, vp, sp = keys.ctypes.data_as(C.c_void_p), vals.ctypes.data_as(C.c_void_p), HOST
+    _check(lib().osmpm_sort_pairs(ctx._h, kp, vp, C.c_int64(int(keys.shape[0])), C.c_int32(nbits), C.c_int(sp)))
+
+
 def newton_settings(max_newton=50, max_cg=1000, fixed_iters=0, guess=0, newton_rtol=1e-8, newton_atol=0.0,
                     cg_rtol=1e-8, ls_min_alpha=2.0 ** -20, energy_noise_rtol=1e-13) -> NewtonSettings:
     return NewtonSettings(max_newton, max_cg, fixed_iters, guess, newton_rtol, newton_atol, cg_rtol, ls_min_alpha,

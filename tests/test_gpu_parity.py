@@ -149,7 +149,10 @@ def test_negative_curvature_parity(ctx, fixed):
     sub = make_sub(ctx, sc)
     sub.p2g()
     st = sub.implicit_solve(osmpm.newton_settings(**kw), raise_on_error=False)
-    assert st.negcurv == st_ref.negcurv >= 1 and st.cg_iters == st_ref.cg_iters and st.status == st_ref.status
+    assert st.negcurv == st_ref.negcurv >= 1 and st.cg_iters == st_ref.cg_iters
+    # same outcome (the two status enums number differently: GPU 4 / oracle 3 = Newton not converged)
+    ORC2GPU = {0: 0, 3: 4, 4: 5}
+    assert st.status == ORC2GPU[st_ref.status]
     if st.status == 0:
         act = ref.active.astype(bool)
         assert rel_linf(sub.read_grid_velocity(), np.where(act[:, None], u_ref / sc.dt, 0.0)) <= 1e-9
@@ -333,3 +336,22 @@ def test_deterministic_mode_is_bitwise_reproducible(ctx, monkeypatch):
         sub.implicit_solve(osmpm.newton_settings(max_newton=3, max_cg=20, fixed_iters=1))
         vs.append(sub.read_grid_velocity())
     assert np.array_equal(vs[0], vs[1])
+
+
+@pytest.mark.parametrize("n,nbits", [(0, 8), (1, 3), (4095, 8), (4097, 13), (100003, 22), (1 << 20, 22),
+                                     (300000, 2), (70000, 32)])
+def test_radix_sort_is_a_stable_sort(ctx, n, nbits):
+    """a1: the hand-written radix sort equals numpy's stable argsort bit for bit (keys and the order of
+    equal keys), on the low nbits bits, for empty / single / ragged / multi-tile sizes."""
+    from paper_2605_09097_b200 import osmpm
+    rng = np.random.default_rng(n + nbits)
+    hi = min(1 << nbits, 1 << 32) if nbits < 32 else 1 << 32
+    keys = rng.integers(0, hi, size=n, dtype=np.uint64).astype(np.uint32)
+    if n > 10:
+        keys[: n // 3] = keys[n // 3]  # many equal keys: stability matters
+    vals = np.arange(n, dtype=np.int32)
+    k, v = keys.copy(), vals.copy()
+    osmpm.sort_pairs(ctx, k, v, nbits)
+    masked = keys & np.uint32((1 << nbits) - 1 if nbits < 32 else 0xFFFFFFFF)
+    order = np.argsort(masked, kind="stable")
+    assert np.array_equal(v, vals[order]) and np.array_equal(k, keys[order])
