@@ -25,37 +25,12 @@
 
 namespace osmpm {
 
-// OSMPM_SW_RECOMPUTE: the per-particle record holds only the fractional position f and G (rows padded
-// to 16 B); phase 2 recomputes the B-spline weights from f (fp64 issue traded for shared-memory
-// bandwidth, the binding resource of the stored-weights layout)
-#ifndef OSMPM_SW_RECOMPUTE
-#define OSMPM_SW_RECOMPUTE 0
-#endif
-
 template <int D, typename R> struct SWRec {
     // G row a starts at GROW(a): 3D fp64 rows padded to 4 reals (16-B aligned: one 16-B + one 8-B load
     // per row; the 30-real record has exactly the room), otherwise packed
     static constexpr int GP = (D == 3 && sizeof(R) == 8) ? 4 : D;
-    static constexpr bool RECOMPUTE = OSMPM_SW_RECOMPUTE != 0;
-    static constexpr int F0 = 0;
-    static constexpr int G0 = (D == 3) ? 4 : 2, GS = (D == 3) ? 4 : 2;  // G row a at G0 + GS a
-    static constexpr int RS = !RECOMPUTE ? HvpRec<D, R>::RS
-                                         : (sizeof(R) == 8 ? ((D == 3) ? 18 : 6) : ((D == 3) ? 20 : 12));
+    static constexpr int RS = HvpRec<D, R>::RS;
 };
-
-// OSMPM_SW_L2PF: stream the next layer's particle inputs into L2 (cp.async.bulk.prefetch.L2) instead
-// of shared memory, and read them with global loads (no staging buffer, no mbarrier)
-#ifndef OSMPM_SW_L2PF
-#define OSMPM_SW_L2PF 0
-#endif
-
-#ifndef OSMPM_SW_SPLIT
-#define OSMPM_SW_SPLIT 1
-#endif
-
-#ifndef OSMPM_SW_UNROLL
-#define OSMPM_SW_UNROLL 4
-#endif
 
 template <int D> struct SW {
     using T = Tile<D>;
@@ -72,11 +47,11 @@ template <int D> struct SW {
 // cells of a warp's lanes start 4 banks apart: conflict-free 8-B loads), 3D fp32 4 (16-B nodes), 2D 2
 template <int D, typename R> struct SVS {
     static constexpr int S = (D == 3) ? (sizeof(R) == 8 ? 3 : 4) : 2;
-    // 3D fp64 split layout (OSMPM_SW_SPLIT): components 0,1 as 16-B pairs [NNP][2], component 2 as a
+    // 3D fp64 split layout: components 0,1 as 16-B pairs [NNP][2], component 2 as a
     // separate [NNP] plane -- one 16-B and one 8-B load per node instead of three 8-B loads, same
     // footprint; rows of 10 nodes put the four cells of a warp at bank offsets 0/8/16/24 (pairs) and
     // 0/20/8/28 (plane): conflict-free
-    static constexpr bool SPLIT = OSMPM_SW_SPLIT && D == 3 && sizeof(R) == 8;
+    static constexpr bool SPLIT = D == 3 && sizeof(R) == 8;
 };
 // shared-memory element of (node, component) in the node tile
 template <int D, typename R>
@@ -199,7 +174,7 @@ constexpr size_t hvp_sw_smem_bytes()
 {
     using T = Tile<D>;
     return 16 + 128 /* alignment of the streamed-input block */ + ((size_t)SW<D>::NNP * SVS<D, R>::S + SW<D>::STG +
-                 (OSMPM_SW_L2PF ? (size_t)0 : (size_t)SWIn<D, R>::TOT) +
+                 (size_t)SWIn<D, R>::TOT +
                  (size_t)SWRec<D, R>::RS * T::NT) *
                     sizeof(R);
 }
@@ -267,9 +242,6 @@ __device__ __forceinline__ void sw_gather(const R* sv, const int* lc, const R (*
 
 // item (cell, a, i): emit the completed kk = 0 plane into the staging slots, shift the window
 template <int V> struct ICst { static constexpr int value = V; };
-#ifndef OSMPM_SW_P1SPLIT
-#define OSMPM_SW_P1SPLIT 1
-#endif
 
 template <int D, typename R>
 __device__ __forceinline__ void sw_emit(int cellL, int a, int i, R* acc, R* stg)
@@ -389,13 +361,6 @@ __device__ __forceinline__ void sw_prefetch(const R* __restrict__ P, const R* __
     const int lb0 = lb & ~(In::UE - 1);                       // 16-B aligned start
     const int cnt = min(le, lb + Tile<D>::NT) - lb0;
     const uint32_t bytes = (uint32_t)((cnt + In::UE - 1) & ~(In::UE - 1)) * sizeof(R);
-    if constexpr (OSMPM_SW_L2PF) {
-        if (lane < In::NF) {
-            const R* src = (lane < D) ? P + (int64_t)(PL<D>::X + lane) * cap + lb0 : cache + (int64_t)(lane - D) * cap + lb0;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-        }
-        return;
-    }
     fence_async_smem();
     if (lane == 0) mbar_expect_tx(bar, bytes * In::NF);
     __syncwarp();
@@ -408,10 +373,8 @@ __device__ __forceinline__ void sw_prefetch(const R* __restrict__ P, const R* __
 // Two 2-D TMA tensor copies per layer instead of one bulk copy per field: the streamed inputs are the
 // field-major SoA arrays seen as 2-D tensors [fields][particles] (x: 3 fields of the particle SoA,
 // the Newton cache: 17 fields), and one box of {PFS particles, fields} lands exactly in the pf
-// layout (field f at pf + f * PFS).  OSMPM_SW_TMAP=0 selects the per-field bulk copies.
-#ifndef OSMPM_SW_TMAP
-#define OSMPM_SW_TMAP 1
-#endif
+// layout (field f at pf + f * PFS).  When the host cannot encode the tensor maps (use_tmap = 0) the
+// per-field bulk copies of sw_prefetch are used instead.
 __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar)
 {
     asm volatile(
@@ -436,16 +399,10 @@ __device__ __forceinline__ void sw_prefetch_tmap(const CUtensorMap* mx, const CU
     }
 }
 
-#ifndef OSMPM_SW_MINB
-#define OSMPM_SW_MINB 3
-#endif
-// fp32 variant: half the shared memory (records, streamed inputs, node tile and staging in fp32) and
-// fewer live registers, so more CTAs fit per SM
-#ifndef OSMPM_SW_MINB_F32
-#define OSMPM_SW_MINB_F32 4
-#endif
+// 3 CTAs per SM in fp64 (128 registers; shared memory 75 KB); the fp32 variant has half the shared
+// memory (records, streamed inputs, node tile and staging in fp32) and fewer live registers: 4
 template <int D, typename R>
-__global__ void __launch_bounds__(Tile<D>::NT, sizeof(R) == 8 ? OSMPM_SW_MINB : OSMPM_SW_MINB_F32)
+__global__ void __launch_bounds__(Tile<D>::NT, sizeof(R) == 8 ? 3 : 4)
 k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, const int* __restrict__ cell_start,
          BoxDev b, const double* __restrict__ din, double* __restrict__ yout, const __grid_constant__ CUtensorMap tmx,
          const __grid_constant__ CUtensorMap tmc, int use_tmap, double* __restrict__ tbuf)
@@ -467,8 +424,8 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
         const uint32_t off = 16 + (uint32_t)((S::NNP * SVS<D, R>::S + S::STG) * sizeof(R));
         pf = reinterpret_cast<R*>(smem_raw + (((base + off + 127u) & ~127u) - base));
     }
-    const bool tmap = OSMPM_SW_TMAP && !OSMPM_SW_L2PF && use_tmap;  // L2PF has no shared-memory input block
-    R* rec = pf + (OSMPM_SW_L2PF ? 0 : SWIn<D, R>::TOT);
+    const bool tmap = use_tmap != 0;
+    R* rec = pf + SWIn<D, R>::TOT;
     const int tile = blockIdx.x;
     const int64_t kt = (int64_t)tile * T::NC;
     __shared__ int scs[T::NC + 1];  // the tile's cell ranges
@@ -527,7 +484,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
             for (int sb = lb; sb < le; sb += T::NT) {
                 const int se = min(sb + T::NT, le);
                 const int q = threadIdx.x, p = sb + q;
-                const bool from_pf = !OSMPM_SW_L2PF && (sb == lb);
+                const bool from_pf = sb == lb;
                 if (sb != lb) __syncthreads();  // previous chunk's records consumed
                 if (from_pf) mbar_wait(bar, parity);
                 // phase 1, instantiated for the two sources of the streamed fields (the shared-memory copy
@@ -555,16 +512,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                     int lc[3] = {0, 0, 0};
                     weights_at<D, R>(x, b, t, lc, w, dw);
                     const RecPtr<R> r(rec, q, RS);
-                    if constexpr (SR::RECOMPUTE) {
-#pragma unroll
-                        for (int a = 0; a < D; ++a) {
-                            R fa;
-                            base_of<R>(x[a], b.o[a], b.inv_dx, &fa);
-                            *r.at(SR::F0 + a) = fa;
-                        }
-                    } else {
-                        store_weights<D, R>(r, w, dw);
-                    }
+                    store_weights<D, R>(r, w, dw);
                     R gd[D * D];
                     sw_gather<D, R>(sv, lc, w, dw, gd);
                     R Sv[Sym<D>::N], A[D * D];
@@ -599,10 +547,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                             }
                             Ga[bb] = fma(cc, s2, fma(ltr, A[a * D + bb], s1));
                         }
-                        if constexpr (SR::RECOMPUTE) {
-#pragma unroll
-                            for (int bb = 0; bb < D; ++bb) *r.at(SR::G0 + SR::GS * a + bb) = Ga[bb];
-                        } else if constexpr (SR::GP == 4) {
+                        if constexpr (SR::GP == 4) {
                             using V2 = typename Vec2<R>::type;
                             V2 g01;
                             g01.x = Ga[0];
@@ -616,9 +561,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                     }
                 };
                 if (p < se) {
-                    if (!OSMPM_SW_P1SPLIT)
-                        phase1(ICst<2>{});
-                    else if (from_pf)
+                    if (from_pf)
                         phase1(ICst<1>{});
                     else
                         phase1(ICst<0>{});
@@ -636,46 +579,18 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                 }
                 if (it < T::ITEMS) {
                     const int p0 = max(ks, sb), p1 = min(ke, se);
-#ifdef OSMPM_SW_NOROT
-                    const int len = p1 - p0, rot = 0;
-#else
                     // (icell & 7) % len without the integer division when len >= 8 (the usual case)
                     const int len = p1 - p0, r7 = icell & 7;
                     const int rot = r7 < len ? r7 : (len > 0 ? r7 % len : 0);
-#endif
-                    constexpr int kUnroll = OSMPM_SW_UNROLL;  // 4 (measured: 2 / 8 slower)
+                    constexpr int kUnroll = 4;  // (measured: 2 / 8 slower)
 #pragma unroll kUnroll
                     for (int k = 0; k < len; ++k) {
                         const RecPtr<R> r(rec, rotated(p0, len, k, rot) - sb, RS);
                         ItemW<D, R> W;
                         R s[D];
-                        if constexpr (SR::RECOMPUTE) {
-                            // quadratic B-spline from f (bspline(): w = 0.5 t^2 | 0.75 - t^2 | 0.5 t^2,
-                            // dw = t | -2t | t times 1/dx with t = f - 3/2, f - 1, f - 1/2)
-                            const R inv = (R)b.inv_dx;
-                            const R tx = *r.at(SR::F0) - (R(1.5) - R(0.5) * ii);
-                            W.wx = (ii == 1) ? fma(-tx, tx, R(0.75)) : R(0.5) * tx * tx;
-                            W.dwx = (ii == 1) ? R(-2) * tx * inv : tx * inv;
+                        W.load(r, ii);
 #pragma unroll
-                            for (int ax = 1; ax < D; ++ax) {
-                                const R f = *r.at(SR::F0 + ax);
-                                const R t0 = f - R(1.5), t1 = f - R(1), t2 = f - R(0.5);
-                                R* wv = (ax == 1) ? W.wy : W.wz;
-                                R* dv = (ax == 1) ? W.dwy : W.dwz;
-                                wv[0] = R(0.5) * t0 * t0;
-                                wv[1] = fma(-t1, t1, R(0.75));
-                                wv[2] = R(0.5) * t2 * t2;
-                                dv[0] = t0 * inv;
-                                dv[1] = R(-2) * t1 * inv;
-                                dv[2] = t2 * inv;
-                            }
-#pragma unroll
-                            for (int bb = 0; bb < D; ++bb) s[bb] = *r.at(SR::G0 + SR::GS * icomp + bb);
-                        } else {
-                            W.load(r, ii);
-#pragma unroll
-                            for (int bb = 0; bb < D; ++bb) s[bb] = *r.at(Rec<D>::G + icomp * SR::GP + bb);
-                        }
+                        for (int bb = 0; bb < D; ++bb) s[bb] = *r.at(Rec<D>::G + icomp * SR::GP + bb);
                         item_linear<D, R>(s, W, acc);
                     }
                 }

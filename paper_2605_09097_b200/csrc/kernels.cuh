@@ -106,85 +106,6 @@ __global__ void k_cell_start(const uint32_t* __restrict__ keys, int64_t n, int64
     for (int64_t k = lo; k <= hi; ++k) cell_start[k] = (int)i;
 }
 
-// =============================================================================================
-// a2: APIC P2G of mass, momentum, stress; per-particle scatter (v1)
-// =============================================================================================
-template <int D, typename R>
-__global__ void k_p2g(const R* __restrict__ P, int64_t cap, int64_t n, const int* __restrict__ mat, BoxDev b,
-                      MatTable mt, double* __restrict__ m, double* __restrict__ mom, double* __restrict__ fsig)
-{
-    using L = PL<D>;
-    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    R w[3][3], dw[3][3], f[3];
-    int c[3] = {0, 0, 0};
-    R inv_dx = (R)b.inv_dx, dx = (R)b.dx;
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-        c[a] = base_of<R>(P[(L::X + a) * cap + p], b.o[a], b.inv_dx, &f[a]) - b.lo[a];
-        bspline<R>(f[a], inv_dx, w[a], dw[a]);
-    }
-    R F[D * D], B[D * D], v[D];
-#pragma unroll
-    for (int k = 0; k < D * D; ++k) {
-        F[k] = P[(L::F + k) * cap + p];
-        B[k] = P[(L::B + k) * cap + p];
-    }
-#pragma unroll
-    for (int a = 0; a < D; ++a) v[a] = P[(L::V + a) * cap + p];
-    const R mp = P[L::M * cap + p], V0 = P[L::VOL * cap + p];
-    const int mid = mat[p];
-    const R mu = (R)mt.mu[mid], lam = (R)mt.lam[mid];
-    // Kirchhoff stress tau = P F^T = mu F F^T + (lam ln J - mu) I
-    R tau[D * D];
-    const R lnJ = log(det<D, R>(F));
-#pragma unroll
-    for (int a = 0; a < D; ++a)
-#pragma unroll
-        for (int bb = 0; bb < D; ++bb) {
-            R s = 0;
-#pragma unroll
-            for (int k = 0; k < D; ++k) s += F[a * D + k] * F[bb * D + k];
-            tau[a * D + bb] = mu * s + (a == bb ? lam * lnJ - mu : R(0));
-        }
-    const R Dinv = R(4) * inv_dx * inv_dx;  // D_p^{-1} = 4/dx^2 I
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-#pragma unroll
-            for (int k = 0; k < Tile<D>::K3; ++k) {
-                R N, gN[3], off[3];
-                off[0] = dx * (R(i) - f[0]);
-                off[1] = dx * (R(j) - f[1]);
-                if (D == 3) {
-                    off[2] = dx * (R(k) - f[2]);
-                    N = w[0][i] * w[1][j] * w[2][k];
-                    gN[0] = dw[0][i] * w[1][j] * w[2][k];
-                    gN[1] = w[0][i] * dw[1][j] * w[2][k];
-                    gN[2] = w[0][i] * w[1][j] * dw[2][k];
-                } else {
-                    N = w[0][i] * w[1][j];
-                    gN[0] = dw[0][i] * w[1][j];
-                    gN[1] = w[0][i] * dw[1][j];
-                }
-                int64_t node = box_node<D>(b, c[0] + i, c[1] + j, c[2] + k);
-                const R mN = mp * N;
-                atomicAdd(&m[node], (double)mN);
-#pragma unroll
-                for (int a = 0; a < D; ++a) {
-                    R aff = 0, t = 0;
-#pragma unroll
-                    for (int bb = 0; bb < D; ++bb) {
-                        aff += B[a * D + bb] * off[bb];
-                        t += tau[a * D + bb] * gN[bb];
-                    }
-                    atomicAdd(&mom[node * D + a], (double)(mN * (v[a] + Dinv * aff)));
-                    atomicAdd(&fsig[node * D + a], (double)(-V0 * t));
-                }
-            }
-}
-
 // node pass: active <=> m > thr (R4), v^n = (mv) / m
 template <int D>
 __global__ void k_p2g_nodes(int64_t nn, const double* __restrict__ m, const double* __restrict__ mom,
@@ -270,79 +191,6 @@ __global__ void k_grad_nodes(int64_t nn, int64_t nown, const double* __restrict_
         }
     }
     block_reduce_store<4>(red, partials);
-}
-
-// =============================================================================================
-// a7: energy only (line search): sum_p V0 Psi(F_p(u)), per particle, u gathered from global
-// partials per block: {sum V0 Psi, sum V0|Psi|, inverted}
-// =============================================================================================
-template <int D, typename R>
-__global__ void k_energy(const R* __restrict__ P, int64_t cap, int64_t n, const int* __restrict__ mat, BoxDev b,
-                         MatTable mt, const double* __restrict__ u, double* __restrict__ partials)
-{
-    using L = PL<D>;
-    double red[3] = {0.0, 0.0, 0.0};
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-        double w[3][3], dw[3][3], f;
-        int c[3] = {0, 0, 0};
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-            c[a] = base_of<double>((double)P[(L::X + a) * cap + p], b.o[a], b.inv_dx, &f) - b.lo[a];
-            bspline<double>(f, b.inv_dx, w[a], dw[a]);
-        }
-        double Mx[D * D];
-#pragma unroll
-        for (int k = 0; k < D * D; ++k) Mx[k] = 0.0;
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int j = 0; j < 3; ++j)
-#pragma unroll
-                for (int k = 0; k < Tile<D>::K3; ++k) {
-                    double gN[3];
-                    if (D == 3) {
-                        gN[0] = dw[0][i] * w[1][j] * w[2][k];
-                        gN[1] = w[0][i] * dw[1][j] * w[2][k];
-                        gN[2] = w[0][i] * w[1][j] * dw[2][k];
-                    } else {
-                        gN[0] = dw[0][i] * w[1][j];
-                        gN[1] = w[0][i] * dw[1][j];
-                    }
-                    const double* uu = u + box_node<D>(b, c[0] + i, c[1] + j, c[2] + k) * D;
-#pragma unroll
-                    for (int a = 0; a < D; ++a)
-#pragma unroll
-                        for (int bb = 0; bb < D; ++bb) Mx[a * D + bb] += uu[a] * gN[bb];
-                }
-#pragma unroll
-        for (int a = 0; a < D; ++a) Mx[a * D + a] += 1.0;
-        double Fn[D * D];
-#pragma unroll
-        for (int k = 0; k < D * D; ++k) Fn[k] = (double)P[(L::F + k) * cap + p];
-        const double V0 = (double)P[L::VOL * cap + p];
-        const int mid = mat[p];
-        const double mu = mt.mu[mid], lam = mt.lam[mid];
-        const double detM = det<D, double>(Mx), detFn = det<D, double>(Fn);
-        if (!(detM > 0.0 && detFn > 0.0)) {
-            red[2] += 1.0;
-            continue;
-        }
-        const double lnJ = log(detM) + log(detFn);
-        double tr = 0.0;
-#pragma unroll
-        for (int a = 0; a < D; ++a)
-#pragma unroll
-            for (int bb = 0; bb < D; ++bb) {
-                double s = 0.0;
-#pragma unroll
-                for (int k = 0; k < D; ++k) s += Mx[a * D + k] * Fn[k * D + bb];
-                tr += s * s;  // |M F^n|_F^2 = tr(M S M^T)
-            }
-        const double psiV = V0 * (0.5 * mu * (tr - D) - mu * lnJ + 0.5 * lam * lnJ * lnJ);
-        red[0] += psiV;
-        red[1] += fabs(psiV);
-    }
-    block_reduce_store<3>(red, partials);
 }
 
 // =============================================================================================

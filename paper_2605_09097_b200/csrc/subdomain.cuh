@@ -508,11 +508,8 @@ struct Sub : public osmpm_subdomain {
         OSMPM_CU(cudaMemsetAsync(mom.p, 0, nn * D * sizeof(double), st()));
         OSMPM_CU(cudaMemsetAsync(fsig.p, 0, nn * D * sizeof(double), st()));
         if (n > 0) {
-            // tiled P2G (p2g_tiled.cuh); OSMPM_P2G=atomic selects the per-particle scatter for A/B
-            static const bool atomic_p2g = getenv("OSMPM_P2G") && std::string(getenv("OSMPM_P2G")) == "atomic";
-            if (atomic_p2g) {
-                KC(); k_p2g<D, R><<<nblk_all(n, 128), 128, 0, st()>>>(P.p, cap, n, mat.p, box, mats, m.p, mom.p, fsig.p);
-            } else {
+            // tiled P2G (p2g_tiled.cuh)
+            {
                 static bool attr = false;
                 if (!attr) {
                     cudaFuncSetAttribute(k_p2g_tiled<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -642,8 +639,6 @@ struct Sub : public osmpm_subdomain {
     // buffers: particle part {E, |E|, inverted} (partA), node part {E, |E|, |g_free|^2, f_scale^2}
     // (partB, owned nodes only)
     // =========================================================================================
-    size_t grad_smem() const { return grad_smem_bytes<D>(); }
-    size_t hvp_smem() const { return hvp_smem_bytes<D, R>(); }
     int grad_blocks_nodes() const { return nblk(box.nnodes, 256); }
 
     osmpm_status grad_scatter(const double* uu, bool need_fmask, double* partA)
@@ -653,39 +648,26 @@ struct Sub : public osmpm_subdomain {
         OSMPM_CU(cudaMemsetAsync(g.p, 0, nn * D * sizeof(double), st()));
         OSMPM_CU(cudaMemsetAsync(dg.p, 0, nn * D * sizeof(double), st()));
         if (!need_fmask) OSMPM_CU(cudaMemsetAsync(fmask.p, 1, nn * D, st()));
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_grad<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grad_smem());
-            cudaFuncSetAttribute(k_hvp<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hvp_smem());
-            attr = true;
+        // sliding-window gradient (grad_sw.cuh)
+        static bool attr_sw = false;
+        if (!attr_sw) {
+            cudaFuncSetAttribute(k_grad_sw<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)grad_sw_smem_bytes<D, R>());
+            attr_sw = true;
         }
-        // sliding-window gradient (grad_sw.cuh); OSMPM_GRAD=tiled selects k_grad for A/B
-        static const bool tiled_grad = getenv("OSMPM_GRAD") && std::string(getenv("OSMPM_GRAD")) == "tiled";
-        if (tiled_grad) {
-            KC(); k_grad<D, R><<<box.ntiles, T::NT, grad_smem(), st()>>>(P.p, cache.p, cap, mat.p, cell_start.p, box,
-                                                                       mats, uu, g.p, dg.p, partA);
-        } else {
-            static bool attr_sw = false;
-            if (!attr_sw) {
-                cudaFuncSetAttribute(k_grad_sw<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)grad_sw_smem_bytes<D, R>());
-                attr_sw = true;
-            }
-            const bool det = det_mode();
-            if (det) {
-                OSMPM_TRY(det_a.need((size_t)box.ntiles * T::NN * D));
-                OSMPM_TRY(det_b.need((size_t)box.ntiles * T::NN * D));
-            }
-            KC(); k_grad_sw<D, R><<<box.ntiles, T::NT, grad_sw_smem_bytes<D, R>(), st()>>>(
-                P.p, cache.p, cap, mat.p, cell_start.p, box, mats, uu, g.p, dg.p, partA, det ? det_a.p : nullptr,
-                det ? det_b.p : nullptr);
-            OSMPM_LAUNCH_CHECK();
-            if (det) {
-                OSMPM_TRY(det_gather(det_a.p, g.p));
-                OSMPM_TRY(det_gather(det_b.p, dg.p));
-            }
+        const bool det = det_mode();
+        if (det) {
+            OSMPM_TRY(det_a.need((size_t)box.ntiles * T::NN * D));
+            OSMPM_TRY(det_b.need((size_t)box.ntiles * T::NN * D));
         }
+        KC(); k_grad_sw<D, R><<<box.ntiles, T::NT, grad_sw_smem_bytes<D, R>(), st()>>>(
+            P.p, cache.p, cap, mat.p, cell_start.p, box, mats, uu, g.p, dg.p, partA, det ? det_a.p : nullptr,
+            det ? det_b.p : nullptr);
         OSMPM_LAUNCH_CHECK();
+        if (det) {
+            OSMPM_TRY(det_gather(det_a.p, g.p));
+            OSMPM_TRY(det_gather(det_b.p, dg.p));
+        }
         return OSMPM_OK;
     }
     osmpm_status grad_nodes(const double* uu, double* partB)
@@ -708,61 +690,33 @@ struct Sub : public osmpm_subdomain {
         return OSMPM_OK;
     }
 
-    // HVP variant: sliding-window tiled kernel (default, hvp_sw.cuh); OSMPM_HVP=tiled | tiled_nopf
-    // select the earlier barrier-phased kernel of tiled.cuh, kept for A/B measurements
-    int hvp_variant() const
-    {
-        static int v = -1;
-        if (v < 0) {
-            const char* e = getenv("OSMPM_HVP");
-            const std::string s = e ? e : "";
-            v = (s == "tiled_nopf") ? 2 : (s == "tiled") ? 0 : 3;
-        }
-        return v;
-    }
-
+    // a5: the sliding-window tiled HVP (hvp_sw.cuh)
     osmpm_status launch_hvp(const double* din, double* yout)
     {
         auto& pf = ctx->prof;
         if (pf.on) pf.begin("hvp", st());
-        if (hvp_variant() == 2) {
-            static bool attr2 = false;
-            if (!attr2) {
-                cudaFuncSetAttribute(k_hvp<D, R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)hvp_smem_bytes<D, R, false>());
-                attr2 = true;
-            }
-            KC(); k_hvp<D, R, false><<<box.ntiles, T::NT, hvp_smem_bytes<D, R, false>(), st()>>>(
-                P.p, cache.p, cap, cell_start.p, box, din, yout);
-        } else if (hvp_variant() == 0) {
-            KC(); k_hvp<D, R><<<box.ntiles, T::NT, hvp_smem(), st()>>>(P.p, cache.p, cap, cell_start.p, box, din, yout);
-        } else {
-            static bool attr3 = false;
-            if (!attr3) {
-                cudaFuncSetAttribute(k_hvp_sw<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)hvp_sw_smem_bytes<D, R>());
-                attr3 = true;
-            }
-            // tensor maps of the streamed inputs, re-encoded when a buffer moves (the sort swaps P)
-            if (tm_P != P.p || tm_C != cache.p || tm_cap != cap) {
-                tm_ok = !(getenv("OSMPM_HVP_TMA") && std::string(getenv("OSMPM_HVP_TMA")) == "0") &&
-                        encode_fields_map<R>(&tm_x, P.p + (size_t)PL<D>::X * cap, D, cap, SWIn<D, R>::PFS) &&
-                        encode_fields_map<R>(&tm_c, cache.p, C::NF, cap, SWIn<D, R>::PFS);
-                tm_P = P.p;
-                tm_C = cache.p;
-                tm_cap = cap;
-                if (getenv("OSMPM_DEBUG_TMA"))
-                    fprintf(stderr, "[osmpm] hvp tensor maps: cap=%lld P=%p cache=%p ok=%d ntiles=%d\n", (long long)cap,
-                            (const void*)P.p, (const void*)cache.p, (int)tm_ok, (int)box.ntiles);
-            }
-            const bool det = det_mode();
-            if (det) OSMPM_TRY(det_a.need((size_t)box.ntiles * T::NN * D));
-            KC(); k_hvp_sw<D, R><<<box.ntiles, T::NT, hvp_sw_smem_bytes<D, R>(), st()>>>(
-                P.p, cache.p, cap, cell_start.p, box, din, yout, tm_x, tm_c, tm_ok ? 1 : 0, det ? det_a.p : nullptr);
-            if (det) {
-                OSMPM_LAUNCH_CHECK();
-                OSMPM_TRY(det_gather(det_a.p, yout));
-            }
+        static bool attr3 = false;
+        if (!attr3) {
+            cudaFuncSetAttribute(k_hvp_sw<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)hvp_sw_smem_bytes<D, R>());
+            attr3 = true;
+        }
+        // tensor maps of the streamed inputs, re-encoded when a buffer moves (the sort swaps P); if the
+        // driver's encoder is unavailable the kernel streams the fields with per-field bulk copies
+        if (tm_P != P.p || tm_C != cache.p || tm_cap != cap) {
+            tm_ok = encode_fields_map<R>(&tm_x, P.p + (size_t)PL<D>::X * cap, D, cap, SWIn<D, R>::PFS) &&
+                    encode_fields_map<R>(&tm_c, cache.p, C::NF, cap, SWIn<D, R>::PFS);
+            tm_P = P.p;
+            tm_C = cache.p;
+            tm_cap = cap;
+        }
+        const bool det = det_mode();
+        if (det) OSMPM_TRY(det_a.need((size_t)box.ntiles * T::NN * D));
+        KC(); k_hvp_sw<D, R><<<box.ntiles, T::NT, hvp_sw_smem_bytes<D, R>(), st()>>>(
+            P.p, cache.p, cap, cell_start.p, box, din, yout, tm_x, tm_c, tm_ok ? 1 : 0, det ? det_a.p : nullptr);
+        if (det) {
+            OSMPM_LAUNCH_CHECK();
+            OSMPM_TRY(det_gather(det_a.p, yout));
         }
         OSMPM_LAUNCH_CHECK();
         if (pf.on) pf.end("hvp", st());
@@ -832,21 +786,12 @@ struct Sub : public osmpm_subdomain {
 
     // line-search energy at uu: block partials particle {E, |E|, inverted} (partA), node {E, |E|}
     // (partB, owned nodes only)
-    // tiled (k_energy_tiled, one CTA per tile) unless OSMPM_ENERGY=particle (k_energy, for A/B)
-    static bool particle_energy()
-    {
-        static const bool v = getenv("OSMPM_ENERGY") && std::string(getenv("OSMPM_ENERGY")) == "particle";
-        return v;
-    }
-    int energy_blocks_particles() const { return particle_energy() ? nblk(n, 256) : box.ntiles; }
+    // tiled (k_energy_tiled, one CTA per tile)
+    int energy_blocks_particles() const { return box.ntiles; }
     osmpm_status energy_launch(const double* uu, double* partA, double* partB)
     {
-        if (particle_energy()) {
-            KC(); k_energy<D, R><<<energy_blocks_particles(), 256, 0, st()>>>(P.p, cap, n, mat.p, box, mats, uu, partA);
-        } else {
-            KC(); k_energy_tiled<D, R><<<box.ntiles, T::NT, 0, st()>>>(P.p, cap, mat.p, cell_start.p, box, mats, uu,
-                                                                        partA);
-        }
+        KC(); k_energy_tiled<D, R><<<box.ntiles, T::NT, 0, st()>>>(P.p, cap, mat.p, cell_start.p, box, mats, uu,
+                                                                    partA);
         OSMPM_LAUNCH_CHECK();
         KC(); k_energy_nodes<D><<<grad_blocks_nodes(), 256, 0, st()>>>(box.nnodes, nown, m.p, vn.p, uu, dt, grav[0],
                                                                         grav[1], grav[2], partB);

@@ -161,23 +161,6 @@ template <typename R> struct Vec2;
 template <> struct Vec2<double> { using type = double2; };
 template <> struct Vec2<float> { using type = float2; };
 
-// phase 0: sv = input vector on the tile nodes, sy (NOUT tiles) = 0
-template <int D, typename R, int NOUT>
-__device__ __forceinline__ void stage_nodes(const BoxDev& b, const int* t, const double* __restrict__ vec, R* sv,
-                                            R* sy)
-{
-    using T = Tile<D>;
-    for (int idx = threadIdx.x; idx < T::NN * D; idx += T::NT) {
-        const int a = idx % D, l = idx / D;
-        int c[3];
-        tnode_coords<D>(l, c);
-        const int64_t g = box_node<D>(b, t[0] * T::T0 + c[0], t[1] * T::T1 + c[1], t[2] * T::T2 + c[2]);
-        sv[l * SV<D>::S + a] = (R)vec[g * D + a];
-#pragma unroll
-        for (int o = 0; o < NOUT; ++o) sy[o * T::NN * D + idx] = R(0);
-    }
-}
-
 // gather gd[a][b] = sum_i v_i,a dN_i/dx_b (tensor-product order, explicit FMA)
 template <int D, typename R>
 __device__ __forceinline__ void gather_grad(const R* sv, const int* lc, const R (*w)[3], const R (*dw)[3], R* gd)
@@ -340,38 +323,6 @@ __device__ __forceinline__ void item_quadratic(const R* Q, const ItemW<D, R>& W,
     }
 }
 
-// zero the staging array (16-B stores)
-template <int D, typename R>
-__device__ __forceinline__ void stage_zero(R* stg)
-{
-    using T = Tile<D>;
-    constexpr int UE = 16 / sizeof(R);
-    static_assert(Stage<D>::SIZE % UE == 0, "stage size");
-    int4 z = make_int4(0, 0, 0, 0);
-    for (int u = threadIdx.x; u < Stage<D>::SIZE / UE; u += T::NT) reinterpret_cast<int4*>(stg)[u] = z;
-}
-
-// phase-2 partials -> staging: item (cell (cx,cy), comp a, x-offset i) owns slot (i, j) of the nodes
-// (cx+i, cy+j, layer+kk); acc index (j*3 + kk) in 3D, (j) in 2D (j = last-axis offset there)
-template <int D, typename R>
-__device__ __forceinline__ void stage_item(int cellL, int a, int i, const R* acc, R* stg)
-{
-    using T = Tile<D>;
-    if (D == 3) {
-        const int cx = cellL / T::T1, cy = cellL % T::T1;
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-#pragma unroll
-            for (int kk = 0; kk < 3; ++kk) {
-                const int nxy = (cx + i) * T::N1 + (cy + j);
-                stg[((nxy * 3 + kk) * 3 + a) * 9 + i * 3 + j] = acc[j * 3 + kk];
-            }
-    } else {
-#pragma unroll
-        for (int j = 0; j < 3; ++j) stg[(((cellL + i) * 3 + j) * 2 + a) * 3 + i] = acc[j];
-    }
-}
-
 // fixed NSLOT-term sums -> node accumulator tile sy
 template <int D, typename R>
 __device__ __forceinline__ void layer_flush(int layer, const R* stg, R* sy)
@@ -424,360 +375,10 @@ __device__ __forceinline__ void weights_at(const Rw* x, const BoxDev& b, const i
 // a5: HVP  y += sum_p V0 dP(F_p(u); gd F^n) F^nT grad N  =  sum_p G_p grad N with
 //     G = gd S' + c' Ah gd^T Ah + l' (Ah : gd) Ah   (derivation from PAPER.md:188, 208)
 // =============================================================================================
-template <int D, bool PF> struct HvpOcc { static constexpr int MIN_BLOCKS = (D == 3) ? (PF ? 3 : 4) : 4; };
-
-// per-particle streamed inputs: x (D) and the Newton cache (CL<D>::NF fields)
 template <int D, typename R> struct HvpIn {
     static constexpr int NF = D + CL<D>::NF;
     static constexpr int UE = 16 / sizeof(R);
     static constexpr int PFS = Tile<D>::NT + 2 * UE;  // per-field capacity (alignment slack)
 };
-
-template <int D, typename R, bool PF = true>
-constexpr size_t hvp_smem_bytes()
-{
-    using T = Tile<D>;
-    constexpr size_t rec = (size_t)HvpRec<D, R>::RS * T::NT;
-    constexpr size_t recstg = rec > (size_t)Stage<D>::SIZE ? rec : (size_t)Stage<D>::SIZE;
-    return 16 + ((size_t)T::NN * SV<D>::S + T::NN * D + recstg +
-                 (PF ? (size_t)HvpIn<D, R>::NF * HvpIn<D, R>::PFS : 0)) * sizeof(R);
-}
-
-// issue the TMA bulk copies of the first min(NT, le - lb) particles of a layer
-template <int D, typename R>
-__device__ __forceinline__ int hvp_prefetch(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, int lb,
-                                            int le, R* pf, uint64_t* bar)
-{
-    using In = HvpIn<D, R>;
-    const int lb0 = lb & ~(In::UE - 1);                       // 16-B aligned start
-    const int cnt = min(le, lb + Tile<D>::NT) - lb0;
-    const int cnt_al = (cnt + In::UE - 1) & ~(In::UE - 1);    // 16-B multiple
-    const uint32_t bytes = (uint32_t)cnt_al * sizeof(R);
-    fence_async_smem();
-    mbar_expect_tx(bar, bytes * In::NF);
-#pragma unroll 1
-    for (int f = 0; f < In::NF; ++f) {
-        const R* src = (f < D) ? P + (int64_t)(PL<D>::X + f) * cap + lb0 : cache + (int64_t)(f - D) * cap + lb0;
-        bulk_g2s(pf + f * In::PFS, src, bytes, bar);
-    }
-    return lb0;
-}
-
-template <int D, typename R, bool PF = true>
-__global__ void __launch_bounds__(Tile<D>::NT, HvpOcc<D, PF>::MIN_BLOCKS)
-k_hvp(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, const int* __restrict__ cell_start,
-      BoxDev b, const double* __restrict__ din, double* __restrict__ yout)
-{
-    using T = Tile<D>;
-    using C = CL<D>;
-    using In = HvpIn<D, R>;
-    constexpr int RS = HvpRec<D, R>::RS;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
-    R* sv = reinterpret_cast<R*>(smem_raw + 16);
-    R* sy = sv + T::NN * SV<D>::S;
-    R* pf = sy + T::NN * D;                 // streamed particle inputs (NF fields x PFS)
-    R* rec = pf + (PF ? In::NF * In::PFS : 0);  // per-particle records, aliased by the staging array
-    R* stg = rec;
-    const int tile = blockIdx.x;
-    const int64_t kt = (int64_t)tile * T::NC;
-    __shared__ int scs[T::NC + 1];  // the tile's cell ranges
-    for (int i = threadIdx.x; i <= T::NC; i += T::NT) scs[i] = cell_start[kt + i];
-    __syncthreads();
-    if (scs[0] == scs[T::NC]) return;
-    // first non-empty layer and its prefetch
-    int layer = 0;
-    while (scs[layer * T::LC] == scs[(layer + 1) * T::LC]) ++layer;
-    int lb0 = 0;
-    if (PF && threadIdx.x == 0) {
-        mbar_init(bar, 1);
-        fence_async_smem();
-        lb0 = hvp_prefetch<D, R>(P, cache, cap, scs[layer * T::LC], scs[(layer + 1) * T::LC], pf, bar);
-    }
-    int t[3];
-    tile_coords<D>(b, tile, t);
-    stage_nodes<D, R, 1>(b, t, din, sv, sy);
-    __syncthreads();
-    const int it = threadIdx.x;
-    const int icell = it / (D * 3), icomp = (it / 3) % D, ii = it % 3;
-    uint32_t parity = 0;
-    while (layer < T::NL) {
-        const int lb = scs[layer * T::LC], le = scs[(layer + 1) * T::LC];
-        int next = layer + 1;
-        while (next < T::NL && scs[next * T::LC] == scs[(next + 1) * T::LC]) ++next;
-        const int pf_base = lb & ~(In::UE - 1);
-        const int ks = scs[layer * T::LC + icell];
-        const int ke = scs[layer * T::LC + icell + 1];
-        R acc[T::NACC];
-#pragma unroll
-        for (int k = 0; k < T::NACC; ++k) acc[k] = R(0);
-        for (int sb = lb; sb < le; sb += T::NT) {
-            const int se = min(sb + T::NT, le);
-            const int q = threadIdx.x, p = sb + q;
-            const bool from_pf = PF && (sb == lb);
-            if (from_pf) mbar_wait(bar, parity);
-            if (p < se) {
-                // streamed inputs: smem copy of the first NT particles, global beyond
-                R x[3], S[Sym<D>::N], A[D * D], cc, ll;
-                if (from_pf) {
-                    const R* s = pf + (p - pf_base);
-#pragma unroll
-                    for (int a = 0; a < D; ++a) x[a] = s[a * In::PFS];
-#pragma unroll
-                    for (int k = 0; k < Sym<D>::N; ++k) S[k] = s[(D + C::S + k) * In::PFS];
-#pragma unroll
-                    for (int k = 0; k < D * D; ++k) A[k] = s[(D + C::A + k) * In::PFS];
-                    cc = s[(D + C::C) * In::PFS];
-                    ll = s[(D + C::L) * In::PFS];
-                } else {
-#pragma unroll
-                    for (int a = 0; a < D; ++a) x[a] = P[(PL<D>::X + a) * cap + p];
-#pragma unroll
-                    for (int k = 0; k < Sym<D>::N; ++k) S[k] = cache[(C::S + k) * cap + p];
-#pragma unroll
-                    for (int k = 0; k < D * D; ++k) A[k] = cache[(C::A + k) * cap + p];
-                    cc = cache[C::C * cap + p];
-                    ll = cache[C::L * cap + p];
-                }
-                R w[3][3], dw[3][3];
-                int lc[3] = {0, 0, 0};
-                weights_at<D, R>(x, b, t, lc, w, dw);
-                R gd[D * D];
-                gather_grad<D, R>(sv, lc, w, dw, gd);
-                const RecPtr<R> r(rec, q, RS);
-                store_weights<D, R>(r, w, dw);
-                // M2 = A gd^T ; tr = A : gd
-                R M2[D * D], tr = R(0);
-#pragma unroll
-                for (int a = 0; a < D; ++a)
-#pragma unroll
-                    for (int bb = 0; bb < D; ++bb) {
-                        R s = R(0);
-#pragma unroll
-                        for (int k = 0; k < D; ++k) s = fma(A[a * D + k], gd[bb * D + k], s);
-                        M2[a * D + bb] = s;
-                        tr = fma(A[a * D + bb], gd[a * D + bb], tr);
-                    }
-                const R ltr = ll * tr;
-#pragma unroll
-                for (int a = 0; a < D; ++a)
-#pragma unroll
-                    for (int bb = 0; bb < D; ++bb) {
-                        R s1 = R(0), s2 = R(0);
-#pragma unroll
-                        for (int k = 0; k < D; ++k) {
-                            s1 = fma(gd[a * D + k], S[sym_idx<D>(k, bb)], s1);
-                            s2 = fma(M2[a * D + k], A[k * D + bb], s2);
-                        }
-                        *r.at(Rec<D>::G + a * D + bb) = fma(cc, s2, fma(ltr, A[a * D + bb], s1));
-                    }
-            }
-            __syncthreads();
-            if (from_pf) {
-                parity ^= 1u;
-                // the streamed buffer is free: start the next layer's copies now
-                if (threadIdx.x == 0 && next < T::NL)
-                    hvp_prefetch<D, R>(P, cache, cap, scs[next * T::LC], scs[(next + 1) * T::LC], pf, bar);
-            }
-            if (it < T::ITEMS) {
-                const int p0 = max(ks, sb), p1 = min(ke, se);
-                const int len = p1 - p0, rot = len > 0 ? (icell & 7) % len : 0;
-                for (int k = 0; k < len; ++k) {
-                    const RecPtr<R> r(rec, rotated(p0, len, k, rot) - sb, RS);
-                    ItemW<D, R> W;
-                    W.load(r, ii);
-                    R s[D];
-#pragma unroll
-                    for (int bb = 0; bb < D; ++bb) s[bb] = *r.at(Rec<D>::G + icomp * D + bb);
-                    item_linear<D, R>(s, W, acc);
-                }
-            }
-            __syncthreads();
-        }
-        stage_zero<D, R>(stg);
-        __syncthreads();
-        if (it < T::ITEMS) stage_item<D, R>(icell, icomp, ii, acc, stg);
-        __syncthreads();
-        layer_flush<D, R>(layer, stg, sy);
-        __syncthreads();
-        layer = next;
-    }
-    (void)lb0;
-    tile_flush<D, R>(b, t, sy, yout);
-}
-
-// =============================================================================================
-// a4: gradient + energy + Newton cache + Jacobi diagonal (tiled, fp64 arithmetic: DESIGN.md R14)
-//   M = I + grad u, F(u) = M F^n, J = det M det F^n,  Ah = M^{-T},  S' = V0 mu F^n F^nT
-//   G_grad = V0 P(F(u)) F^nT = M S' - c' Ah ;  diag_a += gradN^T (S' + (c' + l') Ah_a Ah_a^T) gradN
-//   V0 Psi = 1/2 (tr(M S' M^T) - V0 mu d) - V0 mu ln J + V0 lam/2 ln^2 J
-// partials per CTA: {sum V0 Psi, sum V0 |Psi|, inverted}
-// =============================================================================================
-template <int D>
-constexpr size_t grad_smem_bytes()
-{
-    using T = Tile<D>;
-    constexpr size_t rec = (size_t)GradRec<D>::RS * T::NT;
-    constexpr size_t recstg = rec > (size_t)Stage<D>::SIZE ? rec : (size_t)Stage<D>::SIZE;
-    return ((size_t)T::NN * SV<D>::S + 2 * T::NN * D + recstg) * sizeof(double);
-}
-
-template <int D, typename R>
-__global__ void __launch_bounds__(Tile<D>::NT)
-k_grad(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int* __restrict__ mat,
-       const int* __restrict__ cell_start, BoxDev b, MatTable mt, const double* __restrict__ uin,
-       double* __restrict__ gout, double* __restrict__ dout, double* __restrict__ partials)
-{
-    using T = Tile<D>;
-    using GR = GradRec<D>;
-    using L = PL<D>;
-    using C = CL<D>;
-    using Rd = double;
-    constexpr int RS = GR::RS;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Rd* sv = reinterpret_cast<Rd*>(smem_raw);
-    Rd* sy = sv + T::NN * SV<D>::S;  // [0]: gradient tile, [NN*D]: diagonal tile
-    Rd* rec = sy + 2 * T::NN * D;
-    Rd* stg = rec;
-    const int tile = blockIdx.x;
-    const int64_t kt = (int64_t)tile * T::NC;
-    double red[3] = {0.0, 0.0, 0.0};
-    __shared__ int scs[T::NC + 1];  // the tile's cell ranges
-    for (int i = threadIdx.x; i <= T::NC; i += T::NT) scs[i] = cell_start[kt + i];
-    __syncthreads();
-    if (scs[0] == scs[T::NC]) {
-        if (threadIdx.x == 0) {
-            partials[blockIdx.x * 3 + 0] = 0.0;
-            partials[blockIdx.x * 3 + 1] = 0.0;
-            partials[blockIdx.x * 3 + 2] = 0.0;
-        }
-        return;
-    }
-    int t[3];
-    tile_coords<D>(b, tile, t);
-    stage_nodes<D, Rd, 2>(b, t, uin, sv, sy);
-    __syncthreads();
-    const int it = threadIdx.x;
-    const int icell = it / (D * 3), icomp = (it / 3) % D, ii = it % 3;
-    for (int layer = 0; layer < T::NL; ++layer) {
-        const int lb = scs[layer * T::LC], le = scs[(layer + 1) * T::LC];
-        if (lb == le) continue;
-        const int ks = scs[layer * T::LC + icell];
-        const int ke = scs[layer * T::LC + icell + 1];
-        Rd acc[T::NACC], accd[T::NACC];
-#pragma unroll
-        for (int k = 0; k < T::NACC; ++k) acc[k] = accd[k] = 0.0;
-        for (int sb = lb; sb < le; sb += T::NT) {
-            const int se = min(sb + T::NT, le);
-            const int q = threadIdx.x, p = sb + q;
-            if (p < se) {
-                Rd x[3], w[3][3], dw[3][3];
-                int lc[3] = {0, 0, 0};
-#pragma unroll
-                for (int a = 0; a < D; ++a) x[a] = (Rd)P[(L::X + a) * cap + p];
-                weights_at<D, Rd>(x, b, t, lc, w, dw);
-                Rd Mx[D * D];
-                gather_grad<D, Rd>(sv, lc, w, dw, Mx);
-                const RecPtr<Rd> r(rec, q, RS);
-                store_weights<D, Rd>(r, w, dw);
-#pragma unroll
-                for (int a = 0; a < D; ++a) Mx[a * D + a] += 1.0;
-                Rd Fn[D * D];
-#pragma unroll
-                for (int k = 0; k < D * D; ++k) Fn[k] = (Rd)P[(L::F + k) * cap + p];
-                const Rd V0 = (Rd)P[L::VOL * cap + p];
-                const int mid = mat[p];
-                const Rd mu = mt.mu[mid], lam = mt.lam[mid];
-                Rd S[Sym<D>::N];
-#pragma unroll
-                for (int a = 0; a < D; ++a)
-#pragma unroll
-                    for (int bb = a; bb < D; ++bb) {
-                        Rd s = 0;
-#pragma unroll
-                        for (int k = 0; k < D; ++k) s = fma(Fn[a * D + k], Fn[bb * D + k], s);
-                        S[sym_idx<D>(a, bb)] = V0 * mu * s;
-                    }
-                const Rd detM = det<D, Rd>(Mx), detFn = det<D, Rd>(Fn);
-                Rd Ah[D * D];
-                cofactor<D, Rd>(Mx, Ah);
-                const Rd invdet = 1.0 / detM;
-#pragma unroll
-                for (int k = 0; k < D * D; ++k) Ah[k] *= invdet;
-                const bool ok = detM > 0.0 && detFn > 0.0;
-                const Rd lnJ = ok ? log(detM) + log(detFn) : 0.0;
-                const Rd cc = V0 * (mu - lam * lnJ), ll = V0 * lam;
-                Rd trMSM = 0;
-#pragma unroll
-                for (int a = 0; a < D; ++a)
-#pragma unroll
-                    for (int bb = 0; bb < D; ++bb) {
-                        Rd s = 0;
-#pragma unroll
-                        for (int k = 0; k < D; ++k) s = fma(Mx[a * D + k], S[sym_idx<D>(k, bb)], s);
-                        trMSM = fma(s, Mx[a * D + bb], trMSM);
-                        *r.at(Rec<D>::G + a * D + bb) = fma(-cc, Ah[a * D + bb], s);
-                    }
-                const Rd psiV = 0.5 * (trMSM - V0 * mu * D) - V0 * mu * lnJ + 0.5 * V0 * lam * lnJ * lnJ;
-                red[0] += psiV;
-                red[1] += fabs(psiV);
-                if (!ok) red[2] += 1.0;
-#pragma unroll
-                for (int k = 0; k < Sym<D>::N; ++k) {
-                    *r.at(GR::S + k) = S[k];
-                    cache[(C::S + k) * cap + p] = (R)S[k];
-                }
-#pragma unroll
-                for (int k = 0; k < D * D; ++k) {
-                    *r.at(GR::A + k) = Ah[k];
-                    cache[(C::A + k) * cap + p] = (R)Ah[k];
-                }
-                cache[C::C * cap + p] = (R)cc;
-                cache[C::L * cap + p] = (R)ll;
-                *r.at(GR::CL) = cc + ll;
-            }
-            __syncthreads();
-            if (it < T::ITEMS) {
-                const int p0 = max(ks, sb), p1 = min(ke, se);
-                const int len = p1 - p0, rot = len > 0 ? (icell & 7) % len : 0;
-                for (int k = 0; k < len; ++k) {
-                    const RecPtr<Rd> r(rec, rotated(p0, len, k, rot) - sb, RS);
-                    ItemW<D, Rd> W;
-                    W.load(r, ii);
-                    Rd s[D], Ar[D], Q[Sym<D>::N];
-#pragma unroll
-                    for (int bb = 0; bb < D; ++bb) {
-                        s[bb] = *r.at(Rec<D>::G + icomp * D + bb);
-                        Ar[bb] = *r.at(GR::A + icomp * D + bb);
-                    }
-                    const Rd clv = *r.at(GR::CL);
-#pragma unroll
-                    for (int a = 0; a < D; ++a)
-#pragma unroll
-                        for (int bb = a; bb < D; ++bb)
-                            Q[sym_idx<D>(a, bb)] = fma(clv * Ar[a], Ar[bb], *r.at(GR::S + sym_idx<D>(a, bb)));
-                    item_linear<D, Rd>(s, W, acc);
-                    item_quadratic<D, Rd>(Q, W, accd);
-                }
-            }
-            __syncthreads();
-        }
-        stage_zero<D, Rd>(stg);
-        __syncthreads();
-        if (it < T::ITEMS) stage_item<D, Rd>(icell, icomp, ii, acc, stg);
-        __syncthreads();
-        layer_flush<D, Rd>(layer, stg, sy);
-        __syncthreads();
-        stage_zero<D, Rd>(stg);
-        __syncthreads();
-        if (it < T::ITEMS) stage_item<D, Rd>(icell, icomp, ii, accd, stg);
-        __syncthreads();
-        layer_flush<D, Rd>(layer, stg, sy + T::NN * D);
-        __syncthreads();
-    }
-    tile_flush<D, Rd>(b, t, sy, gout);
-    tile_flush<D, Rd>(b, t, sy + T::NN * D, dout);
-    block_reduce_store<3>(red, partials);
-}
 
 }  // namespace osmpm

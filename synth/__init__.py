@@ -348,3 +348,31 @@ def c5_bench_workload(cells=128, full_box=True, pad=3):
     assert (R >= 0).all() and (R < np.asarray(gd)[None, :3]).all()
     recv = (R[:, 0] * gd[1] + R[:, 1]) * gd[2] + R[:, 2]
     return fine, coarse, np.ascontiguousarray(recv.astype(np.int64))
+
+
+def cantilever_pair(dx_coarse, r=4, ppa=3, L=1.0, H=0.2, x_fine=(0.0, 0.3), x_coarse=(0.2, 1.0), E=1.0e5, nu=0.4,
+                    rho=1000.0, g=0.0, dT=10.0, M=1, y0=1.0, seed=1100):
+    """The dual-domain cantilever of PAPER.md:511-549 (§4.1) at a chosen resolution: beam L x H clamped at
+    x = 0, split longitudinally into a fine subdomain x in x_fine (dx = dx_coarse / r) and a coarse one
+    x in x_coarse (dx_coarse), ppa x ppa particles per cell on the regular lattice (the paper: 9 per cell),
+    material E, nu, rho (the paper: 100 kPa, 0.4, 1000), gravity g downward.  P^∂: particles within one own
+    cell of each artificial cut (R10).  Returns (coarse, fine) scenes; dt = dT (coarse) and
+    dT / M (fine)."""
+    out = []
+    for (lo_x, hi_x, dx, cut) in ((x_coarse[0], x_coarse[1], dx_coarse, x_coarse[0]),
+                                  (x_fine[0], x_fine[1], dx_coarse / r, x_fine[1])):
+        x, vol = lattice((lo_x, y0), (hi_x, y0 + H), dx, ppa)
+        bnd = (np.abs(x[:, 0] - cut) < dx).astype(np.uint8)
+        p = make_particles(x, vol, rho, boundary=bnd)
+        grid = grid_around(np.vstack([x, [[lo_x, y0 - L], [hi_x, y0 + H + 0.1 * L]]]), dx, 4, 2)
+        out.append(Scene(grid, p, [(E, nu)], dT if dx == dx_coarse else dT / M, (0.0, -g, 0.0),
+                         meta={"config": "cantilever", "M": M}))
+    return out[0], out[1]
+
+
+def cantilever_single(dx, ppa=3, L=1.0, H=0.2, E=1.0e5, nu=0.4, rho=1000.0, g=0.0, dT=10.0, y0=1.0):
+    """The single-domain cantilever of the same geometry ("single-domain")."""
+    x, vol = lattice((0.0, y0), (L, y0 + H), dx, ppa)
+    p = make_particles(x, vol, rho)
+    grid = grid_around(np.vstack([x, [[0.0, y0 - L], [L, y0 + H + 0.1 * L]]]), dx, 4, 2)
+    return Scene(grid, p, [(E, nu)], dT, (0.0, -g, 0.0), meta={"config": "cantilever"})
