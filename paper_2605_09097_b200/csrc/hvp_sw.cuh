@@ -405,8 +405,12 @@ template <int D, typename R>
 __global__ void __launch_bounds__(Tile<D>::NT, sizeof(R) == 8 ? 3 : 4)
 k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, const int* __restrict__ cell_start,
          BoxDev b, const double* __restrict__ din, double* __restrict__ yout, const __grid_constant__ CUtensorMap tmx,
-         const __grid_constant__ CUtensorMap tmc, int use_tmap, double* __restrict__ tbuf)
+         const __grid_constant__ CUtensorMap tmc, int use_tmap, double* __restrict__ tbuf,
+         double* __restrict__ pkp)
 {
+    // pkp (optional): per-CTA partial of d^T K d = sum_p G_p : gd_p, the curvature the PCG step length
+    // needs (sum_i d_i . (K d)_i = sum_i d_i . sum_p G_p grad N_ip = sum_p G_p : gd_p), so that PCG needs
+    // no separate pass over y
     using T = Tile<D>;
     using C = CL<D>;
     using In = HvpIn<D, R>;
@@ -458,8 +462,10 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
     __syncthreads();
     if (scs[0] == scs[T::NC]) {
         if constexpr (ASYNC) asm volatile("cp.async.wait_all;" ::: "memory");
+        if (pkp && threadIdx.x == 0) pkp[tile] = 0.0;
         return;
     }
+    double dkd = 0.0;  // this thread's particles' G_p : gd_p
     auto layer_empty = [&](int l) { return scs[l * T::LC] == scs[(l + 1) * T::LC]; };
     if constexpr (ASYNC)
         asm volatile("cp.async.wait_all;" ::: "memory");
@@ -547,6 +553,12 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                             }
                             Ga[bb] = fma(cc, s2, fma(ltr, A[a * D + bb], s1));
                         }
+                        if (pkp) {
+                            R q = R(0);
+#pragma unroll
+                            for (int bb = 0; bb < D; ++bb) q = fma(Ga[bb], gd[a * D + bb], q);
+                            dkd += (double)q;
+                        }
                         if constexpr (SR::GP == 4) {
                             using V2 = typename Vec2<R>::type;
                             V2 g01;
@@ -603,6 +615,10 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
         // the next emit must not overwrite slots still being summed: a non-empty next layer has its
         // records barrier in between; otherwise synchronise here
         if (layer + 1 >= T::NL || layer_empty(layer + 1)) __syncthreads();
+    }
+    if (pkp) {
+        double v[1] = {dkd};
+        block_reduce_store<1>(v, pkp);
     }
 }
 

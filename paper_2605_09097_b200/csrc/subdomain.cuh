@@ -60,7 +60,7 @@ static inline int nblk_all(int64_t n, int bs)
 // ncclAllReduce'd before use.
 struct CGScalars;
 struct GroupBufs {
-    DBuf<double> partA, partB, scal, gsum, halo_tmp;
+    DBuf<double> partA, partB, partM, partH, scal, gsum, halo_tmp;  // partM / partH: PCG d^T M d, d^T K d
     DBuf<CGScalars> cgs;
     DBuf<int> gbounds;
     double* h_scal = nullptr;  // pinned
@@ -691,7 +691,7 @@ struct Sub : public osmpm_subdomain {
     }
 
     // a5: the sliding-window tiled HVP (hvp_sw.cuh)
-    osmpm_status launch_hvp(const double* din, double* yout)
+    osmpm_status launch_hvp(const double* din, double* yout, double* pkp = nullptr)
     {
         auto& pf = ctx->prof;
         if (pf.on) pf.begin("hvp", st());
@@ -713,7 +713,7 @@ struct Sub : public osmpm_subdomain {
         const bool det = det_mode();
         if (det) OSMPM_TRY(det_a.need((size_t)box.ntiles * T::NN * D));
         KC(); k_hvp_sw<D, R><<<box.ntiles, T::NT, hvp_sw_smem_bytes<D, R>(), st()>>>(
-            P.p, cache.p, cap, cell_start.p, box, din, yout, tm_x, tm_c, tm_ok ? 1 : 0, det ? det_a.p : nullptr);
+            P.p, cache.p, cap, cell_start.p, box, din, yout, tm_x, tm_c, tm_ok ? 1 : 0, det ? det_a.p : nullptr, pkp);
         if (det) {
             OSMPM_LAUNCH_CHECK();
             OSMPM_TRY(det_gather(det_a.p, yout));
