@@ -47,6 +47,8 @@ def parse():
                     help="skip the fp32-variant sub-run that a 1-GPU f64 run reports under `variants`")
     ap.add_argument("--no-prof", action="store_true", help="skip the per-kernel event timing (A/B of its overhead)")
     ap.add_argument("--cpu-cells", type=int, default=14, help="oracle sample cube side (cells)")
+    ap.add_argument("--cg-variant", type=int, default=0, choices=[0, 1],
+                    help="PCG variant: 0 standard, 1 single-reduction (Chronopoulos-Gear, DESIGN.md R22)")
     ap.add_argument("--slabs", type=int, default=1,
                     help="x-slabs per GPU (>1: the decomposed path on one device, halo by device copies)")
     return ap.parse_args()
@@ -143,7 +145,7 @@ def fp32_variant(args):
     measured device-only in a child process of this bench (same steps / warm-up)."""
     import subprocess
     cmd = [sys.executable, os.path.abspath(__file__), "--precision", "f32", "--steps", str(args.steps), "--warmup",
-           str(args.warmup), "--cells", str(args.cells), "--newton", str(args.newton), "--cg", str(args.cg),
+           str(args.warmup), "--cells", str(args.cells), "--newton", str(args.newton), "--cg", str(args.cg), "--cg-variant", str(args.cg_variant),
            "--no-e2e", "--no-cpu-baseline", "--no-variants"]
     try:
         out = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
@@ -323,7 +325,7 @@ def main():
     # v_B^{n+1}: the smooth field advanced (scaled) in time -> distinct endpoint for T_m
     csub.set_grid_velocity((cg["v"] * 1.01).contiguous())
     recv_d = torch.from_numpy(recv).to(dev)
-    settings = osmpm.newton_settings(max_newton=args.newton, max_cg=args.cg, fixed_iters=1)
+    settings = osmpm.newton_settings(max_newton=args.newton, max_cg=args.cg, fixed_iters=1, cg_variant=args.cg_variant)
     mask_all = torch.full((recv.shape[0],), 7, dtype=torch.uint8, device=dev)
 
     # a11: the step's initial particle state, restored at the start of every step (warm-up and timed
@@ -479,7 +481,7 @@ def main():
                                "dx=1/512, 8 ppc, one fine implicit sub-step (10 Newton x 50 PCG) with "
                                "coarse<->fine transmission to the dx=1/128 overlap grid",
                    "particles": n, "particles_rank0": n_local, "cells": args.cells, "newton": args.newton,
-                   "cg": args.cg, "active_nodes_rank0": n_active, "box_nodes_rank0": int(np.prod(box_dims)),
+                   "cg": args.cg, "cg_variant": args.cg_variant, "active_nodes_rank0": n_active, "box_nodes_rank0": int(np.prod(box_dims)),
                    "receivers": int(recv.shape[0]),
                    "state": "every step restores the checkpointed initial particle state (a11) first; "
                             "the e2e leg uploads it from pinned host memory instead",

@@ -106,6 +106,10 @@ typedef struct {
 typedef struct {
     int32_t max_newton, max_cg, fixed_iters, guess;
     double newton_rtol, newton_atol, cg_rtol, ls_min_alpha, energy_noise_rtol;
+    int32_t cg_variant;  /* 0: standard Jacobi PCG (two reductions per iteration); 1: single-reduction
+                            PCG (Chronopoulos-Gear, R22: the same iterates in exact arithmetic,
+                            one reduction -- one all-reduce across ranks -- per iteration) */
+    int32_t reserved;    /* 0 */
 } osmpm_newton_settings;
 
 /* Outcome of one implicit solve.  Besides the counts, three events that change what the solve

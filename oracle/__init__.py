@@ -29,7 +29,7 @@ class OrcNewtonSettings(C.Structure):
     _fields_ = [("max_newton", C.c_int32), ("max_cg", C.c_int32), ("fixed_iters", C.c_int32),
                 ("guess", C.c_int32), ("newton_rtol", C.c_double), ("newton_atol", C.c_double),
                 ("cg_rtol", C.c_double), ("ls_min_alpha", C.c_double),
-                ("energy_noise_rtol", C.c_double)]
+                ("energy_noise_rtol", C.c_double), ("cg_variant", C.c_int32), ("reserved", C.c_int32)]
 
 
 class OrcSolveStats(C.Structure):
@@ -264,6 +264,7 @@ def default_settings(**kw) -> OrcNewtonSettings:
     s.cg_rtol = kw.get("cg_rtol", 1e-8)
     s.ls_min_alpha = kw.get("ls_min_alpha", 2.0 ** -20)
     s.energy_noise_rtol = kw.get("energy_noise_rtol", 1e-13)
+    s.cg_variant = kw.get("cg_variant", 0)
     return s
 
 

@@ -37,6 +37,7 @@ typedef struct {
 typedef struct {
     int32_t max_newton, max_cg, fixed_iters, guess;
     double newton_rtol, newton_atol, cg_rtol, ls_min_alpha, energy_noise_rtol;
+    int32_t cg_variant, reserved; /* 0: standard Jacobi PCG; 1: single-reduction (Chronopoulos-Gear) */
 } orc_newton_settings;
 
 typedef struct {
@@ -526,6 +527,62 @@ static double dot_free(int64_t n, const uint8_t* fm, const double* a, const doub
     return s;
 }
 
+/* Single-reduction Jacobi PCG (Chronopoulos & Gear 1989; R22): the same Krylov iterates as
+ * the standard PCG in exact arithmetic, with the two inner products of an iteration taken together
+ * after the one Hessian-vector product, so a distributed solve needs one reduction per iteration.
+ * Iteration k (one HVP each, max_cg in all):
+ *   [tolerance mode: stop if |r_k| <= cg_rtol |g|]
+ *   u_k = diag^-1 r_k,  w_k = H u_k,  gamma_k = (r_k, u_k),  delta_k = (w_k, u_k)
+ *   k = 0: beta = 0, c = delta_0;  k > 0: beta = gamma_k / gamma_{k-1}, c = delta_k - beta gamma_k / alpha_{k-1}
+ *   (c = p_k^T H p_k); c <= 0: non-positive curvature -> stop (k = 0: x = u_0)  [R7]
+ *   alpha_k = gamma_k / c,  p_k = u_k + beta p_{k-1},  s_k = w_k + beta s_{k-1}  (= H p_k)
+ *   x_{k+1} = x_k + alpha_k p_k,  r_{k+1} = r_k - alpha_k s_k
+ * Arrays: xs (x), r, z (u), pv (p), q (w), ut (s), all over nd DOFs. */
+static int pcg_single_reduction(const orc_grid* g, int64_t np, const double* x, const double* F, const double* V0,
+                                const int32_t* mat, const double* E, const double* nu, double dt, const double* mi,
+                                const double* u, const double* gr, const double* dg, const uint8_t* free_mask,
+                                const orc_newton_settings* st, double gn, int64_t nd, double* xs, double* r, double* z,
+                                double* pv, double* q, double* sv, orc_solve_stats* stats)
+{
+    for (int64_t k = 0; k < nd; ++k) {
+        xs[k] = 0.0;
+        r[k] = free_mask[k] ? -gr[k] : 0.0;
+        pv[k] = 0.0;
+        sv[k] = 0.0;
+    }
+    double gamma_old = 0.0, alpha_old = 0.0;
+    for (int cg = 0; cg < st->max_cg; ++cg) {
+        double rn = sqrt(dot_free(nd, free_mask, r, r));
+        if (!st->fixed_iters && rn <= st->cg_rtol * gn) break;
+        for (int64_t k = 0; k < nd; ++k) z[k] = free_mask[k] ? r[k] / dg[k] : 0.0;
+        int rc = orc_hvp(g, np, x, F, V0, mat, E, nu, dt, mi, u, z, NULL, q);
+        if (rc) return rc;
+        for (int64_t k = 0; k < nd; ++k)
+            if (!free_mask[k]) q[k] = 0.0;
+        stats->cg_iters++;
+        double gamma = dot_free(nd, free_mask, r, z);
+        double delta = dot_free(nd, free_mask, q, z);
+        double beta = (cg == 0 || !(gamma_old > 0.0)) ? 0.0 : gamma / gamma_old;
+        double c = (cg == 0) ? delta : delta - beta * gamma / alpha_old;
+        if (!(c > 0.0)) {
+            if (cg == 0)
+                for (int64_t k = 0; k < nd; ++k) xs[k] = z[k];
+            stats->negcurv++;
+            break;
+        }
+        double alpha = gamma / c;
+        for (int64_t k = 0; k < nd; ++k) {
+            pv[k] = z[k] + beta * pv[k];
+            sv[k] = q[k] + beta * sv[k];
+            xs[k] += alpha * pv[k];
+            r[k] -= alpha * sv[k];
+        }
+        gamma_old = gamma;
+        alpha_old = alpha;
+    }
+    return ORC_OK;
+}
+
 int orc_implicit_solve(const orc_grid* g, int64_t np, const double* x, const double* F,
                        const double* V0, const int32_t* mat, const double* E, const double* nu,
                        double dt, const double* mi, const double* vn, const double* fext,
@@ -578,6 +635,12 @@ int orc_implicit_solve(const orc_grid* g, int64_t np, const double* x, const dou
         if (rc) goto done;
         for (int64_t k = 0; k < nd; ++k)
             if (!free_mask[k]) dg[k] = 1.0;
+        if (st->cg_variant == 1) {
+            rc = pcg_single_reduction(g, np, x, F, V0, mat, E, nu, dt, mi, u, gr, dg, free_mask, st, gn, nd, xs,
+                                      r, z, pv, q, ut, stats);
+            if (rc) goto done;
+            goto line_search;
+        }
         /* Jacobi PCG on H dx = -g over the free DOFs */
         for (int64_t k = 0; k < nd; ++k) {
             xs[k] = 0.0;
@@ -615,6 +678,7 @@ int orc_implicit_solve(const orc_grid* g, int64_t np, const double* x, const dou
             rz = rz_new;
             for (int64_t k = 0; k < nd; ++k) pv[k] = z[k] + beta * pv[k];
         }
+    line_search:;
         /* backtracking line search: halve alpha from 1 until E decreases (Z10) */
         double E0, Ea0, Et, Eat;
         rc = orc_energy(g, np, x, F, V0, mat, E, nu, dt, mi, vn, fext, u, &E0, &Ea0);

@@ -215,8 +215,11 @@ k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int
             sw_emit<D, Rd>(icell, icomp, ii, accd, stgd);
         }
         __syncthreads();
-        sw_flush<D, Rd>(b, t, layer, stg, gout, tbg ? tbg + (int64_t)tile * T::NN * D : nullptr);
-        sw_flush<D, Rd>(b, t, layer, stgd, dout, tbd ? tbd + (int64_t)tile * T::NN * D : nullptr);
+        double nodot = 0.0;
+        sw_flush<D, Rd, false>(b, t, layer, stg, gout, tbg ? tbg + (int64_t)tile * T::NN * D : nullptr, nullptr,
+                               nullptr, nodot);
+        sw_flush<D, Rd, false>(b, t, layer, stgd, dout, tbd ? tbd + (int64_t)tile * T::NN * D : nullptr, nullptr,
+                               nullptr, nodot);
         if (layer + 1 >= T::NL || layer_empty(layer + 1)) __syncthreads();
     }
     block_reduce_store<3>(red, partials);

@@ -280,7 +280,7 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
     OSMPM_TRY(gb.partB.need((size_t)std::max<int64_t>(std::max(nbn_tot, nbd_tot), 1) * 4));
     // PCG curvature partials: p^T M p per node-vector block (k_cg_init / k_cg_p), p^T K p per HVP tile
     int64_t nbH = 0;
-    for (int i = 0; i < G.ns; ++i) nbH += G.s[i]->box.ntiles;
+    for (int i = 0; i < G.ns; ++i) nbH += (int64_t)G.s[i]->box.ntiles * HVP_NW<D>;
     const int64_t nbM = nbd_tot;
     OSMPM_TRY(gb.partM.need((size_t)std::max<int64_t>(nbM, 1)));
     OSMPM_TRY(gb.partH.need((size_t)std::max<int64_t>(nbH, 1)));
@@ -348,6 +348,65 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
             converged = true;
             break;
         }
+        if (s->cg_variant == 1) {
+            // single-reduction PCG (Chronopoulos-Gear, R22): one reduction / all-reduce per iteration
+            int64_t off = 0;
+            for (int i = 0; i < G.ns; ++i) {
+                Sub<D, R>* q = G.s[i];
+                const int64_t ndof = q->box.nnodes * D;
+                q->KC();
+                k_cgs_init<D><<<nblk(ndof, 256), 256, 0, st>>>(ndof, q->nown * D, q->fmask.p, q->g.p, q->dg.p, q->r.p,
+                                                               q->z.p, q->p.p, q->cs.p, q->xs.p, q->y.p, q->m.p, idt2,
+                                                               gb.partB.p + off * 3);
+                off += nblk(ndof, 256);
+            }
+            s0->KC();
+            k_cgs_start<<<1, 1, 0, st>>>(gb.cgs.p, gn, s->cg_rtol, s->fixed_iters);
+            OSMPM_LAUNCH_CHECK();
+            int done_it = 0;
+            while (done_it < s->max_cg) {
+                const int cnt = std::min(chunk, s->max_cg - done_it);
+                for (int c = 0; c < cnt; ++c) {
+                    int64_t hoff = 0;
+                    for (int i = 0; i < G.ns; ++i) {
+                        OSMPM_TRY(G.s[i]->launch_hvp(G.s[i]->z.p, G.s[i]->y.p, gb.partH.p + hoff));
+                        hoff += (int64_t)G.s[i]->box.ntiles * HVP_NW<D>;
+                    }
+                    if (pf.on) pf.begin("cg", st);
+                    OSMPM_TRY(halo_sum<D, R>(G, {{&Sub<D, R>::y, D}}));
+                    if (!remote) {
+                        s0->KC();
+                        k_cgs_scalar<<<1, 1024, 0, st>>>(gb.partB.p, (int)nbM, gb.partH.p, (int)nbH, gb.cgs.p);
+                    } else {
+                        s0->KC();
+                        k_cgs_local_sum<<<1, 1024, 0, st>>>(gb.partB.p, (int)nbM, gb.partH.p, (int)nbH, gb.cgs.p,
+                                                            gb.gsum.p);
+                        OSMPM_NCCL(ncclAllReduce(gb.gsum.p, gb.gsum.p, 3, ncclDouble, ncclSum, G.gc->comm, st));
+                        s0->KC();
+                        k_cgs_scalar_sum<<<1, 1, 0, st>>>(gb.gsum.p, gb.cgs.p);
+                    }
+                    off = 0;
+                    for (int i = 0; i < G.ns; ++i) {
+                        Sub<D, R>* q = G.s[i];
+                        const int64_t ndof = q->box.nnodes * D;
+                        q->KC();
+                        k_cgs_update<D><<<nblk(ndof, 256), 256, 0, st>>>(ndof, q->nown * D, q->fmask.p, q->dg.p, q->m.p,
+                                                                         idt2, q->z.p, q->y.p, q->p.p, q->cs.p,
+                                                                         q->xs.p, q->r.p, gb.cgs.p,
+                                                                         gb.partB.p + off * 3);
+                        off += nblk(ndof, 256);
+                    }
+                    if (pf.on) pf.end("cg", st);
+                    OSMPM_LAUNCH_CHECK();
+                }
+                done_it += cnt;
+                if (!s->fixed_iters) {
+                    OSMPM_CU(cudaMemcpyAsync(gb.h_cgs, gb.cgs.p, sizeof(CGScalars), cudaMemcpyDeviceToHost, st));
+                    OSMPM_CU(cudaStreamSynchronize(st));
+                    if (gb.h_cgs->done) break;
+                }
+            }
+        } else {
         // Jacobi PCG on H dx = -g (R6, R7)
         {
             int64_t off = 0;
@@ -381,7 +440,7 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
                     int64_t hoff = 0;
                     for (int i = 0; i < G.ns; ++i) {
                         OSMPM_TRY(G.s[i]->launch_hvp(G.s[i]->p.p, G.s[i]->y.p, gb.partH.p + hoff));
-                        hoff += G.s[i]->box.ntiles;
+                        hoff += (int64_t)G.s[i]->box.ntiles * HVP_NW<D>;
                     }
                 }
                 if (pf.on) pf.begin("cg", st);
@@ -438,6 +497,7 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
                 if (gb.h_cgs->done) break;
             }
         }
+        }  // standard PCG
         OSMPM_CU(cudaMemcpyAsync(gb.h_cgs, gb.cgs.p, sizeof(CGScalars), cudaMemcpyDeviceToHost, st));
         OSMPM_CU(cudaStreamSynchronize(st));
         sts->cg_iters += gb.h_cgs->it + (gb.h_cgs->done == 2 ? 1 : 0);

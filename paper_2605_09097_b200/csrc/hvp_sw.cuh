@@ -25,6 +25,9 @@
 
 namespace osmpm {
 
+// warps per HVP CTA (the per-warp curvature partials of k_hvp_sw)
+template <int D> constexpr int HVP_NW = (Tile<D>::NT + 31) / 32;
+
 template <int D, typename R> struct SWRec {
     // G row a starts at GROW(a): 3D fp64 rows padded to 4 reals (16-B aligned: one 16-B + one 8-B load
     // per row; the 30-real record has exactly the room), otherwise packed
@@ -271,9 +274,13 @@ __device__ __forceinline__ void sw_emit(int cellL, int a, int i, R* acc, R* stg)
 // included) is stored to the tile's own block of node values tb[tile-local node][component]; the node
 // pass k_det_gather then adds the <= 2^D tile blocks covering each node in a fixed tile order, so the
 // result does not depend on the order in which tiles finish (bitwise reproducible).
-template <int D, typename R>
+// With DOT, the flushing thread also accumulates d_node . (this tile's partial y_node) into dot: summed
+// over all tiles that is d^T K d, the PCG curvature (no separate pass over y), from d as staged in the
+// node tile (fp64) or re-read from global memory (fp32 tiles hold d rounded).
+template <int D, typename R, bool DOT>
 __device__ __forceinline__ void sw_flush(const BoxDev& b, const int* t, int plane, const R* stg,
-                                         double* __restrict__ out, double* __restrict__ tb = nullptr)
+                                         double* __restrict__ out, double* __restrict__ tb, const R* sv,
+                                         const double* __restrict__ din, double& dot)
 {
     using T = Tile<D>;
     for (int it = threadIdx.x; it < SW<D>::NITEM; it += T::NT) {
@@ -281,17 +288,27 @@ __device__ __forceinline__ void sw_flush(const BoxDev& b, const int* t, int plan
         R s = stg[it];
 #pragma unroll
         for (int k = 1; k < SW<D>::NSLOT; ++k) s += stg[k * SW<D>::NITEM + it];
+        const int a = it % D, nxy = it / D;
         if (tb) {
-            const int a = it % D, nxy = it / D;
             tb[((D == 3) ? nxy * T::N2 + plane : nxy * T::N1 + plane) * D + a] = (double)s;
-        } else if (s != R(0)) {
-            const int a = it % D, nxy = it / D;
+        }
+        if (s != R(0) && (tb == nullptr || DOT)) {
             int64_t g;
             if (D == 3)
                 g = box_node<D>(b, t[0] * T::T0 + nxy / T::N1, t[1] * T::T1 + nxy % T::N1, t[2] * T::T2 + plane);
             else
                 g = box_node<D>(b, t[0] * T::T0 + nxy, t[1] * T::T1 + plane, 0);
-            atomicAdd(&out[g * D + a], (double)s);
+            if (!tb) atomicAdd(&out[g * D + a], (double)s);
+            if constexpr (DOT) {
+                double dv;
+                if constexpr (sizeof(R) == 8) {
+                    const int ln = (D == 3) ? sw_node<D>(nxy / T::N1, nxy % T::N1, plane) : sw_node<D>(nxy, plane, 0);
+                    dv = (double)sv[sv_elem<D, R>(ln, a, SW<D>::NNP)];
+                } else {
+                    dv = din[g * D + a];
+                }
+                dot = fma(dv, (double)s, dot);
+            }
         }
     }
 }
@@ -408,9 +425,8 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
          const __grid_constant__ CUtensorMap tmc, int use_tmap, double* __restrict__ tbuf,
          double* __restrict__ pkp)
 {
-    // pkp (optional): per-CTA partial of d^T K d = sum_p G_p : gd_p, the curvature the PCG step length
-    // needs (sum_i d_i . (K d)_i = sum_i d_i . sum_p G_p grad N_ip = sum_p G_p : gd_p), so that PCG needs
-    // no separate pass over y
+    // pkp (optional): per-warp partials [tile][warp] of d^T K d = sum over tiles of d . (the tile's partial
+    // y), the curvature the PCG step length needs, accumulated by the plane flushes (sw_flush)
     using T = Tile<D>;
     using C = CL<D>;
     using In = HvpIn<D, R>;
@@ -462,10 +478,10 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
     __syncthreads();
     if (scs[0] == scs[T::NC]) {
         if constexpr (ASYNC) asm volatile("cp.async.wait_all;" ::: "memory");
-        if (pkp && threadIdx.x == 0) pkp[tile] = 0.0;
+        if (pkp && threadIdx.x < HVP_NW<D>) pkp[(int64_t)tile * HVP_NW<D> + threadIdx.x] = 0.0;
         return;
     }
-    double dkd = 0.0;  // this thread's particles' G_p : gd_p
+    double dkd = 0.0;  // this thread's flushed nodes' d . y_tile
     auto layer_empty = [&](int l) { return scs[l * T::LC] == scs[(l + 1) * T::LC]; };
     if constexpr (ASYNC)
         asm volatile("cp.async.wait_all;" ::: "memory");
@@ -553,12 +569,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                             }
                             Ga[bb] = fma(cc, s2, fma(ltr, A[a * D + bb], s1));
                         }
-                        if (pkp) {
-                            R q = R(0);
-#pragma unroll
-                            for (int bb = 0; bb < D; ++bb) q = fma(Ga[bb], gd[a * D + bb], q);
-                            dkd += (double)q;
-                        }
+
                         if constexpr (SR::GP == 4) {
                             using V2 = typename Vec2<R>::type;
                             V2 g01;
@@ -611,14 +622,22 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
         // node plane `layer` is complete: stage it, then sum the slots and RED
         if (it < T::ITEMS) sw_emit<D, R>(icell, icomp, ii, acc, stg);
         __syncthreads();
-        sw_flush<D, R>(b, t, layer, stg, yout, tbuf ? tbuf + (int64_t)tile * T::NN * D : nullptr);
+        if (pkp)
+            sw_flush<D, R, true>(b, t, layer, stg, yout, tbuf ? tbuf + (int64_t)tile * T::NN * D : nullptr, sv, din,
+                                 dkd);
+        else
+            sw_flush<D, R, false>(b, t, layer, stg, yout, tbuf ? tbuf + (int64_t)tile * T::NN * D : nullptr, sv, din,
+                                  dkd);
         // the next emit must not overwrite slots still being summed: a non-empty next layer has its
         // records barrier in between; otherwise synchronise here
         if (layer + 1 >= T::NL || layer_empty(layer + 1)) __syncthreads();
     }
     if (pkp) {
-        double v[1] = {dkd};
-        block_reduce_store<1>(v, pkp);
+        // warp partials, no CTA barrier (the last warp of a 144-thread CTA has 16 lanes)
+        const unsigned mask = __activemask();
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dkd += __shfl_xor_sync(mask, dkd, o);
+        if ((threadIdx.x & 31) == 0) pkp[(int64_t)tile * HVP_NW<D> + (threadIdx.x >> 5)] = dkd;
     }
 }
 

@@ -526,6 +526,137 @@ __global__ void k_cg_p(int64_t ndof, int64_t nown_dof, const uint8_t* __restrict
     block_reduce_store<1>(pm, partM);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Single-reduction Jacobi PCG (Chronopoulos & Gear; R22), one reduction per iteration:
+//   init      r = -g, u = diag^-1 r, x = p = s = 0, y = 0;  partials {r.u, r.r, u^T M u / dt^2}
+//   HVP(u)    y = K u; per-CTA partials u^T K u
+//   scalar    gamma = r.u, delta = u^T (K + M/dt^2) u, beta = gamma / gamma_old (0 first),
+//             c = delta - beta gamma / alpha_old (= p^T H p; delta first), c <= 0 -> stop, alpha = gamma / c
+//   update    p = u + beta p, s = (y + M u / dt^2) + beta s, x += alpha p, r -= alpha s, u = diag^-1 r,
+//             y = 0;  partials for the next iteration
+// (the oracle's pcg_single_reduction, same recurrences)
+// ---------------------------------------------------------------------------------------------
+template <int D>
+__global__ void k_cgs_init(int64_t ndof, int64_t nown_dof, const uint8_t* __restrict__ fm, const double* __restrict__ g,
+                           double* __restrict__ dg, double* __restrict__ r, double* __restrict__ u,
+                           double* __restrict__ p, double* __restrict__ sv, double* __restrict__ x,
+                           double* __restrict__ y, const double* __restrict__ m, double idt2,
+                           double* __restrict__ partials)
+{
+    double red[3] = {0.0, 0.0, 0.0};
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ndof; k += (int64_t)gridDim.x * blockDim.x) {
+        const bool f = fm[k];
+        if (!f) dg[k] = 1.0;
+        const double rk = f ? -g[k] : 0.0;
+        const double uk = rk / dg[k];
+        r[k] = rk;
+        u[k] = uk;
+        p[k] = 0.0;
+        sv[k] = 0.0;
+        x[k] = 0.0;
+        y[k] = 0.0;
+        if (f && k < nown_dof) {
+            red[0] += rk * uk;
+            red[1] += rk * rk;
+            red[2] += m[k / D] * idt2 * uk * uk;
+        }
+    }
+    block_reduce_store<3>(red, partials);
+}
+
+__global__ void k_cgs_start(CGScalars* s, double gn, double cg_rtol, int fixed)
+{
+    s->rz = s->rr = s->alpha = s->beta = s->pq = 0.0;
+    s->gn = gn;
+    s->tol2 = cg_rtol * cg_rtol * gn * gn;
+    s->it = 0;
+    s->negcurv_first = 0;
+    s->fixed = fixed;
+    s->done = 0;
+}
+__device__ __forceinline__ void cgs_scalar(double gamma, double rr, double delta, CGScalars* s)
+{
+    if (!s->fixed && rr <= s->tol2) {
+        s->done = 1;
+        return;
+    }
+    const double beta = (s->it == 0 || !(s->rz > 0.0)) ? 0.0 : gamma / s->rz;
+    const double c = (s->it == 0) ? delta : delta - beta * gamma / s->alpha;
+    s->pq = c;
+    if (!(c > 0.0)) {
+        if (s->it == 0) s->negcurv_first = 1;
+        s->done = 2;
+        return;
+    }
+    s->beta = beta;
+    s->alpha = gamma / c;
+    s->rz = gamma;
+    s->rr = rr;
+    s->it += 1;
+}
+// partB: 3 per block {r.u, r.r, u^T M u}; partH: u^T K u per HVP tile
+__global__ void k_cgs_scalar(const double* partB, int nb, const double* partH, int nh, CGScalars* s)
+{
+    if (s->done) return;
+    double v[3], w[1];
+    final_sum<3>(partB, nb, v);
+    __syncthreads();
+    final_sum<1>(partH, nh, w);
+    if (threadIdx.x == 0) cgs_scalar(v[0], v[1], v[2] + w[0], s);
+}
+// remote: sum this rank's partials -> out[0..2] = {r.u, r.r, u^T (K + M/dt^2) u} for the all-reduce
+__global__ void k_cgs_local_sum(const double* partB, int nb, const double* partH, int nh, const CGScalars* s,
+                                double* out)
+{
+    if (s->done) return;
+    double v[3], w[1];
+    final_sum<3>(partB, nb, v);
+    __syncthreads();
+    final_sum<1>(partH, nh, w);
+    if (threadIdx.x == 0) {
+        out[0] = v[0];
+        out[1] = v[1];
+        out[2] = v[2] + w[0];
+    }
+}
+__global__ void k_cgs_scalar_sum(const double* v, CGScalars* s)
+{
+    if (!s->done) cgs_scalar(v[0], v[1], v[2], s);
+}
+
+template <int D>
+__global__ void k_cgs_update(int64_t ndof, int64_t nown_dof, const uint8_t* __restrict__ fm, const double* __restrict__ dg,
+                             const double* __restrict__ m, double idt2, double* __restrict__ u, double* __restrict__ y,
+                             double* __restrict__ p, double* __restrict__ sv, double* __restrict__ x,
+                             double* __restrict__ r, const CGScalars* s, double* __restrict__ partials)
+{
+    if (s->done) return;
+    const double al = s->alpha, be = s->beta;
+    double red[3] = {0.0, 0.0, 0.0};
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ndof; k += (int64_t)gridDim.x * blockDim.x) {
+        if (fm[k]) {
+            const double mk = m[k / D] * idt2;
+            const double uk = u[k];
+            const double pk = uk + be * p[k];
+            const double sk = (y[k] + mk * uk) + be * sv[k];
+            const double rk = r[k] - al * sk;
+            const double un = rk / dg[k];
+            p[k] = pk;
+            sv[k] = sk;
+            x[k] += al * pk;
+            r[k] = rk;
+            u[k] = un;
+            if (k < nown_dof) {
+                red[0] += rk * un;
+                red[1] += rk * rk;
+                red[2] += mk * un * un;
+            }
+        }
+        y[k] = 0.0;
+    }
+    block_reduce_store<3>(red, partials);
+}
+
 // ut = u + alpha x on free DOFs
 __global__ void k_axpy_free(int64_t ndof, const uint8_t* __restrict__ fm, const double* __restrict__ u, double alpha,
                             const double* __restrict__ x, double* __restrict__ ut)

@@ -137,7 +137,7 @@ struct Sub : public osmpm_subdomain {
     BoxDev box{};
     bool have_grid = false, have_lin = false, have_vnew = false;
     DBuf<int> cell_start;
-    DBuf<double> m, mom, vn, fsig, mb, dval, u, g, dg, xs, r, z, p, y, ut, vnew, tmp;
+    DBuf<double> m, mom, vn, fsig, mb, dval, u, g, dg, xs, r, z, p, y, ut, vnew, tmp, cs;  // cs: s = H p (R22)
     DBuf<uint8_t> act, dmask, fmask;
     DirList dir_user, dir_cpl;
     DBuf<double> stage_io;  // persistent host-I/O staging buffer
@@ -487,7 +487,7 @@ struct Sub : public osmpm_subdomain {
         const size_t nn = box.nnodes, nd = nn * D;
         for (DBuf<double>* b : {&m, &mb})
             OSMPM_TRY(b->need(nn));
-        for (DBuf<double>* b : {&mom, &vn, &fsig, &dval, &u, &g, &dg, &xs, &r, &z, &p, &y, &ut, &vnew})
+        for (DBuf<double>* b : {&mom, &vn, &fsig, &dval, &u, &g, &dg, &xs, &r, &z, &p, &y, &ut, &vnew, &cs})
             OSMPM_TRY(b->need(nd));
         OSMPM_TRY(act.need(nn));
         OSMPM_TRY(dmask.need(nn));

@@ -25,7 +25,7 @@ def ctx():
     c.close()
 
 
-def oracle_step(fine, coarse, recv, pt):
+def oracle_step(fine, coarse, recv, pt, cg_variant=0):
     """One bench step on the oracle from particle state `pt`: returns (new particles, Pi values, stats)."""
     sc = synth.Scene(fine.grid, pt, fine.materials, fine.dt, fine.gravity)
     gs = oracle.p2g(sc)
@@ -37,7 +37,8 @@ def oracle_step(fine, coarse, recv, pt):
     dv = np.zeros((nn, 3))
     dm[recv] = 1
     dv[recv] = vS
-    u, st = oracle.implicit_solve(sc, gs, oracle.default_settings(max_newton=NEWTON, max_cg=CG, fixed_iters=1),
+    u, st = oracle.implicit_solve(sc, gs, oracle.default_settings(max_newton=NEWTON, max_cg=CG, fixed_iters=1,
+                                                                  cg_variant=cg_variant),
                                   dirichlet_mask=dm, dirichlet_v=dv)
     act = gs.active.astype(bool)
     return oracle.g2p(sc, np.where(act[:, None], u / fine.dt, 0.0)), vb, st
@@ -54,7 +55,7 @@ def gpu_setup(ctx, fine, coarse):
     return sub, csub
 
 
-def gpu_step(sub, csub, recv, restore):
+def gpu_step(sub, csub, recv, restore, cg_variant=0):
     from paper_2605_09097_b200 import osmpm
     if restore:
         sub.restore()
@@ -62,25 +63,26 @@ def gpu_step(sub, csub, recv, restore):
     vb = osmpm.transmit(sub, csub, osmpm.FINE_TO_COARSE, alpha=0.0, eps_tol=1e-12)
     vS = osmpm.transmit(csub, sub, osmpm.COARSE_TO_FINE, alpha=0.5, targets=recv)
     sub.set_dirichlet(recv, np.full(recv.shape[0], 7, np.uint8), vS)
-    st = sub.implicit_solve(osmpm.newton_settings(max_newton=NEWTON, max_cg=CG, fixed_iters=1))
+    st = sub.implicit_solve(osmpm.newton_settings(max_newton=NEWTON, max_cg=CG, fixed_iters=1, cg_variant=cg_variant))
     sub.g2p()
     sub.sync()
     return sub.read_particles(fields=("x", "v", "F")), vb, st
 
 
-def test_bench_recipe_25_restored_steps(ctx):
+@pytest.mark.parametrize("cg_variant", [0, 1])
+def test_bench_recipe_25_restored_steps(ctx, cg_variant):
     """25 consecutive bench steps (restore + sub-step) on a 16^3-cell C5 cube: every step completes,
     with no line-search failure, equals the oracle's step at 1e-9 (displacement, v, F - I) and Pi at
     1e-11, and all steps do the same work."""
     fine, coarse, recv = synth.c5_bench_workload(16, full_box=False)
     x0 = fine.particles.x.copy()
-    ref, vb_ref, st_ref = oracle_step(fine, coarse, recv, fine.particles)
+    ref, vb_ref, st_ref = oracle_step(fine, coarse, recv, fine.particles, cg_variant)
     assert st_ref.status == 0 and st_ref.ls_failures == 0 and st_ref.newton_iters == NEWTON
     sub, csub = gpu_setup(ctx, fine, coarse)
     sub.checkpoint()
     first = None
     for k in range(25):
-        out, vb, st = gpu_step(sub, csub, recv, restore=True)
+        out, vb, st = gpu_step(sub, csub, recv, restore=True, cg_variant=cg_variant)
         assert st.status == 0 and st.ls_failures == 0, (k, st.ls_failures)
         assert st.newton_iters == NEWTON and st.negcurv == st_ref.negcurv
         if st.negcurv == 0:

@@ -120,6 +120,27 @@ def test_implicit_solve_parity_fixed_iterations(ctx):
     assert rel_linf(v, np.where(act[:, None], u_ref / sc.dt, 0.0)) <= 1e-9
 
 
+@pytest.mark.parametrize("variant", [0, 1])
+def test_fixed_iteration_solve_parity_both_pcg_variants(ctx, variant):
+    """R22: standard and single-reduction PCG, each against the oracle running the same variant, fixed
+    3 x 20 and converged."""
+    from paper_2605_09097_b200 import osmpm
+    sc = synth.random_fixture(dim=3, cells=(5, 5, 4), seed=104)
+    ref = oracle.p2g(sc)
+    act = ref.active.astype(bool)
+    for kw, tol in ((dict(max_newton=3, max_cg=20, fixed_iters=1), 1e-9),
+                    (dict(newton_rtol=1e-12, cg_rtol=1e-12, max_cg=4000, max_newton=50), 1e-8)):
+        u_ref, st_ref = oracle.implicit_solve(sc, ref, oracle.default_settings(cg_variant=variant, **kw))
+        sub = make_sub(ctx, sc)
+        sub.p2g()
+        st = sub.implicit_solve(osmpm.newton_settings(cg_variant=variant, **kw))
+        assert st.status == 0 and st_ref.status == 0
+        if kw.get("fixed_iters"):
+            assert st.cg_iters == st_ref.cg_iters == 60
+        assert rel_linf(sub.read_grid_velocity(), np.where(act[:, None], u_ref / sc.dt, 0.0)) <= tol
+        sub.close()
+
+
 def test_fixed_mode_line_search_failure_parity(ctx):
     """R8 fixed-iteration policy on both sides: no trial accepted -> alpha = 0, counted, u unchanged."""
     from paper_2605_09097_b200 import osmpm

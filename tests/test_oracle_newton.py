@@ -295,3 +295,49 @@ def test_fixed_mode_negative_curvature_stops_pcg():
         assert s.negcurv >= 1 and s.cg_iters < 60
         if fixed:
             assert s.status == 0 and s.newton_iters == 2
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_single_reduction_pcg_matches_standard_pcg(dim):
+    """R22: the single-reduction PCG (Chronopoulos-Gear) produces the standard PCG's Krylov iterates
+    (identical in exact arithmetic): fixed 3 x 20 solves agree to round-off, converged solves to the
+    tolerance, and both report the same counts."""
+    sc = synth.random_fixture(dim=dim, seed=61, cells=(4, 3, 3) if dim == 3 else (7, 5, 1))
+    gs = oracle.p2g(sc)
+    u0, s0 = oracle.implicit_solve(sc, gs, oracle.default_settings(max_newton=3, max_cg=20, fixed_iters=1))
+    u1, s1 = oracle.implicit_solve(sc, gs, oracle.default_settings(max_newton=3, max_cg=20, fixed_iters=1,
+                                                                   cg_variant=1))
+    act = gs.active.astype(bool)
+    scale = np.abs(u0[act]).max()
+    assert np.abs(u1[act] - u0[act]).max() <= 1e-10 * scale
+    assert s1.cg_iters == s0.cg_iters == 60 and s1.newton_iters == 3
+    kw = dict(newton_rtol=1e-12, cg_rtol=1e-12, max_cg=4000)
+    uc0, c0 = oracle.implicit_solve(sc, gs, oracle.default_settings(**kw))
+    uc1, c1 = oracle.implicit_solve(sc, gs, oracle.default_settings(cg_variant=1, **kw))
+    assert c0.status == c1.status == 0
+    assert np.abs(uc1[act] - uc0[act]).max() <= 1e-9 * np.abs(uc0[act]).max()
+
+
+def test_single_reduction_pcg_special_cases():
+    """mu = lambda = 0: H = M / dt^2 is the Jacobi preconditioner itself, so one PCG iteration solves
+    the Newton system exactly (free fall: v^{n+1} = v^n + dt g) -- in both variants; the
+    indefinite tangent of test_fixed_mode_negative_curvature_stops_pcg stops both at the same point."""
+    sc = synth.random_fixture(dim=2, seed=62, cells=(5, 4, 1))
+    sc.materials = [(0.0, 0.3), (0.0, 0.3)]
+    sc.gravity = (0.3, -9.81, 0.0)
+    gs = oracle.p2g(sc)
+    u, s = oracle.implicit_solve(sc, gs, oracle.default_settings(cg_variant=1, newton_rtol=1e-13, cg_rtol=1e-14))
+    act = gs.active.astype(bool)
+    v = u[act] / sc.dt
+    np.testing.assert_allclose(v, gs.v[act] + sc.dt * np.array([0.3, -9.81]), rtol=0, atol=1e-12)
+    sc2 = synth.random_fixture(dim=2, seed=59, cells=(4, 4, 1), F_sigma=0.0)
+    sc2.particles.F[:] = np.diag([0.3, 0.3])
+    sc2.dt = 1.0
+    gs2 = oracle.p2g(sc2)
+    out = []
+    for var in (0, 1):
+        _, st = oracle.implicit_solve(sc2, gs2, oracle.default_settings(max_newton=2, max_cg=30, fixed_iters=1,
+                                                                        guess=1, cg_variant=var),
+                                      raise_on_error=False)
+        out.append((st.negcurv, st.cg_iters))
+    assert out[0] == out[1] and out[0][0] >= 1
