@@ -164,12 +164,17 @@ def transfer_rooflines(fam, n_particles, n_active_nodes, word, peak):
             plus material, flag and id: 9 B) per particle;
       p2g   read the sorted 26-word SoA per particle, write m, mv, f^sigma (7 fp64) per active node;
       g2p   read x, F (12 words) and write x, v, F, B (24 words) per particle, read v (3 fp64) per
-            active node."""
+            active node;
+      grad  SURVEY.md §8(d): 190 B (fp64) / 95 B (fp32) per particle per call (a4);
+      pi    read m, v (4 fp64) per active fine node and its activity flag per box node (a9; the coarse
+            accumulators are L2-resident)."""
     out = {}
     per_launch = {
         "sort": n_particles * (3 * word + 8 + 2 * (26 * word + 9)),
         "p2g": n_particles * 26 * word + n_active_nodes * 7 * 8,
         "g2p": n_particles * 36 * word + n_active_nodes * 3 * 8,
+        "grad": n_particles * (190 if word == 8 else 95),
+        "pi": n_active_nodes * 4 * 8 + int(n_active_nodes * 1.1),
     }
     s_n, s_ms = fam.get("sort", (0, 0.0))
     for k, by in per_launch.items():
@@ -382,7 +387,7 @@ def main():
     launches_timed = ctx.launch_count() - l0
     ms = e0.elapsed_time(e1) / args.steps
     hv_n, hv_ms = ctx.kernel_time("hvp")
-    fam = {f: ctx.kernel_time(f) for f in ("hvp", "grad", "energy", "p2g", "g2p", "sort", "cg", "transmit")}
+    fam = {f: ctx.kernel_time(f) for f in ("hvp", "grad", "energy", "p2g", "g2p", "sort", "cg", "pi", "interp")}
     ctx.profile(False)
     ms_max = max_over_ranks(dist, ms, dev)
 

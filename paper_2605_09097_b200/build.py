@@ -1,4 +1,5 @@
 """Builds libosmpm.so in-tree with nvcc for sm_100a (no JIT cache, no torch extension)."""
+import hashlib
 import os
 import subprocess
 
@@ -27,22 +28,40 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std
          "-L", os.path.join(NCCL, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(NCCL, "lib")]
 
 
-def _newest_source():
-    t = 0.0
+def source_hash():
+    """sha256 (first 16 hex digits) of every source the library is built from (csrc/, include/) and of
+    the compiler flags; embedded in the library (osmpm_version) and recorded beside it."""
+    h = hashlib.sha256()
     for d in (CSRC, os.path.join(ROOT, "include")):
-        for f in os.listdir(d):
-            t = max(t, os.path.getmtime(os.path.join(d, f)))
-    return t
+        for f in sorted(os.listdir(d)):
+            h.update(f.encode())
+            with open(os.path.join(d, f), "rb") as fh:
+                h.update(fh.read())
+    h.update(" ".join(FLAGS).encode())
+    return h.hexdigest()[:16]
+
+
+def built_hash():
+    try:
+        with open(OUT + ".srchash") as fh:
+            return fh.read().strip()
+    except OSError:
+        return None
 
 
 def build(force=False, verbose=False):
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= _newest_source():
+    """Rebuild unless the library on disk was built from exactly the current sources (hash check, not
+    timestamps: a snapshot copied to another machine keeps neither order nor mtimes)."""
+    hs = source_hash()
+    if not force and os.path.exists(OUT) and built_hash() == hs:
         return OUT
-    cmd = [NVCC, *FLAGS, *[os.path.join(CSRC, s) for s in SOURCES], "-o", OUT + ".tmp"]
+    cmd = [NVCC, *FLAGS, f"-DOSMPM_SRC_HASH=\"{hs}\"", *[os.path.join(CSRC, s) for s in SOURCES], "-o", OUT + ".tmp"]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)
     os.replace(OUT + ".tmp", OUT)
+    with open(OUT + ".srchash", "w") as fh:
+        fh.write(hs + "\n")
     return OUT
 
 

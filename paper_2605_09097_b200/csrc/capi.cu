@@ -91,7 +91,10 @@ using namespace osmpm;
 extern "C" {
 
 const char* osmpm_last_error(void) { return g_err.c_str(); }
-const char* osmpm_version(void) { return "osmpm 0.1 (sm_100a)"; }
+#ifndef OSMPM_SRC_HASH
+#define OSMPM_SRC_HASH "unknown"
+#endif
+const char* osmpm_version(void) { return "osmpm 0.2 (sm_100a) src " OSMPM_SRC_HASH; }
 
 osmpm_status osmpm_ctx_create(int device, void* cuda_stream, osmpm_ctx** out)
 {
@@ -433,9 +436,8 @@ osmpm_status osmpm_coupler_create(osmpm_subdomain* coarse, osmpm_subdomain* fine
     CHECK_ARG(coarse && fine && settings && out, "NULL argument");
     CHECK_ARG(coarse->dim == fine->dim && coarse->prec == fine->prec, "coupler: subdomains differ in dim / precision");
     CHECK_ARG(coarse->ctx == fine->ctx, "coupler: subdomains belong to different contexts");
-    CHECK_ARG(!coarse->decomposed && !fine->decomposed,
-              "coupler: slab-decomposed subdomains are driven by the caller (osmpm_transmit / osmpm_implicit_solve), "
-              "not by the coupler");
+    CHECK_ARG(!coarse->decomposed, "coupler: the coarse subdomain must not be decomposed (create it with "
+                                   "decompose = 0: it is replicated on every rank)");
     CHECK_ARG(settings->M >= 1, "M must be >= 1");
     CHECK_ARG(settings->k_max >= 1 || settings->parity_fixed_k >= 1, "k_max and parity_fixed_k both < 1: no Schwarz iteration");
     SET_DEVICE(coarse->ctx);

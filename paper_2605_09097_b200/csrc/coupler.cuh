@@ -8,6 +8,9 @@
 #include <cmath>
 #include <vector>
 
+#include <map>
+
+#include "dist.cuh"
 #include "transmit.cuh"
 
 struct osmpm_coupler {
@@ -32,15 +35,25 @@ __global__ void k_lerp(int64_t n, const double* __restrict__ a, const double* __
 
 template <int D, typename R>
 struct Coupler : public osmpm_coupler {
-    Sub<D, R>* B = nullptr;
-    Sub<D, R>* S = nullptr;
-    std::vector<int64_t> recvB, recvS;           // receivers (dense node indices, ascending)
+    Sub<D, R>* B = nullptr;   // coarse subdomain: never decomposed (replicated on every rank)
+    Sub<D, R>* Ss = nullptr;  // fine subdomain, whole ...
+    Dist<D, R>* Sd = nullptr; // ... or slab-decomposed (over this rank's local slabs and the ranks)
+    std::vector<int64_t> recvB, recvS;           // receivers (dense node indices, ascending); recvS: this
+    std::vector<char> ownS;                      // rank's slab boxes (owned + ghost planes), ownS: owned
     DBuf<int64_t> dB, dS;
-    DBuf<uint8_t> maskB, maskS;
-    DBuf<double> vGB, vGBnew, vSn, vSnp1, vSprev, vbc, num, den;
+    DBuf<uint8_t> maskB, maskS, flagsB;
+    DBuf<double> vGB, vGBnew, vSn, vSnp1, vSprev, vbc, num, red2;
     bool prepared = false;
     double eps_tol = 0.0;
     cudaStream_t st() const { return B->st(); }
+    SlabGroup<D, R> FG() { return Sd ? Sd->group() : Ss->self_group(); }
+    bool multi() { return Sd && Sd->gc && Sd->gc->multi(); }
+    GridGeo fine_geo() const { return Sd ? geo_of(Sd) : geo_of(Ss); }
+    const int64_t* fine_gdims() const { return Sd ? Sd->gdims : Ss->gdims; }
+    double fine_median_mass() { return FG().s[0]->median_mass; }
+    double fine_total_mass() const { return Sd ? Sd->total_mass : Ss->total_mass; }
+    double fine_dx() const { return Sd ? Sd->dx : Ss->dx; }
+    const double* fine_origin() const { return Sd ? Sd->origin : Ss->origin; }
 
     // ------------------------------------------------------------------------------------------
     // host helpers
@@ -101,107 +114,144 @@ struct Coupler : public osmpm_coupler {
 
     // ------------------------------------------------------------------------------------------
     // Step 0: store, P2G both, Gamma, arbitration, receivers, v_GammaB^(0)
+    //
+    // A decomposed fine subdomain: every slab evaluates Gamma_S and the arbitration on ALL nodes of its
+    // box (owned and ghost planes: their m, m^∂ and activity are consistent after the halo sums, so a
+    // ghost node takes exactly its owner's decision, and this rank's Dirichlet data cover its ghosts);
+    // the coarse nodes a fine donor takes over are OR-ed over the ranks (all-reduce max) and the coarse
+    // Gamma_B is rank 0's (broadcast; the replicated coarse subdomain runs deterministically).
     // ------------------------------------------------------------------------------------------
     osmpm_status prepare() override
     {
-        OSMPM_TRY(S->checkpoint());
+        SlabGroup<D, R> G = FG();
+        OSMPM_TRY(fine->checkpoint());
         OSMPM_TRY(B->p2g());
-        OSMPM_TRY(S->p2g());
+        OSMPM_TRY(fine->p2g());
         OSMPM_TRY(B->boundary_mass());
-        OSMPM_TRY(S->boundary_mass());
+        for (int i = 0; i < G.ns; ++i) OSMPM_TRY(G.s[i]->boundary_mass());
+        OSMPM_TRY(halo_sum<D, R>(G, {{&Sub<D, R>::mb, 1}}));
         // Pi denominator of the step-0 fine grid (eligibility of coarse receivers, R13)
-        OSMPM_TRY(project_accumulate(S, B, false, num, den));
-        std::vector<double> mB, mbB, mS, mbS, denB;
-        std::vector<uint8_t> aB, aS;
+        const int64_t nnB = B->dense_nodes();
+        OSMPM_TRY(num.need((size_t)nnB * (D + 1)));
+        OSMPM_TRY(project_accumulate_group<D, R>(G, B, false, num.p));
+        std::vector<double> mB, mbB, denB;
+        std::vector<uint8_t> aB;
         OSMPM_TRY(d2h(mB, B->m.p, B->box.nnodes, st()));
         OSMPM_TRY(d2h(mbB, B->mb.p, B->box.nnodes, st()));
         OSMPM_TRY(d2h(aB, B->act.p, B->box.nnodes, st()));
-        OSMPM_TRY(d2h(mS, S->m.p, S->box.nnodes, st()));
-        OSMPM_TRY(d2h(mbS, S->mb.p, S->box.nnodes, st()));
-        OSMPM_TRY(d2h(aS, S->act.p, S->box.nnodes, st()));
-        OSMPM_TRY(d2h(denB, den.p, B->dense_nodes(), st()));
+        OSMPM_TRY(d2h(denB, num.p + nnB * D, nnB, st()));
         OSMPM_CU(cudaStreamSynchronize(st()));
-        const double tauB = set.tau_gamma_rel * B->median_mass, tauS = set.tau_gamma_rel * S->median_mass;
-        // Gamma_alpha = {active i : m^b_i > tau} (Eq. boundary_grid_set), as dense index -> box index
-        std::vector<char> hatB(B->box.nnodes, 0);
+        const double tauB = set.tau_gamma_rel * B->median_mass, tauS = set.tau_gamma_rel * fine_median_mass();
+        // Gamma_B = {active I : m^b_I > tau} (Eq. boundary_grid_set), coarse box indices
+        std::vector<uint8_t> hatB(B->box.nnodes, 0), dropB(B->box.nnodes, 0);
         for (int64_t i = 0; i < B->box.nnodes; ++i) hatB[i] = aB[i] && mbB[i] > tauB;
-        std::vector<int64_t> gS;  // fine Gamma (box indices)
-        for (int64_t i = 0; i < S->box.nnodes; ++i)
-            if (aS[i] && mbS[i] > tauS) gS.push_back(i);
-        std::vector<char> hatS_keep(gS.size(), 1);
-        const double tol = 1e-9 * std::min(B->dx, S->dx);
-        for (size_t q = 0; q < gS.size(); ++q) {
-            int64_t k[3];
-            if (dense_of_box(S, gS[q], k) < 0) continue;
-            int64_t kk[3] = {0, 0, 0};
-            bool coincide = true;
-            for (int a = 0; a < D; ++a) {
-                const double x = S->origin[a] + S->dx * (double)k[a];
-                const double X = (x - B->origin[a]) / B->dx;
-                kk[a] = (int64_t)std::llround(X);
-                if (std::fabs(X - (double)kk[a]) * B->dx > tol || kk[a] < 0 || kk[a] >= B->gdims[a]) coincide = false;
-            }
-            if (!coincide) continue;
-            const int64_t gI = (D == 3) ? (kk[0] * B->gdims[1] + kk[1]) * B->gdims[2] + kk[2] : kk[0] * B->gdims[1] + kk[1];
-            const int64_t I = box_of(B, gI);
-            if (I < 0 || !hatB[I]) continue;
-            // ambiguous overlap node (Eq. overlap_donor): donor = larger nodal mass, ties -> B
-            if (mB[I] >= mS[gS[q]])
-                hatB[I] = 0;       // B donates: S receives
-            else
-                hatS_keep[q] = 0;  // S donates: B receives
+        if (multi()) {
+            OSMPM_TRY(flagsB.need(std::max<int64_t>(B->box.nnodes, 1)));
+            OSMPM_CU(cudaMemcpyAsync(flagsB.p, hatB.data(), B->box.nnodes, cudaMemcpyHostToDevice, st()));
+            OSMPM_NCCL(ncclBroadcast(flagsB.p, flagsB.p, B->box.nnodes, ncclUint8, 0, Sd->gc->comm, st()));
+            OSMPM_CU(cudaMemcpyAsync(hatB.data(), flagsB.p, B->box.nnodes, cudaMemcpyDeviceToHost, st()));
+            OSMPM_CU(cudaStreamSynchronize(st()));
         }
-        // coarse receivers need fine support (R13)
+        // fine Gamma_S candidates on every local slab's whole box (dense index -> owned?)
+        const double tol = 1e-9 * std::min(B->dx, fine_dx());
+        std::map<int64_t, char> candS;  // dense index -> owned by this rank
+        for (int si = 0; si < G.ns; ++si) {
+            Sub<D, R>* S = G.s[si];
+            std::vector<double> mS, mbS;
+            std::vector<uint8_t> aS;
+            OSMPM_TRY(d2h(mS, S->m.p, S->box.nnodes, st()));
+            OSMPM_TRY(d2h(mbS, S->mb.p, S->box.nnodes, st()));
+            OSMPM_TRY(d2h(aS, S->act.p, S->box.nnodes, st()));
+            OSMPM_CU(cudaStreamSynchronize(st()));
+            for (int64_t i = 0; i < S->box.nnodes; ++i) {
+                if (!(aS[i] && mbS[i] > tauS)) continue;
+                int64_t k[3];
+                const int64_t g = dense_of_box(S, i, k);
+                if (g < 0) continue;
+                const bool owned = i < S->nown;
+                // coincident coarse node?  ambiguous overlap node (Eq. overlap_donor): donor = larger nodal
+                // mass, ties -> B
+                bool keep = true;
+                int64_t kk[3] = {0, 0, 0};
+                bool coincide = true;
+                for (int a = 0; a < D; ++a) {
+                    const double x = S->origin[a] + S->dx * (double)k[a];
+                    const double X = (x - B->origin[a]) / B->dx;
+                    kk[a] = (int64_t)std::llround(X);
+                    if (std::fabs(X - (double)kk[a]) * B->dx > tol || kk[a] < 0 || kk[a] >= B->gdims[a]) coincide = false;
+                }
+                if (coincide) {
+                    const int64_t gI =
+                        (D == 3) ? (kk[0] * B->gdims[1] + kk[1]) * B->gdims[2] + kk[2] : kk[0] * B->gdims[1] + kk[1];
+                    const int64_t I = box_of(B, gI);
+                    if (I >= 0 && hatB[I]) {
+                        if (mB[I] >= mS[i])
+                            dropB[I] = 1;  // B donates: S receives
+                        else
+                            keep = false;  // S donates: B receives
+                    }
+                }
+                if (!keep) continue;
+                // fine receivers need an active coarse stencil (R13)
+                double f[3];
+                int64_t base[3] = {0, 0, 0};
+                for (int a = 0; a < D; ++a) {
+                    const double x = S->origin[a] + S->dx * (double)k[a];
+                    const double X = (x - B->origin[a]) / B->dx;
+                    base[a] = (int64_t)std::floor(X - 0.5);
+                    f[a] = X - (double)base[a];
+                }
+                bool ok = true;
+                for (int o0 = 0; o0 < 3 && ok; ++o0)
+                    for (int o1 = 0; o1 < 3 && ok; ++o1)
+                        for (int o2 = 0; o2 < (D == 3 ? 3 : 1) && ok; ++o2) {
+                            const int off[3] = {o0, o1, o2};
+                            double w = 1.0;
+                            for (int a = 0; a < D; ++a) w *= bsw(f[a], off[a]);
+                            if (!(w > 0.0)) continue;
+                            int64_t kc[3] = {0, 0, 0};
+                            for (int a = 0; a < D; ++a) {
+                                kc[a] = base[a] + off[a];
+                                if (kc[a] < 0 || kc[a] >= B->gdims[a]) ok = false;
+                            }
+                            if (!ok) break;
+                            const int64_t gI = (D == 3) ? (kc[0] * B->gdims[1] + kc[1]) * B->gdims[2] + kc[2]
+                                                        : kc[0] * B->gdims[1] + kc[1];
+                            const int64_t I = box_of(B, gI);
+                            if (I < 0 || !aB[I]) ok = false;
+                        }
+                if (!ok) continue;
+                char& o = candS[g];  // a node seen by two local slabs: owned if either owns it
+                o = (char)(o || owned);
+            }
+        }
+        if (multi()) {
+            OSMPM_CU(cudaMemcpyAsync(flagsB.p, dropB.data(), B->box.nnodes, cudaMemcpyHostToDevice, st()));
+            OSMPM_NCCL(ncclAllReduce(flagsB.p, flagsB.p, B->box.nnodes, ncclUint8, ncclMax, Sd->gc->comm, st()));
+            OSMPM_CU(cudaMemcpyAsync(dropB.data(), flagsB.p, B->box.nnodes, cudaMemcpyDeviceToHost, st()));
+            OSMPM_CU(cudaStreamSynchronize(st()));
+        }
+        recvS.clear();
+        ownS.clear();
+        for (auto& kv : candS) {
+            recvS.push_back(kv.first);
+            ownS.push_back(kv.second);
+        }
+        // coarse receivers: Gamma_B minus the nodes a fine donor took, with fine support (R13)
         recvB.clear();
         for (int64_t i = 0; i < B->box.nnodes; ++i) {
-            if (!hatB[i]) continue;
+            if (!hatB[i] || dropB[i]) continue;
             int64_t k[3];
             const int64_t g = dense_of_box(B, i, k);
             if (g >= 0 && denB[g] > tauB) recvB.push_back(g);
         }
         std::sort(recvB.begin(), recvB.end());
-        // fine receivers need an active coarse stencil (R13)
-        recvS.clear();
-        for (size_t q = 0; q < gS.size(); ++q) {
-            if (!hatS_keep[q]) continue;
-            int64_t k[3];
-            const int64_t g = dense_of_box(S, gS[q], k);
-            if (g < 0) continue;
-            double f[3];
-            int64_t base[3] = {0, 0, 0};
-            for (int a = 0; a < D; ++a) {
-                const double x = S->origin[a] + S->dx * (double)k[a];
-                const double X = (x - B->origin[a]) / B->dx;
-                base[a] = (int64_t)std::floor(X - 0.5);
-                f[a] = X - (double)base[a];
-            }
-            bool ok = true;
-            for (int o0 = 0; o0 < 3 && ok; ++o0)
-                for (int o1 = 0; o1 < 3 && ok; ++o1)
-                    for (int o2 = 0; o2 < (D == 3 ? 3 : 1) && ok; ++o2) {
-                        const int off[3] = {o0, o1, o2};
-                        double w = 1.0;
-                        for (int a = 0; a < D; ++a) w *= bsw(f[a], off[a]);
-                        if (!(w > 0.0)) continue;
-                        int64_t kk[3] = {0, 0, 0};
-                        for (int a = 0; a < D; ++a) {
-                            kk[a] = base[a] + off[a];
-                            if (kk[a] < 0 || kk[a] >= B->gdims[a]) ok = false;
-                        }
-                        if (!ok) break;
-                        const int64_t gI =
-                            (D == 3) ? (kk[0] * B->gdims[1] + kk[1]) * B->gdims[2] + kk[2] : kk[0] * B->gdims[1] + kk[1];
-                        const int64_t I = box_of(B, gI);
-                        if (I < 0 || !aB[I]) ok = false;
-                    }
-            if (ok) recvS.push_back(g);
-        }
-        std::sort(recvS.begin(), recvS.end());
         const int64_t nB = recvB.size(), nS = recvS.size();
         OSMPM_TRY(dB.need(std::max<int64_t>(nB, 1)));
         OSMPM_TRY(dS.need(std::max<int64_t>(nS, 1)));
         OSMPM_TRY(maskB.need(std::max<int64_t>(nB, 1)));
         OSMPM_TRY(maskS.need(std::max<int64_t>(nS, 1)));
+        OSMPM_TRY(red2.need(4));
         for (DBuf<double>* bb : {&vGB, &vGBnew})
             OSMPM_TRY(bb->need(std::max<int64_t>(nB, 1) * D));
         for (DBuf<double>* bb : {&vSn, &vSnp1, &vSprev, &vbc})
@@ -211,14 +261,14 @@ struct Coupler : public osmpm_coupler {
         OSMPM_CU(cudaMemsetAsync(maskB.p, (1 << D) - 1, std::max<int64_t>(nB, 1), st()));
         OSMPM_CU(cudaMemsetAsync(maskS.p, (1 << D) - 1, std::max<int64_t>(nS, 1), st()));
         // v_GammaB^(0) = Pi(v_S^n) on the coarse receivers (R16)
-        eps_tol = set.eps_tol >= 0 ? set.eps_tol : 1e-12 * S->total_mass;
+        eps_tol = set.eps_tol >= 0 ? set.eps_tol : 1e-12 * fine_total_mass();
         if (nB) {
-            OSMPM_TRY(project_out<D, R>(st(), B, nB, dB.p, num.p, den.p, eps_tol, vGB.p));
+            OSMPM_TRY(project_out<D, R>(st(), B, nB, dB.p, num.p, num.p + nnB * D, eps_tol, vGB.p));
         }
         // v_GammaS^(0) = I(v_B^n) (R15: r_S at k = 0 compares I(v_B^(1)) with I(v_B^n))
         if (nS) {
             B->KC();
-            k_interp<D><<<nblk_all(nS, 256), 256, 0, st()>>>(nS, dS.p, geo_of(S), B->box, B->vn.p, nullptr, 0.0,
+            k_interp<D><<<nblk_all(nS, 256), 256, 0, st()>>>(nS, dS.p, fine_geo(), B->box, B->vn.p, nullptr, 0.0,
                                                              vSprev.p, B->err.p);
             OSMPM_LAUNCH_CHECK();
         }
@@ -235,10 +285,10 @@ struct Coupler : public osmpm_coupler {
         const int64_t nS = recvS.size();
         if (!nS) return OSMPM_OK;
         B->KC();
-        k_interp<D><<<nblk_all(nS, 256), 256, 0, st()>>>(nS, dS.p, geo_of(S), B->box, B->vn.p, nullptr, 0.0, vSn.p,
+        k_interp<D><<<nblk_all(nS, 256), 256, 0, st()>>>(nS, dS.p, fine_geo(), B->box, B->vn.p, nullptr, 0.0, vSn.p,
                                                          B->err.p);
         B->KC();
-        k_interp<D><<<nblk_all(nS, 256), 256, 0, st()>>>(nS, dS.p, geo_of(S), B->box, B->vnew.p, nullptr, 0.0,
+        k_interp<D><<<nblk_all(nS, 256), 256, 0, st()>>>(nS, dS.p, fine_geo(), B->box, B->vnew.p, nullptr, 0.0,
                                                          vSnp1.p, B->err.p);
         OSMPM_LAUNCH_CHECK();
         return OSMPM_OK;
@@ -262,7 +312,10 @@ struct Coupler : public osmpm_coupler {
             }
             OSMPM_TRY(endpoints());
         }
-        if (!S->have_grid) OSMPM_TRY(S->p2g());
+        SlabGroup<D, R> G = FG();
+        bool grid = true;
+        for (int i = 0; i < G.ns; ++i) grid = grid && G.s[i]->have_grid;
+        if (!grid) OSMPM_TRY(fine->p2g());
         const int64_t nS = recvS.size();
         const double alpha = (double)m / (double)set.M;  // Eq. temporal_interp
         if (nS) {
@@ -270,28 +323,36 @@ struct Coupler : public osmpm_coupler {
             k_lerp<<<nblk_all(nS * D, 256), 256, 0, st()>>>(nS * D, vSn.p, vSnp1.p, alpha, vbc.p);
             OSMPM_LAUNCH_CHECK();
         }
-        OSMPM_TRY(S->set_dirlist(S->dir_cpl, nS, dS.p, maskS.p, vbc.p, OSMPM_DEVICE));
-        OSMPM_TRY(S->implicit_solve(&set.fine, stats));
+        // every local slab gets this rank's receiver list (each keeps the nodes of its own box)
+        for (int i = 0; i < G.ns; ++i)
+            OSMPM_TRY(G.s[i]->set_dirlist(G.s[i]->dir_cpl, nS, dS.p, maskS.p, vbc.p, OSMPM_DEVICE));
+        OSMPM_TRY(fine->implicit_solve(&set.fine, stats));
         if (m == set.M) {
             // v_GammaB^(k+1) = Pi(last sub-step's solved fine velocities) (R16)
-            OSMPM_TRY(project_accumulate(S, B, true, num, den));
+            const int64_t nnB = B->dense_nodes();
+            OSMPM_TRY(num.need((size_t)nnB * (D + 1)));
+            OSMPM_TRY(project_accumulate_group<D, R>(G, B, true, num.p));
             const int64_t nB = recvB.size();
             if (nB) {
-                OSMPM_TRY(project_out<D, R>(st(), B, nB, dB.p, num.p, den.p, eps_tol, vGBnew.p));
+                OSMPM_TRY(project_out<D, R>(st(), B, nB, dB.p, num.p, num.p + nnB * D, eps_tol, vGBnew.p));
             }
         }
-        return S->g2p();
+        return fine->g2p();
     }
 
-    static double rel_change(const std::vector<double>& nw, const std::vector<double>& old)
+    static void rel_parts(const std::vector<double>& nw, const std::vector<double>& old, const std::vector<char>* own,
+                          double* num2, double* den2)
     {
         double a = 0.0, b = 0.0;
         for (size_t i = 0; i < nw.size(); ++i) {
+            if (own && !(*own)[i / D]) continue;
             a += (nw[i] - old[i]) * (nw[i] - old[i]);
             b += nw[i] * nw[i];
         }
-        return b > 0.0 ? std::sqrt(a / b) : std::sqrt(a);
+        *num2 = a;
+        *den2 = b;
     }
+    static double rel_of(double a, double b) { return b > 0.0 ? std::sqrt(a / b) : std::sqrt(a); }
 
     osmpm_status step(osmpm_schwarz_report* rep) override
     {
@@ -299,9 +360,19 @@ struct Coupler : public osmpm_coupler {
         osmpm_schwarz_report* RP = rep ? rep : &local;
         std::memset(RP, 0, sizeof(*RP));
         OSMPM_TRY(prepare());
-        RP->n_recv_B = (int)recvB.size();
-        RP->n_recv_S = (int)recvS.size();
         const int64_t nB = recvB.size(), nS = recvS.size();
+        RP->n_recv_B = (int)nB;
+        int64_t nS_own = 0;
+        for (char o : ownS) nS_own += o ? 1 : 0;
+        if (multi()) {
+            double v = (double)nS_own;
+            OSMPM_CU(cudaMemcpyAsync(red2.p, &v, sizeof(double), cudaMemcpyHostToDevice, st()));
+            OSMPM_NCCL(ncclAllReduce(red2.p, red2.p, 1, ncclDouble, ncclSum, Sd->gc->comm, st()));
+            OSMPM_CU(cudaMemcpyAsync(&v, red2.p, sizeof(double), cudaMemcpyDeviceToHost, st()));
+            OSMPM_CU(cudaStreamSynchronize(st()));
+            nS_own = (int64_t)v;
+        }
+        RP->n_recv_S = (int)nS_own;
         const int n_iter = set.parity_fixed_k > 0 ? set.parity_fixed_k : set.k_max;
         std::vector<double> hGB, hGBnew, hSnp1, hSprev;
         for (int k = 0; k < n_iter; ++k) {
@@ -310,19 +381,32 @@ struct Coupler : public osmpm_coupler {
             OSMPM_TRY(B->set_dirlist(B->dir_cpl, nB, dB.p, maskB.p, vGB.p, OSMPM_DEVICE));
             OSMPM_TRY(B->implicit_solve(&set.coarse, nullptr));
             // Step 2: restore the fine particles (Alg. 1) and sub-cycle
-            OSMPM_TRY(S->restore());
-            OSMPM_TRY(S->p2g());
+            OSMPM_TRY(fine->restore());
+            OSMPM_TRY(fine->p2g());
             for (int m = 1; m <= set.M; ++m) {
                 OSMPM_TRY(substep(m, nullptr));
                 RP->fine_substeps++;
             }
-            // Step 3: interface residuals (Eqs. convergence_residuals / criterion)
+            // Step 3: interface residuals (Eqs. convergence_residuals / criterion); r_S over this rank's
+            // owned receivers, summed over the ranks
             OSMPM_TRY(d2h(hGB, vGB.p, nB * D, st()));
             OSMPM_TRY(d2h(hGBnew, vGBnew.p, nB * D, st()));
             OSMPM_TRY(d2h(hSnp1, vSnp1.p, nS * D, st()));
             OSMPM_TRY(d2h(hSprev, vSprev.p, nS * D, st()));
             OSMPM_CU(cudaStreamSynchronize(st()));
-            const double rB = rel_change(hGBnew, hGB), rS = rel_change(hSnp1, hSprev);
+            double bn, bd, sn, sd;
+            rel_parts(hGBnew, hGB, nullptr, &bn, &bd);
+            rel_parts(hSnp1, hSprev, &ownS, &sn, &sd);
+            if (multi()) {
+                double v[2] = {sn, sd};
+                OSMPM_CU(cudaMemcpyAsync(red2.p, v, 2 * sizeof(double), cudaMemcpyHostToDevice, st()));
+                OSMPM_NCCL(ncclAllReduce(red2.p, red2.p, 2, ncclDouble, ncclSum, Sd->gc->comm, st()));
+                OSMPM_CU(cudaMemcpyAsync(v, red2.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st()));
+                OSMPM_CU(cudaStreamSynchronize(st()));
+                sn = v[0];
+                sd = v[1];
+            }
+            const double rB = rel_of(bn, bd), rS = rel_of(sn, sd);
             if (k < 256) {
                 RP->r_B[k] = rB;
                 RP->r_S[k] = rS;
@@ -339,9 +423,12 @@ struct Coupler : public osmpm_coupler {
         // Step 4: post-convergence coarse G2P + advection with v_B^(k*+1)
         OSMPM_TRY(B->g2p());
         OSMPM_TRY(B->sync());
-        OSMPM_TRY(S->sync());
+        OSMPM_TRY(fine->sync());
         B->dir_cpl.n = 0;
-        S->dir_cpl.n = 0;
+        {
+            SlabGroup<D, R> G = FG();
+            for (int i = 0; i < G.ns; ++i) G.s[i]->dir_cpl.n = 0;
+        }
         prepared = false;
         if (!RP->converged && set.parity_fixed_k <= 0) {
             set_error("Schwarz iteration did not converge in k_max = %d iterations (r_B = %g, r_S = %g)", set.k_max,
@@ -360,7 +447,10 @@ inline osmpm_status coupler_create(osmpm_subdomain* coarse, osmpm_subdomain* fin
     {                                                                                               \
         auto* q = new Coupler<DD, RR>();                                                            \
         q->B = static_cast<Sub<DD, RR>*>(coarse);                                                   \
-        q->S = static_cast<Sub<DD, RR>*>(fine);                                                     \
+        if (fine->decomposed)                                                                       \
+            q->Sd = static_cast<Dist<DD, RR>*>(fine);                                               \
+        else                                                                                        \
+            q->Ss = static_cast<Sub<DD, RR>*>(fine);                                                \
         c = q;                                                                                      \
     }
     if (coarse->dim == 3 && coarse->prec == OSMPM_F64) MK(3, double)
@@ -370,6 +460,14 @@ inline osmpm_status coupler_create(osmpm_subdomain* coarse, osmpm_subdomain* fin
 #undef MK
     c->coarse = coarse;
     c->fine = fine;
+    // a decomposed fine subdomain over several ranks: the replicated coarse subdomain runs in the
+    // deterministic scatter mode so that every rank's coarse solve is bitwise the same
+    if (fine->decomposed && fine->ctx->gc.multi()) {
+        if (coarse->dim == 3 && coarse->prec == OSMPM_F64) static_cast<Sub<3, double>*>(coarse)->det_force = true;
+        else if (coarse->dim == 2 && coarse->prec == OSMPM_F64) static_cast<Sub<2, double>*>(coarse)->det_force = true;
+        else if (coarse->dim == 3) static_cast<Sub<3, float>*>(coarse)->det_force = true;
+        else static_cast<Sub<2, float>*>(coarse)->det_force = true;
+    }
     c->set = *s;
     *out = c;
     return OSMPM_OK;

@@ -181,6 +181,7 @@ __device__ __forceinline__ void final_sum(const double* partials, int nb, double
     double v[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) v[k] = 0.0;
+#pragma unroll 4
     for (int i = threadIdx.x; i < nb; i += blockDim.x)
 #pragma unroll
         for (int k = 0; k < NV; ++k) v[k] += partials[(int64_t)i * NV + k];

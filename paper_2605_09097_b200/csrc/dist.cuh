@@ -111,6 +111,7 @@ struct Dist : public osmpm_subdomain {
     double origin[3] = {0, 0, 0}, dx = 1;
     int64_t gdims[3] = {1, 1, 1};
     int64_t n_total = 0;
+    double total_mass = 0.0;  // of the whole subdomain (every rank sees the full view)
     DBuf<double> dense_io;          // dense node / creation-order particle staging
     DBuf<unsigned char> mig_recv[2];  // migration payload from the left / right rank
     DBuf<unsigned long long> mig_cnt;
@@ -169,6 +170,8 @@ struct Dist : public osmpm_subdomain {
                 OSMPM_CU(cudaMemcpy(ms.data(), pv->m, ms.size() * sizeof(double), cudaMemcpyDeviceToHost));
             std::sort(ms.begin(), ms.end());
             med = (pv->n % 2) ? ms[pv->n / 2] : 0.5 * (ms[pv->n / 2 - 1] + ms[pv->n / 2]);
+            total_mass = 0.0;
+            for (double mm : ms) total_mass += mm;
         }
         for (int k = 0; k < L_; ++k) {
             const int gs = first_slab + k;

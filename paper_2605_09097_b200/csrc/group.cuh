@@ -280,7 +280,7 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
     OSMPM_TRY(gb.partB.need((size_t)std::max<int64_t>(std::max(nbn_tot, nbd_tot), 1) * 4));
     // PCG curvature partials: p^T M p per node-vector block (k_cg_init / k_cg_p), p^T K p per HVP tile
     int64_t nbH = 0;
-    for (int i = 0; i < G.ns; ++i) nbH += (int64_t)G.s[i]->box.ntiles * HVP_NW<D>;
+    for (int i = 0; i < G.ns; ++i) nbH += G.s[i]->box.ntiles;
     const int64_t nbM = nbd_tot;
     OSMPM_TRY(gb.partM.need((size_t)std::max<int64_t>(nbM, 1)));
     OSMPM_TRY(gb.partH.need((size_t)std::max<int64_t>(nbH, 1)));
@@ -370,7 +370,7 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
                     int64_t hoff = 0;
                     for (int i = 0; i < G.ns; ++i) {
                         OSMPM_TRY(G.s[i]->launch_hvp(G.s[i]->z.p, G.s[i]->y.p, gb.partH.p + hoff));
-                        hoff += (int64_t)G.s[i]->box.ntiles * HVP_NW<D>;
+                        hoff += G.s[i]->box.ntiles;
                     }
                     if (pf.on) pf.begin("cg", st);
                     OSMPM_TRY(halo_sum<D, R>(G, {{&Sub<D, R>::y, D}}));
@@ -440,7 +440,7 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
                     int64_t hoff = 0;
                     for (int i = 0; i < G.ns; ++i) {
                         OSMPM_TRY(G.s[i]->launch_hvp(G.s[i]->p.p, G.s[i]->y.p, gb.partH.p + hoff));
-                        hoff += (int64_t)G.s[i]->box.ntiles * HVP_NW<D>;
+                        hoff += G.s[i]->box.ntiles;
                     }
                 }
                 if (pf.on) pf.begin("cg", st);

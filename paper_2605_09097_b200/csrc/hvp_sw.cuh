@@ -425,8 +425,8 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
          const __grid_constant__ CUtensorMap tmc, int use_tmap, double* __restrict__ tbuf,
          double* __restrict__ pkp)
 {
-    // pkp (optional): per-warp partials [tile][warp] of d^T K d = sum over tiles of d . (the tile's partial
-    // y), the curvature the PCG step length needs, accumulated by the plane flushes (sw_flush)
+    // pkp (optional): per-CTA partials of d^T K d = sum over tiles of d . (the tile's partial y), the
+    // curvature the PCG step length needs, accumulated by the plane flushes (sw_flush)
     using T = Tile<D>;
     using C = CL<D>;
     using In = HvpIn<D, R>;
@@ -449,6 +449,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
     const int tile = blockIdx.x;
     const int64_t kt = (int64_t)tile * T::NC;
     __shared__ int scs[T::NC + 1];  // the tile's cell ranges
+    __shared__ double wdot[HVP_NW<D>];
     int t[3];
     tile_coords<D>(b, tile, t);
     // the node tile of d (fp64: asynchronous, in flight while the cell ranges load) and the staging
@@ -478,7 +479,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
     __syncthreads();
     if (scs[0] == scs[T::NC]) {
         if constexpr (ASYNC) asm volatile("cp.async.wait_all;" ::: "memory");
-        if (pkp && threadIdx.x < HVP_NW<D>) pkp[(int64_t)tile * HVP_NW<D> + threadIdx.x] = 0.0;
+        if (pkp && threadIdx.x == 0) pkp[tile] = 0.0;
         return;
     }
     double dkd = 0.0;  // this thread's flushed nodes' d . y_tile
@@ -630,14 +631,23 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                                   dkd);
         // the next emit must not overwrite slots still being summed: a non-empty next layer has its
         // records barrier in between; otherwise synchronise here
+        if (pkp && layer == T::NL + 1) {
+            // warp partials of the curvature into shared memory before the closing barrier (the last
+            // warp of a 144-thread CTA has 16 lanes)
+            const unsigned mask = __activemask();
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) dkd += __shfl_xor_sync(mask, dkd, o);
+            if ((threadIdx.x & 31) == 0) wdot[threadIdx.x >> 5] = dkd;
+        }
         if (layer + 1 >= T::NL || layer_empty(layer + 1)) __syncthreads();
     }
-    if (pkp) {
-        // warp partials, no CTA barrier (the last warp of a 144-thread CTA has 16 lanes)
-        const unsigned mask = __activemask();
+    // the last layer's closing barrier above has made every warp's partial visible: one per CTA, in a
+    // fixed order
+    if (pkp && threadIdx.x == 0) {
+        double v = 0.0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) dkd += __shfl_xor_sync(mask, dkd, o);
-        if ((threadIdx.x & 31) == 0) pkp[(int64_t)tile * HVP_NW<D> + (threadIdx.x >> 5)] = dkd;
+        for (int w = 0; w < HVP_NW<D>; ++w) v += wdot[w];
+        pkp[tile] = v;
     }
 }
 

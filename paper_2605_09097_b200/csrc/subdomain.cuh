@@ -147,10 +147,13 @@ struct Sub : public osmpm_subdomain {
     // OSMPM_DETERMINISTIC=1: the sliding-window gradient and HVP store per-tile node blocks that a
     // node pass sums in a fixed tile order instead of RED-ing into the node arrays (bitwise
     // reproducible Newton-PCG; read at every launch so a process can switch)
-    static bool det_mode()
+    // det_force: set by the coupler on the replicated coarse subdomain of a multi-rank run, so that every
+    // rank computes bitwise the same coarse solution
+    bool det_force = false;
+    bool det_mode() const
     {
         const char* e = getenv("OSMPM_DETERMINISTIC");
-        return e && e[0] == '1';
+        return det_force || (e && e[0] == '1');
     }
     osmpm_status det_gather(const double* tb, double* out)
     {

@@ -274,7 +274,7 @@ osmpm_status project_accumulate_group(SlabGroup<D, R> F, Sub<D, R>* coarse, bool
     OSMPM_CU(cudaMemsetAsync(num, 0, nnb * (D + 1) * sizeof(double), st));
     double* denp = num + nnb * D;  // num and den contiguous: one all-reduce
     auto& pf = F.ctx->prof;
-    if (pf.on) pf.begin("transmit", st);
+    if (pf.on) pf.begin("pi", st);
     int* gdc = coarse->pi_gd.p;
     if (!gdc) {
         OSMPM_TRY(coarse->pi_gd.need(3));
@@ -328,7 +328,7 @@ osmpm_status project_accumulate_group(SlabGroup<D, R> F, Sub<D, R>* coarse, bool
         OSMPM_LAUNCH_CHECK();
     }
     OSMPM_TRY(group_allreduce<D, R>(F, num, (int)(nnb * (D + 1))));
-    if (pf.on) pf.end("transmit", st);
+    if (pf.on) pf.end("pi", st);
     return OSMPM_OK;
 }
 
@@ -426,13 +426,13 @@ osmpm_status transmit_impl(SlabGroup<D, R> SG, Sub<D, R>* src, Sub<D, R>* dstc, 
             return OSMPM_E_INVALID_ARG;
         }
         if (nt > 0) {
-            if (src->ctx->prof.on) src->ctx->prof.begin("transmit", st);
+            if (src->ctx->prof.on) src->ctx->prof.begin("interp", st);
             src->KC();
             k_interp<D><<<nblk_all(nt, 256), 256, 0, st>>>(nt, tptr, dst_geo, src->box, src->vn.p,
                                                            need_solved ? src->vnew.p : nullptr, alpha, optr,
                                                            src->err.p);
             OSMPM_LAUNCH_CHECK();
-            if (src->ctx->prof.on) src->ctx->prof.end("transmit", st);
+            if (src->ctx->prof.on) src->ctx->prof.end("interp", st);
         }
     }
     if (sp == OSMPM_HOST) {

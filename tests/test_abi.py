@@ -50,6 +50,15 @@ def test_version_string(libpath):
     assert b"sm_100a" in lib.osmpm_version()
 
 
+def test_library_is_built_from_the_current_sources(libpath):
+    """build() embeds the sha256 of csrc/ + include/ + flags; the loaded library must carry the hash of
+    the sources in the tree (no stale binary from another checkout)."""
+    from paper_2605_09097_b200 import build
+    lib = ctypes.CDLL(libpath)
+    lib.osmpm_version.restype = ctypes.c_char_p
+    assert lib.osmpm_version().decode().endswith("src " + build.source_hash())
+
+
 def test_binding_fails_loudly_without_library(tmp_path, monkeypatch):
     from paper_2605_09097_b200 import osmpm
     monkeypatch.setattr(osmpm, "LIB_PATH", str(tmp_path / "missing.so"))
