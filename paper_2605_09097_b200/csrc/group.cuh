@@ -278,11 +278,10 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
         nbd_tot += nblk(nn * D, 256);
     }
     OSMPM_TRY(gb.partB.need((size_t)std::max<int64_t>(std::max(nbn_tot, nbd_tot), 1) * 4));
-    // PCG curvature partials: p^T M p per node-vector block (k_cg_init / k_cg_p), p^T K p per HVP tile
+    // single-reduction PCG (R22): 3 partials per node-vector block in partB, u^T K u per HVP tile in partH
     int64_t nbH = 0;
     for (int i = 0; i < G.ns; ++i) nbH += G.s[i]->box.ntiles;
     const int64_t nbM = nbd_tot;
-    OSMPM_TRY(gb.partM.need((size_t)std::max<int64_t>(nbM, 1)));
     OSMPM_TRY(gb.partH.need((size_t)std::max<int64_t>(nbH, 1)));
     const bool remote = G.multi();
     double g0 = 0.0, gref = 0.0;
@@ -415,8 +414,7 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
                 const int64_t ndof = q->box.nnodes * D;
                 q->KC();
                 k_cg_init<D><<<nblk(ndof, 256), 256, 0, st>>>(ndof, q->nown * D, q->fmask.p, q->g.p, q->dg.p, q->r.p,
-                                                              q->z.p, q->p.p, q->xs.p, q->y.p, q->m.p, idt2,
-                                                              gb.partB.p + off * 2, gb.partM.p + off);
+                                                              q->z.p, q->p.p, q->xs.p, q->y.p, gb.partB.p + off * 2);
                 off += nblk(ndof, 256);
             }
             if (!remote) {
@@ -435,37 +433,36 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
         while (done_it < s->max_cg) {
             const int cnt = std::min(chunk, s->max_cg - done_it);
             for (int c = 0; c < cnt; ++c) {
-                // y = K p, and per-CTA partials of p^T K p for the step length (k_hvp_sw)
-                {
-                    int64_t hoff = 0;
-                    for (int i = 0; i < G.ns; ++i) {
-                        OSMPM_TRY(G.s[i]->launch_hvp(G.s[i]->p.p, G.s[i]->y.p, gb.partH.p + hoff));
-                        hoff += G.s[i]->box.ntiles;
-                    }
-                }
+                for (int i = 0; i < G.ns; ++i) OSMPM_TRY(G.s[i]->launch_hvp(G.s[i]->p.p, G.s[i]->y.p));
                 if (pf.on) pf.begin("cg", st);
                 OSMPM_TRY(halo_sum<D, R>(G, {{&Sub<D, R>::y, D}}));
-                // alpha = r.z / (p^T M p / dt^2 + p^T K p): the mass part comes from k_cg_init / k_cg_p
-                if (!remote) {
-                    s0->KC();
-                    k_cg_alpha<<<1, 1024, 0, st>>>(gb.partM.p, (int)nbM, gb.partH.p, (int)nbH, gb.cgs.p);
-                } else {
-                    s0->KC();
-                    k_final_sum2_cg<<<1, 1024, 0, st>>>(gb.partM.p, (int)nbM, gb.partH.p, (int)nbH, gb.cgs.p,
-                                                        gb.gsum.p);
-                    OSMPM_NCCL(ncclAllReduce(gb.gsum.p, gb.gsum.p, 1, ncclDouble, ncclSum, G.gc->comm, st));
-                    s0->KC();
-                    k_cg_alpha_sum<<<1, 1, 0, st>>>(gb.gsum.p, gb.cgs.p);
-                }
-                OSMPM_LAUNCH_CHECK();
                 int64_t off = 0;
+                for (int i = 0; i < G.ns; ++i) {
+                    Sub<D, R>* q = G.s[i];
+                    const int64_t nn = q->box.nnodes;
+                    q->KC();
+                    k_cg_q<D><<<nblk(nn, 256), 256, 0, st>>>(nn, q->nown, q->fmask.p, q->m.p, idt2, q->p.p, q->y.p,
+                                                             gb.cgs.p, gb.partB.p + off);
+                    off += nblk(nn, 256);
+                }
+                OSMPM_TRY(reduce(
+                    1, off,
+                    [&](double* pp, int nb) {
+                        s0->KC();
+                        k_cg_alpha<<<1, 1024, 0, st>>>(pp, nb, gb.cgs.p);
+                    },
+                    [&](double* v) {
+                        s0->KC();
+                        k_cg_alpha_sum<<<1, 1, 0, st>>>(v, gb.cgs.p);
+                    }));
+                off = 0;
                 for (int i = 0; i < G.ns; ++i) {
                     Sub<D, R>* q = G.s[i];
                     const int64_t ndof = q->box.nnodes * D;
                     q->KC();
-                    k_cg_update<D><<<nblk(ndof, 256), 256, 0, st>>>(ndof, q->nown * D, q->fmask.p, q->p.p, q->y.p,
-                                                                    q->m.p, idt2, q->dg.p, q->xs.p, q->r.p, q->z.p,
-                                                                    gb.cgs.p, gb.partB.p + off * 2);
+                    k_cg_update<<<nblk(ndof, 256), 256, 0, st>>>(ndof, q->nown * D, q->fmask.p, q->p.p, q->y.p,
+                                                                 q->dg.p, q->xs.p, q->r.p, q->z.p, gb.cgs.p,
+                                                                 gb.partB.p + off * 2);
                     off += nblk(ndof, 256);
                 }
                 OSMPM_TRY(reduce(
@@ -478,14 +475,11 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
                         s0->KC();
                         k_cg_beta_sum<<<1, 1, 0, st>>>(v, gb.cgs.p);
                     }));
-                off = 0;
                 for (int i = 0; i < G.ns; ++i) {
                     Sub<D, R>* q = G.s[i];
                     const int64_t ndof = q->box.nnodes * D;
                     q->KC();
-                    k_cg_p<D><<<nblk(ndof, 256), 256, 0, st>>>(ndof, q->nown * D, q->fmask.p, q->z.p, q->p.p, q->y.p,
-                                                               q->m.p, idt2, gb.cgs.p, gb.partM.p + off);
-                    off += nblk(ndof, 256);
+                    k_cg_p<<<nblk(ndof, 256), 256, 0, st>>>(ndof, q->fmask.p, q->z.p, q->p.p, q->y.p, gb.cgs.p);
                 }
                 if (pf.on) pf.end("cg", st);
                 OSMPM_LAUNCH_CHECK();

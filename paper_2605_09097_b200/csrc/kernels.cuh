@@ -349,15 +349,14 @@ struct CGScalars {
     int done, it, negcurv_first, fixed;
 };
 
-// r = -g (free), z = r/diag, p = z, x = 0, y = 0 ; partials {rz, rr} and {p^T M p / dt^2}
+// r = -g (free), z = r/diag, p = z, x = 0, y = 0 ; partials {rz, rr}
 template <int D>
 __global__ void k_cg_init(int64_t ndof, int64_t nown_dof, const uint8_t* __restrict__ fm, const double* __restrict__ g,
                           double* __restrict__ dg, double* __restrict__ r, double* __restrict__ z,
                           double* __restrict__ p, double* __restrict__ x, double* __restrict__ y,
-                          const double* __restrict__ m, double idt2, double* __restrict__ partials,
-                          double* __restrict__ partM)
+                          double* __restrict__ partials)
 {
-    double red[2] = {0.0, 0.0}, pm[1] = {0.0};
+    double red[2] = {0.0, 0.0};
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ndof; k += (int64_t)gridDim.x * blockDim.x) {
         const bool f = fm[k];
         if (!f) dg[k] = 1.0;
@@ -371,11 +370,9 @@ __global__ void k_cg_init(int64_t ndof, int64_t nown_dof, const uint8_t* __restr
         if (f && k < nown_dof) {
             red[0] += rk * zk;
             red[1] += rk * rk;
-            pm[0] += m[k / D] * idt2 * zk * zk;
         }
     }
     block_reduce_store<2>(red, partials);
-    block_reduce_store<1>(pm, partM);
 }
 
 __device__ __forceinline__ void cg_init_fin(const double* v, CGScalars* s, double gn, double cg_rtol, int fixed)
@@ -404,6 +401,30 @@ __global__ void k_cg_init_fin_sum(const double* v, CGScalars* s, double gn, doub
     cg_init_fin(v, s, gn, cg_rtol, fixed);
 }
 
+// q = y + m/dt^2 p on free DOFs, 0 elsewhere (in place in y) ; partial p.q
+template <int D>
+__global__ void k_cg_q(int64_t nn, int64_t nown, const uint8_t* __restrict__ fm, const double* __restrict__ m, double idt2,
+                       const double* __restrict__ p, double* __restrict__ y, const CGScalars* s,
+                       double* __restrict__ partials)
+{
+    double red[1] = {0.0};
+    if (!s->done) {
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const int64_t k = i * D + a;
+                // non-free DOFs (inactive, Dirichlet) are skipped without touching memory: their p is
+                // 0 and y there is never read (k_cg_update skips them too; k_cg_p re-zeroes y)
+                if (!fm[k]) continue;
+                const double q = y[k] + m[i] * idt2 * p[k];
+                y[k] = q;
+                if (i < nown) red[0] += p[k] * q;
+            }
+        }
+    }
+    block_reduce_store<1>(red, partials);
+}
+
 __device__ __forceinline__ void cg_alpha(const double* v, CGScalars* s)
 {
     {
@@ -419,39 +440,21 @@ __device__ __forceinline__ void cg_alpha(const double* v, CGScalars* s)
         }
     }
 }
-// p.q = p^T M p / dt^2 (partials of k_cg_init / k_cg_p) + p^T K p (partials of the HVP, k_hvp_sw's pkp)
-__device__ __forceinline__ void final_sum2(const double* a, int na, const double* b, int nb, double* out)
-{
-    double v[1], w[1];
-    final_sum<1>(a, na, v);
-    __syncthreads();
-    final_sum<1>(b, nb, w);
-    if (threadIdx.x == 0) out[0] = v[0] + w[0];
-}
-__global__ void k_cg_alpha(const double* partM, int nbM, const double* partH, int nbH, CGScalars* s)
+__global__ void k_cg_alpha(const double* partials, int nb, CGScalars* s)
 {
     if (s->done) return;
-    __shared__ double pq[1];
-    final_sum2(partM, nbM, partH, nbH, pq);
-    if (threadIdx.x == 0) cg_alpha(pq, s);
-}
-__global__ void k_final_sum2_cg(const double* partM, int nbM, const double* partH, int nbH, const CGScalars* s,
-                                double* out)
-{
-    if (s->done) return;
-    final_sum2(partM, nbM, partH, nbH, out);
+    double v[1];
+    final_sum<1>(partials, nb, v);
+    if (threadIdx.x == 0) cg_alpha(v, s);
 }
 __global__ void k_cg_alpha_sum(const double* v, CGScalars* s)
 {
     if (!s->done) cg_alpha(v, s);
 }
 
-// q = K p (y, from the HVP) + M p / dt^2 formed on the fly ; x += alpha p ; r -= alpha q ; z = r/diag ;
-// partials {r.z, r.r}
-template <int D>
+// x += alpha p ; r -= alpha q ; z = r/diag ; partials {r.z, r.r}
 __global__ void k_cg_update(int64_t ndof, int64_t nown_dof, const uint8_t* __restrict__ fm, const double* __restrict__ p,
-                            const double* __restrict__ y, const double* __restrict__ m, double idt2,
-                            const double* __restrict__ dg, double* __restrict__ x,
+                            const double* __restrict__ q, const double* __restrict__ dg, double* __restrict__ x,
                             double* __restrict__ r, double* __restrict__ z, const CGScalars* s,
                             double* __restrict__ partials)
 {
@@ -460,10 +463,8 @@ __global__ void k_cg_update(int64_t ndof, int64_t nown_dof, const uint8_t* __res
         const double al = s->alpha;
         for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ndof; k += (int64_t)gridDim.x * blockDim.x) {
             if (!fm[k]) continue;  // x, r, z stay 0 on non-free DOFs (k_cg_init)
-            const double pk = p[k];
-            const double qk = y[k] + m[k / D] * idt2 * pk;
-            const double xk = x[k] + al * pk;
-            const double rk = r[k] - al * qk;
+            const double xk = x[k] + al * p[k];
+            const double rk = r[k] - al * q[k];
             const double zk = rk / dg[k];
             x[k] = xk;
             r[k] = rk;
@@ -506,24 +507,16 @@ __global__ void k_final_sum_cg(const double* partials, int nb, const CGScalars* 
     final_sum<NV>(partials, nb, out);
 }
 
-// p = z + beta p ; y = 0 ; partials {p^T M p / dt^2} of the new p
-template <int D>
-__global__ void k_cg_p(int64_t ndof, int64_t nown_dof, const uint8_t* __restrict__ fm, const double* __restrict__ z,
-                       double* __restrict__ p, double* __restrict__ y, const double* __restrict__ m, double idt2,
-                       const CGScalars* s, double* __restrict__ partM)
+// p = z + beta p ; y = 0
+__global__ void k_cg_p(int64_t ndof, const uint8_t* __restrict__ fm, const double* __restrict__ z,
+                       double* __restrict__ p, double* __restrict__ y, const CGScalars* s)
 {
     if (s->done) return;
     const double be = s->beta;
-    double pm[1] = {0.0};
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ndof; k += (int64_t)gridDim.x * blockDim.x) {
-        if (fm[k]) {  // p stays 0 on non-free DOFs
-            const double pk = z[k] + be * p[k];
-            p[k] = pk;
-            if (k < nown_dof) pm[0] += m[k / D] * idt2 * pk * pk;
-        }
+        if (fm[k]) p[k] = z[k] + be * p[k];  // p stays 0 on non-free DOFs
         y[k] = 0.0;
     }
-    block_reduce_store<1>(pm, partM);
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -60,7 +60,7 @@ static inline int nblk_all(int64_t n, int bs)
 // ncclAllReduce'd before use.
 struct CGScalars;
 struct GroupBufs {
-    DBuf<double> partA, partB, partM, partH, scal, gsum, halo_tmp;  // partM / partH: PCG d^T M d, d^T K d
+    DBuf<double> partA, partB, partH, scal, gsum, halo_tmp;  // partH: the HVP's d^T K d partials (R22)
     DBuf<CGScalars> cgs;
     DBuf<int> gbounds;
     double* h_scal = nullptr;  // pinned
