@@ -45,9 +45,11 @@ def tip_mask(x0, dx):
 
 
 def measure(x0, x, dx):
+    """(W, H) of the centre-line tip from the displacement of the particles nearest to it (the lattice
+    puts them a fraction of a cell inside the beam end, so positions are not compared with L)."""
     t = tip_mask(x0, dx)
-    xt, yt = x[t, 0].mean(), x[t, 1].mean()
-    return xt / L, (Y0 + H / 2 - yt) / L
+    ux, uy = (x[t, 0] - x0[t, 0]).mean(), (x[t, 1] - x0[t, 1]).mean()
+    return 1.0 + ux / L, -uy / L
 
 
 def clamp_nodes(grid):
