@@ -1,0 +1,209 @@
+"""Elastic-inclusion benchmark with OS-MPM on the GPU, and the single- vs dual-domain cost ratio
+(§4.3).
+
+Geometry and material as scripts/eshelby.py (the single-domain check, R20): a matrix disk of
+radius b = 0.5 (E_out = 100 kPa, nu = 0.3) with a centred inclusion R = 0.1 (E_in = ratio x E_out) whose
+particles start at F0 = (1 - delta) I, 2 x 2 particles per cell (the paper: 4 per cell),
+mirror constraints on the centre lines.  Stresses sampled at particles against the Lame reference of
+the finite composite disk (eshelby.reference_stress).
+
+  single  the whole disk at h (the paper's single-domain reference)
+  dual    OS-MPM as in PAPER.md:605-610: fine Omega_S = the square [0.5 - w, 0.5 + w]^2 (w = 0.15, the
+          C3 footprint) at h around the inclusion, coarse Omega_B = the disk minus the square shrunk by
+          `overlap` coarse cells at 2h, M = 2 (dT = 2 dt), coupled by Alg. 1 (eps_conv = 1e-5)
+
+Protocols (the same for both runs):
+  static   one quasi-static frame (dT = 10 s; inertia negligible) from the misfit state
+  dynamic  the paper's: frames of dt = 0.01 s x (1/32) / h (dt / h constant; dual: dT = 2 dt, M = 2)
+           until the l-inf grid velocity is below `vtol` on every grid
+
+Errors: inclusion mean pressure over r < R - 2h (fine particles) and the relative L2 error of
+(sigma_rr, sigma_tt) over the matrix annulus 1.5 R < r < b - 3h (each point sampled by the domain that
+owns it: fine particles inside the square shrunk by the overlap, coarse particles outside the square).
+Cost: GPU wall time of the solves (every call synchronises).
+
+  python scripts/inclusion_dual.py [--protocol static|dynamic] [--ratio 1 2 5] [--inv-h 64 128 256]
+Prints one JSON line per (ratio, h).
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+
+import eshelby as es  # noqa: E402
+import synth  # noqa: E402
+
+W_FINE = 0.15
+
+
+def static_settings():
+    from paper_2605_09097_b200 import osmpm
+    return osmpm.newton_settings(newton_rtol=1e-7, cg_rtol=1e-10, max_cg=40000, max_newton=40, guess=1,
+                                 energy_noise_rtol=1e-12)
+
+
+def dynamic_settings():
+    from paper_2605_09097_b200 import osmpm
+    return osmpm.newton_settings(newton_rtol=1e-8, newton_atol=1e-12, cg_rtol=1e-8, max_cg=20000, max_newton=30,
+                                 energy_noise_rtol=1e-12)
+
+
+def mirror_bc(grid):
+    nx, ny = grid.dims[0], grid.dims[1]
+    k = np.stack(np.meshgrid(np.arange(nx), np.arange(ny), indexing="ij"), -1).reshape(-1, 2)
+    xs = np.asarray(grid.origin[:2]) + k * grid.dx
+    bits = np.zeros(xs.shape[0], np.uint8)
+    bits[np.abs(xs[:, 0] - es.XC) <= 1e-12] |= 1
+    bits[np.abs(xs[:, 1] - es.YC) <= 1e-12] |= 2
+    sel = np.flatnonzero(bits)
+    return sel, bits[sel]
+
+
+def pair(inv_h, ratio, dT, overlap=2, delta=es.DELTA):
+    """(coarse, fine) scenes of the dual decomposition (module docstring)."""
+    h = 1.0 / inv_h
+    H = 2.0 * h
+    c = np.array([es.XC, es.YC])
+    mats = [(es.E_OUT, es.NU), (es.E_OUT * ratio, es.NU)]
+    # fine: the square around the inclusion
+    xf, vf = synth.lattice((es.XC - W_FINE, es.YC - W_FINE), (es.XC + W_FINE, es.YC + W_FINE), h, 2)
+    rf = np.sqrt(((xf - c) ** 2).sum(axis=1))
+    bf = (np.abs(xf - c).max(axis=1) > W_FINE - h).astype(np.uint8)      # P^∂: one cell inside the cut
+    pf = synth.make_particles(xf, vf, es.RHO, mat=(rf < es.R_INC).astype(np.int32), boundary=bf)
+    pf.F[rf < es.R_INC] = (1.0 - delta) * np.eye(2)
+    # coarse: the disk minus the square shrunk by `overlap` coarse cells
+    hole = W_FINE - overlap * H
+    xc, vc = synth.lattice((es.XC - es.B_OUT, es.YC - es.B_OUT), (es.XC + es.B_OUT, es.YC + es.B_OUT), H, 2,
+                           inside=lambda p: (((p - c) ** 2).sum(axis=1) < es.B_OUT ** 2)
+                           & (np.abs(p - c).max(axis=1) > hole))
+    rc = np.sqrt(((xc - c) ** 2).sum(axis=1))
+    bc = (np.abs(xc - c).max(axis=1) < hole + H).astype(np.uint8)
+    pc = synth.make_particles(xc, vc, es.RHO, mat=(rc < es.R_INC).astype(np.int32), boundary=bc)
+    pc.F[rc < es.R_INC] = (1.0 - delta) * np.eye(2)
+    allx = np.vstack([xf, xc])
+    fine = synth.Scene(synth.grid_around(xf, h, 4, 2), pf, mats, dT / 2, (0.0, 0.0, 0.0))
+    coarse = synth.Scene(synth.grid_around(allx, H, 4, 2), pc, mats, dT, (0.0, 0.0, 0.0))
+    return coarse, fine, hole
+
+
+def measure_dual(ratio, coarse, fine, hole, Fc, Ff, h):
+    c = np.array([es.XC, es.YC])
+    in_f = np.abs(fine.particles.x - c).max(axis=1) < hole
+    out_c = np.abs(coarse.particles.x - c).max(axis=1) > W_FINE
+    x0 = np.vstack([fine.particles.x[in_f], coarse.particles.x[out_c]])
+    F = np.vstack([Ff[in_f], Fc[out_c]])
+    mat = np.concatenate([fine.particles.mat[in_f], coarse.particles.mat[out_c]])
+    return _measure(ratio, x0, F, mat, h)
+
+
+def _measure(ratio, x0, F, mat, h):
+    lo, Go = es.lame(es.E_OUT, es.NU)
+    li, Gi = es.lame(es.E_OUT * ratio, es.NU)
+    mu = np.where(mat == 1, Gi, Go)
+    lam = np.where(mat == 1, li, lo)
+    sig = es.cauchy(F, mu, lam)
+    d = x0 - np.array([es.XC, es.YC])
+    r = np.sqrt((d ** 2).sum(axis=1))
+    er = d / np.maximum(r, 1e-300)[:, None]
+    et = np.stack([-er[:, 1], er[:, 0]], axis=1)
+    srr = np.einsum("ni,nij,nj->n", er, sig, er)
+    stt = np.einsum("ni,nij,nj->n", et, sig, et)
+    ref_rr, ref_tt = es.reference_stress(ratio, r)
+    inside = r < es.R_INC - 2 * h
+    ann = (r > 1.5 * es.R_INC) & (r < es.B_OUT - 3 * 2 * h)
+    p_in = -0.5 * (sig[inside, 0, 0] + sig[inside, 1, 1]).mean()
+    p_ref = -es.reference_stress(ratio, [0.0])[0][0]
+    num = np.sqrt(((srr[ann] - ref_rr[ann]) ** 2 + (stt[ann] - ref_tt[ann]) ** 2).sum())
+    den = np.sqrt((ref_rr[ann] ** 2 + ref_tt[ann] ** 2).sum())
+    return {"p_in_err": p_in / p_ref - 1.0, "err_out": num / den}
+
+
+def run_single(inv_h, ratio, protocol, vtol, max_frames):
+    from paper_2605_09097_b200 import osmpm
+    h = 1.0 / inv_h
+    dT = 10.0 if protocol == "static" else 0.01 * 32.0 / inv_h
+    sc, sel, bits = es.scene(inv_h, ratio, dt=dT)
+    ctx = osmpm.Context(0)
+    sub = osmpm.Subdomain(ctx, sc.grid, sc.dt, sc.particles, sc.materials, sc.gravity)
+    sub.set_dirichlet(sel, bits, np.zeros((sel.size, 2)))
+    ns = static_settings() if protocol == "static" else dynamic_settings()
+    t0 = time.time()
+    frames = 0
+    while True:
+        sub.p2g()
+        sub.implicit_solve(ns)
+        v = sub.read_grid_velocity()
+        sub.g2p()
+        frames += 1
+        if protocol == "static" or np.abs(v).max() < vtol or frames >= max_frames:
+            break
+    sub.sync()
+    t = time.time() - t0
+    F = sub.read_particles(fields=("F",))["F"]
+    res = _measure(ratio, sc.particles.x, F, sc.particles.mat, h)
+    res.update(seconds=t, frames=frames, particles=int(sc.particles.n))
+    sub.close()
+    ctx.close()
+    return res
+
+
+def run_dual(inv_h, ratio, protocol, vtol, max_frames, overlap=2):
+    from paper_2605_09097_b200 import osmpm
+    h = 1.0 / inv_h
+    dT = 10.0 if protocol == "static" else 2 * 0.01 * (32.0 / inv_h)
+    coarse, fine, hole = pair(inv_h, ratio, dT, overlap)
+    ctx = osmpm.Context(0)
+    sb = osmpm.Subdomain(ctx, coarse.grid, coarse.dt, coarse.particles, coarse.materials, coarse.gravity)
+    ss = osmpm.Subdomain(ctx, fine.grid, fine.dt, fine.particles, fine.materials, fine.gravity)
+    for sub, sc in ((sb, coarse), (ss, fine)):
+        sel, bits = mirror_bc(sc.grid)
+        sub.set_dirichlet(sel, bits, np.zeros((sel.size, 2)))
+    ns = static_settings() if protocol == "static" else dynamic_settings()
+    cpl = osmpm.Coupler(sb, ss, osmpm.schwarz_settings(M=2, eps_conv=1e-5, k_max=3000, coarse=ns, fine=ns))
+    t0 = time.time()
+    frames, iters = 0, 0
+    while True:
+        rep = cpl.step()
+        frames += 1
+        iters += rep.iters
+        if protocol == "static":
+            break
+        vb = sb.read_grid_velocity()
+        vs = ss.read_grid_velocity()
+        if max(np.abs(vb).max(), np.abs(vs).max()) < vtol or frames >= max_frames:
+            break
+    sb.sync()
+    t = time.time() - t0
+    Fc = sb.read_particles(fields=("F",))["F"]
+    Ff = ss.read_particles(fields=("F",))["F"]
+    res = measure_dual(ratio, coarse, fine, hole, Fc, Ff, h)
+    res.update(seconds=t, frames=frames, schwarz_iters=iters, particles_fine=int(fine.particles.n),
+               particles_coarse=int(coarse.particles.n), n_recv_B=rep.n_recv_B, n_recv_S=rep.n_recv_S)
+    cpl.close()
+    sb.close()
+    ss.close()
+    ctx.close()
+    return res
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--protocol", default="static", choices=["static", "dynamic"])
+    ap.add_argument("--ratio", type=float, nargs="+", default=[1.0, 2.0, 5.0])
+    ap.add_argument("--inv-h", type=int, nargs="+", default=[64, 128, 256])
+    ap.add_argument("--vtol", type=float, default=1e-6)
+    ap.add_argument("--max-frames", type=int, default=2000)
+    a = ap.parse_args()
+    for ratio in a.ratio:
+        for n in a.inv_h:
+            s = run_single(n, ratio, a.protocol, a.vtol, a.max_frames)
+            d = run_dual(n, ratio, a.protocol, a.vtol, a.max_frames)
+            print(json.dumps({"protocol": a.protocol, "ratio": ratio, "inv_h": n, "single": s, "dual": d,
+                              "cost_ratio_single_over_dual": s["seconds"] / d["seconds"]}), flush=True)
