@@ -109,7 +109,10 @@ typedef struct {
     int32_t cg_variant;  /* 0: standard Jacobi PCG (two reductions per iteration); 1: single-reduction
                             PCG (Chronopoulos-Gear, R22: the same iterates in exact arithmetic,
                             one reduction -- one all-reduce across ranks -- per iteration) */
-    int32_t reserved;    /* 0 */
+    int32_t psd;         /* PSD projection of the per-particle tangent blocks (R23):
+                            0 never (the timed path), 1 in a second PCG solve when the Newton direction
+                            fails the descent check g . dx < 0, 2 always.  Projected solves run the
+                            standard PCG with per-particle scatter kernels (not bitwise reproducible). */
 } osmpm_newton_settings;
 
 /* Outcome of one implicit solve.  Besides the counts, three events that change what the solve
@@ -125,7 +128,8 @@ typedef struct {
 typedef struct {
     int32_t newton_iters, cg_iters, ls_halvings, status;
     double grad_norm0, grad_norm, energy;
-    int32_t negcurv, ls_failures, floor_accept, reserved;
+    int32_t negcurv, ls_failures, floor_accept;
+    int32_t psd_solves;  /* PCG solves run with the PSD-projected tangent (settings.psd) */
 } osmpm_solve_stats;
 
 /* Schwarz coupling settings (R10-R16).

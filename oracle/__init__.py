@@ -29,14 +29,14 @@ class OrcNewtonSettings(C.Structure):
     _fields_ = [("max_newton", C.c_int32), ("max_cg", C.c_int32), ("fixed_iters", C.c_int32),
                 ("guess", C.c_int32), ("newton_rtol", C.c_double), ("newton_atol", C.c_double),
                 ("cg_rtol", C.c_double), ("ls_min_alpha", C.c_double),
-                ("energy_noise_rtol", C.c_double), ("cg_variant", C.c_int32), ("reserved", C.c_int32)]
+                ("energy_noise_rtol", C.c_double), ("cg_variant", C.c_int32), ("psd", C.c_int32)]
 
 
 class OrcSolveStats(C.Structure):
     _fields_ = [("newton_iters", C.c_int32), ("cg_iters", C.c_int32), ("ls_halvings", C.c_int32),
                 ("status", C.c_int32), ("grad_norm0", C.c_double), ("grad_norm", C.c_double),
                 ("energy", C.c_double), ("negcurv", C.c_int32), ("ls_failures", C.c_int32),
-                ("floor_accept", C.c_int32), ("reserved", C.c_int32)]
+                ("floor_accept", C.c_int32), ("psd_solves", C.c_int32)]
 
 
 def build(force: bool = False) -> str:
@@ -230,26 +230,37 @@ def gradient(scene, gs: GridState, u, particles=None):
     return out
 
 
-def hvp(scene, gs: GridState, u, dvec, node_mask=None, particles=None):
+def hvp(scene, gs: GridState, u, dvec, node_mask=None, particles=None, psd=False):
+    """psd: per-particle tangent blocks projected to PSD (R23)."""
     pt, args, keep = _newton_args(scene, particles)
     g = grid_struct(scene.grid)
     u = _f64(u)
     dvec = _f64(dvec)
     out = np.zeros_like(u)
     nm = None if node_mask is None else np.ascontiguousarray(node_mask, dtype=np.uint8)
-    rc = lib().orc_hvp(C.byref(g), *args, _p(gs.m), _p(u), _p(dvec),
-                       None if nm is None else _p(nm, np.uint8), _p(out))
+    rc = lib().orc_hvp_ex(C.byref(g), *args, _p(gs.m), _p(u), _p(dvec),
+                          None if nm is None else _p(nm, np.uint8), _p(out), C.c_int(1 if psd else 0))
     check(rc, "hvp")
     return out
 
 
-def diag(scene, gs: GridState, u, particles=None):
+def diag(scene, gs: GridState, u, particles=None, psd=False):
     pt, args, keep = _newton_args(scene, particles)
     g = grid_struct(scene.grid)
     u = _f64(u)
     out = np.zeros_like(u)
-    rc = lib().orc_diag(C.byref(g), *args, _p(gs.m), _p(u), _p(out))
+    rc = lib().orc_diag_ex(C.byref(g), *args, _p(gs.m), _p(u), _p(out), C.c_int(1 if psd else 0))
     check(rc, "diag")
+    return out
+
+
+def tangent_psd(F, E, nu):
+    """The PSD projection T+ of one particle's tangent block d^2 Psi / dF dF (d^2 x d^2, row-major vec)."""
+    F = _f64(F)
+    d = F.shape[0]
+    mu, lam = lame(E, nu)
+    out = np.zeros((d * d, d * d))
+    lib().orc_tangent_psd(C.c_int(d), _p(np.ascontiguousarray(F)), C.c_double(mu), C.c_double(lam), _p(out))
     return out
 
 
@@ -265,6 +276,7 @@ def default_settings(**kw) -> OrcNewtonSettings:
     s.ls_min_alpha = kw.get("ls_min_alpha", 2.0 ** -20)
     s.energy_noise_rtol = kw.get("energy_noise_rtol", 1e-13)
     s.cg_variant = kw.get("cg_variant", 0)
+    s.psd = kw.get("psd", 0)
     return s
 
 

@@ -37,7 +37,9 @@ typedef struct {
 typedef struct {
     int32_t max_newton, max_cg, fixed_iters, guess;
     double newton_rtol, newton_atol, cg_rtol, ls_min_alpha, energy_noise_rtol;
-    int32_t cg_variant, reserved; /* 0: standard Jacobi PCG; 1: single-reduction (Chronopoulos-Gear) */
+    int32_t cg_variant; /* 0: standard Jacobi PCG; 1: single-reduction (Chronopoulos-Gear) */
+    int32_t psd;        /* PSD projection of the per-particle tangent blocks (R23):
+                           0 never, 1 when the Newton direction fails the descent check, 2 always */
 } orc_newton_settings;
 
 typedef struct {
@@ -46,7 +48,8 @@ typedef struct {
     /* events that change what a solve returns (R7, R8): PCG solves cut short by
      * non-positive curvature; fixed-iteration Newton steps whose line search found no decrease
      * (alpha = 0 taken); converged solves accepted at the energy round-off floor */
-    int32_t negcurv, ls_failures, floor_accept, reserved;
+    int32_t negcurv, ls_failures, floor_accept, psd_solves; /* psd_solves: PCG solves run with the
+                                                             projected tangent (R23) */
 } orc_solve_stats;
 
 enum { ORC_OK = 0, ORC_OUT_OF_DOMAIN = 1, ORC_INVERTED = 2, ORC_NEWTON_NC = 3, ORC_LS_STAGNATION = 4 };
@@ -232,6 +235,94 @@ void orc_dP(int d, const double* F, const double* dF, double mu, double lam, dou
     double AdF = 0.0;
     for (int i = 0; i < d * d; ++i) AdF += A[i] * dF[i];
     for (int i = 0; i < d * d; ++i) dP[i] = mu * dF[i] + (mu - lam * lnJ) * T2[i] + lam * AdF * A[i];
+}
+
+/* PSD projection of the per-particle tangent block ("per-particle tangent blocks are
+ * eigen-projected to positive semidefinite"; R23).  The block is the d^2 x d^2 matrix
+ * T = d^2 Psi / dF dF (symmetric: a Hessian) acting on vec(dF), row-major vec; its columns are orc_dP
+ * of the unit directions.  T = Q diag(l) Q^T by cyclic Jacobi rotations (plain, to convergence), then
+ * T+ = Q diag(max(l, 0)) Q^T, and dP = T+ vec(dF). */
+static void sym_eig_jacobi(int n, double* A, double* Q)
+{
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) Q[i * n + j] = (i == j) ? 1.0 : 0.0;
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        double off = 0.0, diag = 0.0;
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) {
+                if (i == j) diag += A[i * n + i] * A[i * n + i];
+                else off += A[i * n + j] * A[i * n + j];
+            }
+        if (off <= 1e-32 * diag) break;
+        for (int p = 0; p < n - 1; ++p)
+            for (int q = p + 1; q < n; ++q) {
+                double apq = A[p * n + q];
+                if (apq == 0.0) continue;
+                double theta = (A[q * n + q] - A[p * n + p]) / (2.0 * apq);
+                double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+                for (int k = 0; k < n; ++k) { /* A <- J^T A J, columns p, q then rows p, q */
+                    double akp = A[k * n + p], akq = A[k * n + q];
+                    A[k * n + p] = c * akp - sn * akq;
+                    A[k * n + q] = sn * akp + c * akq;
+                }
+                for (int k = 0; k < n; ++k) {
+                    double apk = A[p * n + k], aqk = A[q * n + k];
+                    A[p * n + k] = c * apk - sn * aqk;
+                    A[q * n + k] = sn * apk + c * aqk;
+                }
+                for (int k = 0; k < n; ++k) {
+                    double qkp = Q[k * n + p], qkq = Q[k * n + q];
+                    Q[k * n + p] = c * qkp - sn * qkq;
+                    Q[k * n + q] = sn * qkp + c * qkq;
+                }
+            }
+    }
+}
+
+void orc_tangent_psd(int d, const double* F, double mu, double lam, double* Tp)
+{
+    int n = d * d;
+    double T[81], Q[81], E[9] = {0}, col[9];
+    for (int k = 0; k < n; ++k) {
+        memset(E, 0, sizeof(E));
+        E[k] = 1.0;
+        orc_dP(d, F, E, mu, lam, col);
+        for (int i = 0; i < n; ++i) T[i * n + k] = col[i];
+    }
+    for (int i = 0; i < n; ++i)
+        for (int j = i + 1; j < n; ++j) {
+            double a = 0.5 * (T[i * n + j] + T[j * n + i]);
+            T[i * n + j] = T[j * n + i] = a;
+        }
+    sym_eig_jacobi(n, T, Q);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < n; ++k) {
+                double l = T[k * n + k];
+                if (l > 0.0) s += Q[i * n + k] * l * Q[j * n + k];
+            }
+            Tp[i * n + j] = s;
+        }
+}
+
+void orc_dP_psd(int d, const double* F, const double* dF, double mu, double lam, double* dP)
+{
+    int n = d * d;
+    double Tp[81];
+    orc_tangent_psd(d, F, mu, lam, Tp);
+    for (int i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (int k = 0; k < n; ++k) s += Tp[i * n + k] * dF[k];
+        dP[i] = s;
+    }
+}
+
+static void tangent_apply(int psd, int d, const double* F, const double* dF, double mu, double lam, double* dP)
+{
+    if (psd) orc_dP_psd(d, F, dF, mu, lam, dP);
+    else orc_dP(d, F, dF, mu, lam, dP);
 }
 
 static int cmp_double(const void* a, const void* b)
@@ -428,9 +519,9 @@ int orc_gradient(const orc_grid* g, int64_t np, const double* x, const double* F
  *   dF_p = (sum_j d_j grad N_jp^T) F_p^n.
  * `node_mask` (may be NULL) restricts the output to masked nodes (sampled full-size parity):
  * only particles whose stencil touches a masked node are visited; the rest of y is zero. */
-int orc_hvp(const orc_grid* g, int64_t np, const double* x, const double* F, const double* V0,
-            const int32_t* mat, const double* E, const double* nu, double dt, const double* mi,
-            const double* u, const double* dvec, const uint8_t* node_mask, double* y)
+int orc_hvp_ex(const orc_grid* g, int64_t np, const double* x, const double* F, const double* V0,
+               const int32_t* mat, const double* E, const double* nu, double dt, const double* mi,
+               const double* u, const double* dvec, const uint8_t* node_mask, double* y, int psd)
 {
     int d = g->d;
     int64_t nn = n_nodes(g);
@@ -458,7 +549,7 @@ int orc_hvp(const orc_grid* g, int64_t np, const double* x, const double* F, con
                 G[a * d + b] = s;
             }
         matmul(d, G, Fn, dF);
-        orc_dP(d, Fu, dF, mu, lam, dP);
+        tangent_apply(psd, d, Fu, dF, mu, lam, dP);
         transpose(d, Fn, FnT);
         matmul(d, dP, FnT, dPFnT);
         for (int s = 0; s < c; ++s) {
@@ -473,11 +564,18 @@ int orc_hvp(const orc_grid* g, int64_t np, const double* x, const double* F, con
     return ORC_OK;
 }
 
+int orc_hvp(const orc_grid* g, int64_t np, const double* x, const double* F, const double* V0,
+            const int32_t* mat, const double* E, const double* nu, double dt, const double* mi,
+            const double* u, const double* dvec, const uint8_t* node_mask, double* y)
+{
+    return orc_hvp_ex(g, np, x, F, V0, mat, E, nu, dt, mi, u, dvec, node_mask, y, 0);
+}
+
 /* O6: Jacobi diagonal, by definition diag_{i,a} = e_{i,a}^T H e_{i,a}:
  *   m_i/dt^2 + sum_p V0 (e_a h^T) : dP(F_p(u); e_a h^T),  h = F_p^{nT} grad N_ip.            */
-int orc_diag(const orc_grid* g, int64_t np, const double* x, const double* F, const double* V0,
-             const int32_t* mat, const double* E, const double* nu, double dt, const double* mi,
-             const double* u, double* diag)
+int orc_diag_ex(const orc_grid* g, int64_t np, const double* x, const double* F, const double* V0,
+                const int32_t* mat, const double* E, const double* nu, double dt, const double* mi,
+                const double* u, double* diag, int psd)
 {
     int d = g->d;
     int64_t nn = n_nodes(g);
@@ -502,7 +600,7 @@ int orc_diag(const orc_grid* g, int64_t np, const double* x, const double* F, co
             for (int a = 0; a < d; ++a) {
                 memset(dF, 0, sizeof(dF));
                 for (int b = 0; b < d; ++b) dF[a * d + b] = h[b];
-                orc_dP(d, Fu, dF, mu, lam, dP);
+                tangent_apply(psd, d, Fu, dF, mu, lam, dP);
                 double q = 0.0;
                 for (int k = 0; k < d * d; ++k) q += dF[k] * dP[k];
                 diag[idx[s] * d + a] += V0[p] * q;
@@ -510,6 +608,13 @@ int orc_diag(const orc_grid* g, int64_t np, const double* x, const double* F, co
         }
     }
     return ORC_OK;
+}
+
+int orc_diag(const orc_grid* g, int64_t np, const double* x, const double* F, const double* V0,
+             const int32_t* mat, const double* E, const double* nu, double dt, const double* mi,
+             const double* u, double* diag)
+{
+    return orc_diag_ex(g, np, x, F, V0, mat, E, nu, dt, mi, u, diag, 0);
 }
 
 /* ------------------------------------------------------------------------------------------ */
@@ -542,7 +647,7 @@ static int pcg_single_reduction(const orc_grid* g, int64_t np, const double* x, 
                                 const int32_t* mat, const double* E, const double* nu, double dt, const double* mi,
                                 const double* u, const double* gr, const double* dg, const uint8_t* free_mask,
                                 const orc_newton_settings* st, double gn, int64_t nd, double* xs, double* r, double* z,
-                                double* pv, double* q, double* sv, orc_solve_stats* stats)
+                                double* pv, double* q, double* sv, orc_solve_stats* stats, int psd)
 {
     for (int64_t k = 0; k < nd; ++k) {
         xs[k] = 0.0;
@@ -555,7 +660,7 @@ static int pcg_single_reduction(const orc_grid* g, int64_t np, const double* x, 
         double rn = sqrt(dot_free(nd, free_mask, r, r));
         if (!st->fixed_iters && rn <= st->cg_rtol * gn) break;
         for (int64_t k = 0; k < nd; ++k) z[k] = free_mask[k] ? r[k] / dg[k] : 0.0;
-        int rc = orc_hvp(g, np, x, F, V0, mat, E, nu, dt, mi, u, z, NULL, q);
+        int rc = orc_hvp_ex(g, np, x, F, V0, mat, E, nu, dt, mi, u, z, NULL, q, psd);
         if (rc) return rc;
         for (int64_t k = 0; k < nd; ++k)
             if (!free_mask[k]) q[k] = 0.0;
@@ -579,6 +684,53 @@ static int pcg_single_reduction(const orc_grid* g, int64_t np, const double* x, 
         }
         gamma_old = gamma;
         alpha_old = alpha;
+    }
+    return ORC_OK;
+}
+
+/* Standard Jacobi PCG on H dx = -g over the free DOFs (stops per DESIGN.md R6, R7). */
+static int pcg_standard(const orc_grid* g, int64_t np, const double* x, const double* F, const double* V0,
+                        const int32_t* mat, const double* E, const double* nu, double dt, const double* mi,
+                        const double* u, const double* gr, const double* dg, const uint8_t* free_mask,
+                        const orc_newton_settings* st, double gn, int64_t nd, double* xs, double* r, double* z,
+                        double* pv, double* q, orc_solve_stats* stats, int psd)
+{
+    int rc;
+    for (int64_t k = 0; k < nd; ++k) {
+        xs[k] = 0.0;
+        r[k] = free_mask[k] ? -gr[k] : 0.0;
+        z[k] = r[k] / dg[k];
+        pv[k] = z[k];
+    }
+    double rz = dot_free(nd, free_mask, r, z);
+    for (int cg = 0; cg < st->max_cg; ++cg) {
+        double rn = sqrt(dot_free(nd, free_mask, r, r));
+        if (!st->fixed_iters && rn <= st->cg_rtol * gn) break;
+        rc = orc_hvp_ex(g, np, x, F, V0, mat, E, nu, dt, mi, u, pv, NULL, q, psd);
+        if (rc) return rc;
+        for (int64_t k = 0; k < nd; ++k)
+            if (!free_mask[k]) q[k] = 0.0;
+        stats->cg_iters++;
+        double pq = dot_free(nd, free_mask, pv, q);
+        if (!(pq > 0.0)) {
+            /* non-positive curvature: stop with the current iterate, or the preconditioned
+             * steepest-descent direction -diag^-1 g if it is the first (R7; the same in
+             * fixed-iteration mode, whose remaining iterations then leave xs unchanged) */
+            if (cg == 0)
+                for (int64_t k = 0; k < nd; ++k) xs[k] = z[k];
+            stats->negcurv++;
+            break;
+        }
+        double alpha = rz / pq;
+        for (int64_t k = 0; k < nd; ++k) {
+            xs[k] += alpha * pv[k];
+            r[k] -= alpha * q[k];
+            z[k] = free_mask[k] ? r[k] / dg[k] : 0.0;
+        }
+        double rz_new = dot_free(nd, free_mask, r, z);
+        double beta = (rz > 0.0) ? rz_new / rz : 0.0;
+        rz = rz_new;
+        for (int64_t k = 0; k < nd; ++k) pv[k] = z[k] + beta * pv[k];
     }
     return ORC_OK;
 }
@@ -631,54 +783,30 @@ int orc_implicit_solve(const orc_grid* g, int64_t np, const double* x, const dou
             converged = 1;
             break;
         }
-        rc = orc_diag(g, np, x, F, V0, mat, E, nu, dt, mi, u, dg);
-        if (rc) goto done;
-        for (int64_t k = 0; k < nd; ++k)
-            if (!free_mask[k]) dg[k] = 1.0;
-        if (st->cg_variant == 1) {
-            rc = pcg_single_reduction(g, np, x, F, V0, mat, E, nu, dt, mi, u, gr, dg, free_mask, st, gn, nd, xs,
-                                      r, z, pv, q, ut, stats);
-            if (rc) goto done;
-            goto line_search;
-        }
-        /* Jacobi PCG on H dx = -g over the free DOFs */
-        for (int64_t k = 0; k < nd; ++k) {
-            xs[k] = 0.0;
-            r[k] = free_mask[k] ? -gr[k] : 0.0;
-            z[k] = r[k] / dg[k];
-            pv[k] = z[k];
-        }
-        double rz = dot_free(nd, free_mask, r, z);
-        for (int cg = 0; cg < st->max_cg; ++cg) {
-            double rn = sqrt(dot_free(nd, free_mask, r, r));
-            if (!st->fixed_iters && rn <= st->cg_rtol * gn) break;
-            rc = orc_hvp(g, np, x, F, V0, mat, E, nu, dt, mi, u, pv, NULL, q);
+        /* the Newton direction: Jacobi PCG (standard or single-reduction, R22), with the per-particle
+         * tangent blocks projected to PSD always (psd = 2) or, psd = 1, in a second solve when the first
+         * direction fails the descent check g . dx < 0 (R23) */
+        for (int psd_now = (st->psd == 2);;) {
+            rc = orc_diag_ex(g, np, x, F, V0, mat, E, nu, dt, mi, u, dg, psd_now);
             if (rc) goto done;
             for (int64_t k = 0; k < nd; ++k)
-                if (!free_mask[k]) q[k] = 0.0;
-            stats->cg_iters++;
-            double pq = dot_free(nd, free_mask, pv, q);
-            if (!(pq > 0.0)) {
-                /* non-positive curvature: stop with the current iterate, or the preconditioned
-                 * steepest-descent direction -diag^-1 g if it is the first (R7; the same in
-                 * fixed-iteration mode, whose remaining iterations then leave xs unchanged) */
-                if (cg == 0)
-                    for (int64_t k = 0; k < nd; ++k) xs[k] = z[k];
-                stats->negcurv++;
-                break;
+                if (!free_mask[k]) dg[k] = 1.0;
+            /* projected solves use the standard PCG (as the GPU path, whose projected HVP yields no
+             * single-reduction curvature partials) */
+            if (st->cg_variant == 1 && !psd_now)
+                rc = pcg_single_reduction(g, np, x, F, V0, mat, E, nu, dt, mi, u, gr, dg, free_mask, st, gn, nd, xs,
+                                          r, z, pv, q, ut, stats, psd_now);
+            else
+                rc = pcg_standard(g, np, x, F, V0, mat, E, nu, dt, mi, u, gr, dg, free_mask, st, gn, nd, xs, r, z,
+                                  pv, q, stats, psd_now);
+            if (rc) goto done;
+            if (psd_now) stats->psd_solves++;
+            if (st->psd == 1 && !psd_now && !(dot_free(nd, free_mask, gr, xs) < 0.0)) {
+                psd_now = 1;
+                continue;
             }
-            double alpha = rz / pq;
-            for (int64_t k = 0; k < nd; ++k) {
-                xs[k] += alpha * pv[k];
-                r[k] -= alpha * q[k];
-                z[k] = free_mask[k] ? r[k] / dg[k] : 0.0;
-            }
-            double rz_new = dot_free(nd, free_mask, r, z);
-            double beta = (rz > 0.0) ? rz_new / rz : 0.0;
-            rz = rz_new;
-            for (int64_t k = 0; k < nd; ++k) pv[k] = z[k] + beta * pv[k];
+            break;
         }
-    line_search:;
         /* backtracking line search: halve alpha from 1 until E decreases (Z10) */
         double E0, Ea0, Et, Eat;
         rc = orc_energy(g, np, x, F, V0, mat, E, nu, dt, mi, vn, fext, u, &E0, &Ea0);

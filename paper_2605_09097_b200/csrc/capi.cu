@@ -321,6 +321,7 @@ osmpm_status osmpm_implicit_solve(osmpm_subdomain* sub, const osmpm_newton_setti
     CHECK_ARG(settings, "settings is NULL");
     CHECK_ARG(settings->max_newton >= 0 && settings->max_cg >= 0, "negative iteration caps");
     CHECK_ARG(settings->cg_variant == 0 || settings->cg_variant == 1, "cg_variant must be 0 or 1");
+    CHECK_ARG(settings->psd >= 0 && settings->psd <= 2, "psd must be 0, 1 or 2");
     SUB_CALL(sub, implicit_solve(settings, stats));
 }
 osmpm_status osmpm_read_grid_velocity(osmpm_subdomain* sub, double* v, osmpm_memspace space)

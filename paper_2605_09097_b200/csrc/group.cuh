@@ -249,6 +249,46 @@ osmpm_status group_hvp(SlabGroup<D, R> G)
     return OSMPM_OK;
 }
 
+// R23: switch the group's HVP and Jacobi diagonal to the PSD-projected tangent blocks at the current u
+template <int D, typename R>
+osmpm_status group_psd_prepare(SlabGroup<D, R> G)
+{
+    for (int i = 0; i < G.ns; ++i) OSMPM_TRY(G.s[i]->psd_scatter());
+    OSMPM_TRY(halo_sum<D, R>(G, {{&Sub<D, R>::dg, D}}));
+    for (int i = 0; i < G.ns; ++i) {
+        Sub<D, R>* q = G.s[i];
+        q->KC();
+        k_add_mass_diag<<<nblk_all(q->box.nnodes, 256), 256, 0, G.st>>>(q->box.nnodes, D, q->m.p,
+                                                                          1.0 / (q->dt * q->dt), q->dg.p);
+        OSMPM_LAUNCH_CHECK();
+        q->psd_active = true;
+    }
+    return OSMPM_OK;
+}
+
+// g . x over the free owned DOFs of the group (the descent check of R23)
+template <int D, typename R>
+osmpm_status group_dot_gx(SlabGroup<D, R> G, double* out)
+{
+    GroupBufs& gb = *G.gb;
+    int64_t off = 0;
+    for (int i = 0; i < G.ns; ++i) {
+        Sub<D, R>* q = G.s[i];
+        const int64_t ndof = q->box.nnodes * D;
+        q->KC();
+        k_dot_free<<<nblk(ndof, 256), 256, 0, G.st>>>(ndof, q->nown * D, q->fmask.p, q->g.p, q->xs.p,
+                                                       gb.partB.p + off);
+        off += nblk(ndof, 256);
+    }
+    G.s[0]->KC();
+    k_final_sum<1><<<1, 1024, 0, G.st>>>(gb.partB.p, (int)off, gb.scal.p + 20);
+    OSMPM_LAUNCH_CHECK();
+    OSMPM_TRY(group_allreduce<D, R>(G, gb.scal.p + 20, 1));
+    OSMPM_CU(cudaMemcpyAsync(out, gb.scal.p + 20, sizeof(double), cudaMemcpyDeviceToHost, G.st));
+    OSMPM_CU(cudaStreamSynchronize(G.st));
+    return OSMPM_OK;
+}
+
 // ---------------------------------------------------------------------------------------------
 // a3-a7: Newton-PCG with backtracking line search over the group (DESIGN.md
 // R5-R8).  CG scalars live on the device (gb.cgs); a CG iteration has no host synchronisation.
@@ -347,7 +387,10 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
             converged = true;
             break;
         }
-        if (s->cg_variant == 1) {
+        // the Newton direction (R6, R7, R22, R23): PCG with the exact tangent, or with the
+        // PSD-projected one always (psd = 2) / when the first direction fails the descent check (psd = 1)
+        auto run_pcg = [&](int variant) -> osmpm_status {
+        if (variant == 1) {
             // single-reduction PCG (Chronopoulos-Gear, R22): one reduction / all-reduce per iteration
             int64_t off = 0;
             for (int i = 0; i < G.ns; ++i) {
@@ -502,6 +545,24 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
                 OSMPM_CU(cudaMemcpyAsync(q->xs.p, q->z.p, q->box.nnodes * D * sizeof(double),
                                          cudaMemcpyDeviceToDevice, st));
             }
+            return OSMPM_OK;
+        };
+        if (s->psd == 2) {
+            OSMPM_TRY(group_psd_prepare<D, R>(G));
+            sts->psd_solves++;
+        }
+        // the projected HVP produces no curvature partials: projected solves use the standard PCG
+        OSMPM_TRY(run_pcg(s->psd == 2 ? 0 : s->cg_variant));
+        if (s->psd == 1) {
+            double gx = 0.0;
+            OSMPM_TRY(group_dot_gx<D, R>(G, &gx));
+            if (!(gx < 0.0)) {
+                OSMPM_TRY(group_psd_prepare<D, R>(G));
+                sts->psd_solves++;
+                OSMPM_TRY(run_pcg(0));
+            }
+        }
+        for (int i = 0; i < G.ns; ++i) G.s[i]->psd_active = false;
         // backtracking line search (R8)
         double alpha = 1.0, Et = 0.0, Eat = 0.0;
         bool at_floor = false, ls_fail = false;

@@ -650,6 +650,16 @@ __global__ void k_cgs_update(int64_t ndof, int64_t nown_dof, const uint8_t* __re
     block_reduce_store<3>(red, partials);
 }
 
+// partials of a . b over the free owned DOFs
+__global__ void k_dot_free(int64_t ndof, int64_t nown_dof, const uint8_t* __restrict__ fm, const double* __restrict__ a,
+                           const double* __restrict__ b, double* __restrict__ partials)
+{
+    double red[1] = {0.0};
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ndof; k += (int64_t)gridDim.x * blockDim.x)
+        if (fm[k] && k < nown_dof) red[0] += a[k] * b[k];
+    block_reduce_store<1>(red, partials);
+}
+
 // ut = u + alpha x on free DOFs
 __global__ void k_axpy_free(int64_t ndof, const uint8_t* __restrict__ fm, const double* __restrict__ u, double alpha,
                             const double* __restrict__ x, double* __restrict__ ut)

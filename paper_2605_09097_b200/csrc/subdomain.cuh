@@ -11,6 +11,7 @@
 
 #include "kernels.cuh"
 #include "radix_sort.cuh"
+#include "psd.cuh"
 #include "runtime.h"
 
 namespace osmpm {
@@ -142,6 +143,8 @@ struct Sub : public osmpm_subdomain {
     DirList dir_user, dir_cpl;
     DBuf<double> stage_io;  // persistent host-I/O staging buffer
     DBuf<int> pi_gd;  // dense-box dims on the device when this subdomain is Pi's coarse side (transmit.cuh)
+    DBuf<double> Tpsd;        // PSD-projected tangent blocks (psd.cuh), packed, field-major
+    bool psd_active = false;  // the HVP of the current PCG solve uses them (R23)
     DBuf<double> det_a, det_b, det_c;  // per-tile node blocks of the deterministic scatter mode (hvp_sw.cuh)
 
     // OSMPM_DETERMINISTIC=1: the sliding-window gradient and HVP store per-tile node blocks that a
@@ -698,6 +701,16 @@ struct Sub : public osmpm_subdomain {
     {
         auto& pf = ctx->prof;
         if (pf.on) pf.begin("hvp", st());
+        if (psd_active) {
+            // projected-tangent variant (psd.cuh): per-particle scatter; the single-reduction PCG's
+            // curvature partials are not produced here, so psd solves use the standard PCG
+            if (n > 0) {
+                KC(); k_hvp_psd<D, R><<<nblk_all(n, 128), 128, 0, st()>>>(P.p, cap, n, box, Tpsd.p, din, yout);
+            }
+            OSMPM_LAUNCH_CHECK();
+            if (pf.on) pf.end("hvp", st());
+            return OSMPM_OK;
+        }
         static bool attr3 = false;
         if (!attr3) {
             cudaFuncSetAttribute(k_hvp_sw<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -723,6 +736,20 @@ struct Sub : public osmpm_subdomain {
         }
         OSMPM_LAUNCH_CHECK();
         if (pf.on) pf.end("hvp", st());
+        return OSMPM_OK;
+    }
+
+    // R23: projected tangents at the current u, and the Jacobi diagonal they give (particle part; the
+    // group adds the halo and the mass term)
+    osmpm_status psd_scatter()
+    {
+        OSMPM_TRY(Tpsd.need((size_t)PSD<D>::NP * cap));
+        OSMPM_CU(cudaMemsetAsync(dg.p, 0, box.nnodes * D * sizeof(double), st()));
+        if (n > 0) {
+            KC(); k_psd_tangent<D, R><<<nblk_all(n, 128), 128, 0, st()>>>(P.p, cap, n, mat.p, box, mats, u.p, Tpsd.p);
+            KC(); k_diag_psd<D, R><<<nblk_all(n, 128), 128, 0, st()>>>(P.p, cap, n, box, Tpsd.p, dg.p);
+        }
+        OSMPM_LAUNCH_CHECK();
         return OSMPM_OK;
     }
 

@@ -49,14 +49,14 @@ class NewtonSettings(C.Structure):
     _fields_ = [("max_newton", C.c_int32), ("max_cg", C.c_int32), ("fixed_iters", C.c_int32), ("guess", C.c_int32),
                 ("newton_rtol", C.c_double), ("newton_atol", C.c_double), ("cg_rtol", C.c_double),
                 ("ls_min_alpha", C.c_double), ("energy_noise_rtol", C.c_double), ("cg_variant", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("psd", C.c_int32)]
 
 
 class SolveStats(C.Structure):
     _fields_ = [("newton_iters", C.c_int32), ("cg_iters", C.c_int32), ("ls_halvings", C.c_int32),
                 ("status", C.c_int32), ("grad_norm0", C.c_double), ("grad_norm", C.c_double),
                 ("energy", C.c_double), ("negcurv", C.c_int32), ("ls_failures", C.c_int32),
-                ("floor_accept", C.c_int32), ("reserved", C.c_int32)]
+                ("floor_accept", C.c_int32), ("psd_solves", C.c_int32)]
 
 
 class SchwarzSettings(C.Structure):
@@ -112,9 +112,10 @@ def sort_pairs(ctx, keys, vals, nbits):
 
 
 def newton_settings(max_newton=50, max_cg=1000, fixed_iters=0, guess=0, newton_rtol=1e-8, newton_atol=0.0,
-                    cg_rtol=1e-8, ls_min_alpha=2.0 ** -20, energy_noise_rtol=1e-13, cg_variant=0) -> NewtonSettings:
+                    cg_rtol=1e-8, ls_min_alpha=2.0 ** -20, energy_noise_rtol=1e-13, cg_variant=0,
+                    psd=0) -> NewtonSettings:
     return NewtonSettings(max_newton, max_cg, fixed_iters, guess, newton_rtol, newton_atol, cg_rtol, ls_min_alpha,
-                          energy_noise_rtol, cg_variant, 0)
+                          energy_noise_rtol, cg_variant, psd)
 
 
 # --------------------------------------------------------------------------------------------
