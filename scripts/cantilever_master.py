@@ -34,11 +34,11 @@ L, H, E, NU, RHO = 1.0, 0.2, 1.0e5, 0.4, 1000.0
 Y0 = 1.0
 
 
-def newton(guess=1):
+def newton(guess=1, rtol=1e-8):
     """guess 1: u = 0 (a single load step from rest); guess 0: u = dt v^n, the previous frame's increment
     (progressive loading: each load level starts from the previous equilibrium's increment)."""
     from paper_2605_09097_b200 import osmpm
-    return osmpm.newton_settings(newton_rtol=1e-8, newton_atol=0.0, cg_rtol=1e-10, max_cg=40000, max_newton=60,
+    return osmpm.newton_settings(newton_rtol=rtol, newton_atol=0.0, cg_rtol=1e-10, max_cg=40000, max_newton=100,
                                  guess=guess, energy_noise_rtol=1e-12)
 
 
@@ -61,7 +61,7 @@ def clamp_nodes(grid):
     return (ci[:, None] * ny + np.arange(ny)[None, :]).reshape(-1).astype(np.int64)
 
 
-def run_single(dx, gammas, dT=10.0, guess=1):
+def run_single(dx, gammas, dT=10.0, guess=1, rtol=1e-8):
     from paper_2605_09097_b200 import osmpm
     sc = synth.cantilever_single(dx, L=L, H=H, E=E, nu=NU, rho=RHO, dT=dT, y0=Y0)
     ctx = osmpm.Context(0)
@@ -74,7 +74,11 @@ def run_single(dx, gammas, dT=10.0, guess=1):
         sub.set_gravity((0.0, -g, 0.0))
         t0 = time.time()
         sub.p2g()
-        st = sub.implicit_solve(newton(guess))
+        try:
+            st = sub.implicit_solve(newton(guess, rtol))
+        except osmpm.OsmpmError as e:
+            out.append({"gamma": G, "error": str(e)})
+            break
         sub.g2p()
         x = sub.read_particles(fields=("x",))["x"]
         W, Hh = measure(sc.particles.x, x, dx)
@@ -85,7 +89,7 @@ def run_single(dx, gammas, dT=10.0, guess=1):
     return out
 
 
-def run_dual(dx_b, gammas, r=4, dT=10.0, M=1, k_max=2000, guess=1):
+def run_dual(dx_b, gammas, r=4, dT=10.0, M=1, k_max=2000, guess=1, rtol=1e-8):
     from paper_2605_09097_b200 import osmpm
     coarse, fine = synth.cantilever_pair(dx_b, r=r, L=L, H=H, E=E, nu=NU, rho=RHO, dT=dT, M=M, y0=Y0)
     ctx = osmpm.Context(0)
@@ -93,7 +97,7 @@ def run_dual(dx_b, gammas, r=4, dT=10.0, M=1, k_max=2000, guess=1):
     ss = osmpm.Subdomain(ctx, fine.grid, fine.dt, fine.particles, fine.materials, fine.gravity)
     cl = clamp_nodes(fine.grid)
     ss.set_dirichlet(cl, np.full(cl.size, 3, np.uint8), np.zeros((cl.size, 2)))
-    ns = newton(guess)
+    ns = newton(guess, rtol)
     cpl = osmpm.Coupler(sb, ss, osmpm.schwarz_settings(M=M, eps_conv=1e-5, k_max=k_max, coarse=ns, fine=ns))
     out = []
     for G in gammas:
@@ -130,6 +134,8 @@ if __name__ == "__main__":
     ap.add_argument("--gammas", type=float, nargs="+", default=[0.03, 0.1, 0.3, 1.0, 3.0])
     ap.add_argument("--dT", type=float, default=10.0)
     ap.add_argument("--no-dual", action="store_true")
+    ap.add_argument("--guess", type=int, default=1)
+    ap.add_argument("--rtol", type=float, default=1e-8)
     a = ap.parse_args()
     if a.mode == "res":
         G = [0.05]
@@ -144,8 +150,8 @@ if __name__ == "__main__":
     else:
         for dxb in a.dxb:
             line = {"mode": "curve", "dx_B": dxb, "elastica": [elastica_row(G) for G in a.gammas],
-                    "single": run_single(dxb, a.gammas, a.dT, guess=0)}
+                    "single": run_single(dxb, a.gammas, a.dT, guess=a.guess, rtol=a.rtol)}
             print(json.dumps(line), flush=True)
             if not a.no_dual:
-                line["dual"] = run_dual(dxb, a.gammas, dT=a.dT, guess=0)
+                line["dual"] = run_dual(dxb, a.gammas, dT=a.dT, guess=a.guess, rtol=a.rtol)
                 print(json.dumps(line), flush=True)
