@@ -306,6 +306,26 @@ osmpm_status osmpm_transmit(osmpm_subdomain* src, osmpm_subdomain* dst, osmpm_di
 osmpm_status osmpm_coupler_create(osmpm_subdomain* coarse, osmpm_subdomain* fine,
                                   const osmpm_schwarz_settings* settings, osmpm_coupler** out);
 void osmpm_coupler_destroy(osmpm_coupler* cpl);
+/* Host only (no GPU): the coupler's receiver decision for one fine node box -- the whole fine subdomain,
+ * or one slab of it with its two ghost planes (R21) -- exposed so that the distributed
+ * arbitration can be tested without GPUs.  Gamma_S candidates are the box nodes with active_s and
+ * mb_s > tau_s (Eq. boundary_grid_set); a candidate coinciding with a coarse node
+ * flagged in gamma_b is arbitrated by raw nodal mass, ties to B (Eq. overlap_donor):
+ * if B donates, drop_b[that coarse box node] is set to 1 (the fine side receives), else the candidate is
+ * dropped; a remaining candidate is a fine receiver if every coarse stencil node with N > 0 is active
+ * (R13).  Boxes: node k = lo + l, box-local index (l0 * dims1 + l1) * dims2 + l2 (2D: dims[2]
+ * ignored); all per-node arrays are over the box.  recv (capacity n_cap; NULL: count only) receives the
+ * dense fine node indices of the receivers, ascending; owned[q] = 1 if its box-local index is < nown
+ * (the slab owns it; ghost-plane nodes come after the owned ones).  Errors: INVALID_ARG (NULL, dims,
+ * capacity). */
+osmpm_status osmpm_schwarz_receivers_host(const osmpm_grid_desc* coarse, const int64_t coarse_lo[3],
+                                          const int64_t coarse_dims[3], const double* m_b, const uint8_t* gamma_b,
+                                          const uint8_t* active_b, const osmpm_grid_desc* fine,
+                                          const int64_t fine_lo[3], const int64_t fine_dims[3], int64_t nown,
+                                          const double* m_s, const double* mb_s, const uint8_t* active_s,
+                                          double tau_s, uint8_t* drop_b, int64_t n_cap, int64_t* recv,
+                                          uint8_t* owned, int64_t* n_recv);
+
 /* Step 0 of Alg. 1: store fine particles, P2G both, Gamma_B, Gamma_S,
  * arbitration, receivers, v_Gamma_B^(0) = Pi(v_S^n).  Called by schwarz_step; exposed so a caller
  * can drive sub-steps itself. */

@@ -431,6 +431,46 @@ osmpm_status osmpm_transmit(osmpm_subdomain* src, osmpm_subdomain* dst, osmpm_di
 #undef TR
 }
 
+osmpm_status osmpm_schwarz_receivers_host(const osmpm_grid_desc* coarse, const int64_t coarse_lo[3],
+                                          const int64_t coarse_dims[3], const double* m_b, const uint8_t* gamma_b,
+                                          const uint8_t* active_b, const osmpm_grid_desc* fine,
+                                          const int64_t fine_lo[3], const int64_t fine_dims[3], int64_t nown,
+                                          const double* m_s, const double* mb_s, const uint8_t* active_s,
+                                          double tau_s, uint8_t* drop_b, int64_t n_cap, int64_t* recv,
+                                          uint8_t* owned, int64_t* n_recv)
+{
+    CHECK_ARG(coarse && fine && coarse_lo && coarse_dims && fine_lo && fine_dims && m_b && gamma_b && active_b &&
+                  m_s && mb_s && active_s && drop_b && n_recv,
+              "NULL argument");
+    CHECK_ARG(coarse->dim == fine->dim && (coarse->dim == 2 || coarse->dim == 3), "dim must be 2 or 3 on both");
+    auto mk = [](const osmpm_grid_desc* g, const int64_t* lo, const int64_t* nn) {
+        HostBox h{};
+        h.d = g->dim;
+        h.dx = g->dx;
+        for (int a = 0; a < 3; ++a) {
+            h.o[a] = g->origin[a];
+            h.gd[a] = a < g->dim ? g->dims[a] : 1;
+            h.lo[a] = a < g->dim ? lo[a] : 0;
+            h.nn[a] = a < g->dim ? nn[a] : 1;
+        }
+        return h;
+    };
+    std::map<int64_t, char> cand;
+    fine_box_receivers(mk(coarse, coarse_lo, coarse_dims), m_b, gamma_b, active_b, mk(fine, fine_lo, fine_dims), nown,
+                       m_s, mb_s, active_s, tau_s, drop_b, cand);
+    *n_recv = (int64_t)cand.size();
+    CHECK_ARG((int64_t)cand.size() <= n_cap || !recv, "receiver capacity n_cap too small");
+    if (recv) {
+        int64_t q = 0;
+        for (auto& kv : cand) {
+            recv[q] = kv.first;
+            if (owned) owned[q] = (uint8_t)kv.second;
+            ++q;
+        }
+    }
+    return OSMPM_OK;
+}
+
 osmpm_status osmpm_coupler_create(osmpm_subdomain* coarse, osmpm_subdomain* fine,
                                   const osmpm_schwarz_settings* settings, osmpm_coupler** out)
 {

@@ -33,6 +33,113 @@ __global__ void k_lerp(int64_t n, const double* __restrict__ a, const double* __
     if (i < n) out[i] = (1.0 - alpha) * a[i] + alpha * b[i];
 }
 
+// ---------------------------------------------------------------------------------------------
+// Host logic of one fine node box (a whole fine subdomain, or one slab with its ghost planes; R21):
+// Gamma_S candidates (active, m^∂ > tau_S; Eq. boundary_grid_set), the arbitration of nodes that
+// coincide with a coarse Gamma_B node (Eq. overlap_donor: the larger raw nodal mass donates, ties -> B;
+// R12) and the eligibility of fine receivers (every coarse stencil node with N > 0 active; R13).
+// Boxes: node (l0,l1,l2) of a box = dense node lo + l, box-local index (l0*n1 + l1)*n2 + l2.
+// Out: dropB[I] |= 1 for coarse Gamma_B nodes a fine node takes over (B donates); cand[g] = owned?
+// for the fine receivers (dense index g), owned = box-local index < nown.
+// ---------------------------------------------------------------------------------------------
+struct HostBox {
+    int d;
+    double o[3], dx;
+    int64_t gd[3], lo[3], nn[3];
+    int64_t nodes() const { return nn[0] * nn[1] * (d == 3 ? nn[2] : 1); }
+    // box-local index of dense node k (or -1)
+    int64_t local(const int64_t* k) const
+    {
+        int64_t l[3] = {0, 0, 0};
+        for (int a = 0; a < d; ++a) {
+            l[a] = k[a] - lo[a];
+            if (k[a] < 0 || k[a] >= gd[a] || l[a] < 0 || l[a] >= nn[a]) return -1;
+        }
+        return d == 3 ? (l[0] * nn[1] + l[1]) * nn[2] + l[2] : l[0] * nn[1] + l[1];
+    }
+    int64_t dense(int64_t i, int64_t* k) const
+    {
+        int64_t l[3] = {0, 0, 0};
+        if (d == 3) {
+            l[2] = i % nn[2];
+            l[1] = (i / nn[2]) % nn[1];
+            l[0] = i / (nn[2] * nn[1]);
+        } else {
+            l[1] = i % nn[1];
+            l[0] = i / nn[1];
+        }
+        for (int a = 0; a < 3; ++a) k[a] = a < d ? lo[a] + l[a] : 0;
+        for (int a = 0; a < d; ++a)
+            if (k[a] >= gd[a]) return -1;
+        return d == 3 ? (k[0] * gd[1] + k[1]) * gd[2] + k[2] : k[0] * gd[1] + k[1];
+    }
+};
+
+static inline double bspline_host(double f, int o)
+{
+    if (o == 0) return 0.5 * (1.5 - f) * (1.5 - f);
+    if (o == 1) return 0.75 - (f - 1.0) * (f - 1.0);
+    return 0.5 * (f - 0.5) * (f - 0.5);
+}
+
+inline void fine_box_receivers(const HostBox& Bx, const double* mB, const uint8_t* hatB, const uint8_t* actB,
+                               const HostBox& Sx, int64_t nown, const double* mS, const double* mbS,
+                               const uint8_t* actS, double tauS, uint8_t* dropB, std::map<int64_t, char>& cand)
+{
+    const int D = Sx.d;
+    const double tol = 1e-9 * std::min(Bx.dx, Sx.dx);
+    for (int64_t i = 0; i < Sx.nodes(); ++i) {
+        if (!(actS[i] && mbS[i] > tauS)) continue;
+        int64_t k[3];
+        const int64_t g = Sx.dense(i, k);
+        if (g < 0) continue;
+        const bool owned = i < nown;
+        bool keep = true;
+        int64_t kk[3] = {0, 0, 0};
+        bool coincide = true;
+        for (int a = 0; a < D; ++a) {
+            const double x = Sx.o[a] + Sx.dx * (double)k[a];
+            const double X = (x - Bx.o[a]) / Bx.dx;
+            kk[a] = (int64_t)std::llround(X);
+            if (std::fabs(X - (double)kk[a]) * Bx.dx > tol || kk[a] < 0 || kk[a] >= Bx.gd[a]) coincide = false;
+        }
+        if (coincide) {
+            const int64_t I = Bx.local(kk);
+            if (I >= 0 && hatB[I]) {
+                if (mB[I] >= mS[i])
+                    dropB[I] = 1;  // B donates: S receives
+                else
+                    keep = false;  // S donates: B receives
+            }
+        }
+        if (!keep) continue;
+        double f[3];
+        int64_t base[3] = {0, 0, 0};
+        for (int a = 0; a < D; ++a) {
+            const double x = Sx.o[a] + Sx.dx * (double)k[a];
+            const double X = (x - Bx.o[a]) / Bx.dx;
+            base[a] = (int64_t)std::floor(X - 0.5);
+            f[a] = X - (double)base[a];
+        }
+        bool ok = true;
+        for (int o0 = 0; o0 < 3 && ok; ++o0)
+            for (int o1 = 0; o1 < 3 && ok; ++o1)
+                for (int o2 = 0; o2 < (D == 3 ? 3 : 1) && ok; ++o2) {
+                    const int off[3] = {o0, o1, o2};
+                    double w = 1.0;
+                    for (int a = 0; a < D; ++a) w *= bspline_host(f[a], off[a]);
+                    if (!(w > 0.0)) continue;
+                    int64_t kc[3] = {0, 0, 0};
+                    for (int a = 0; a < D; ++a) kc[a] = base[a] + off[a];
+                    const int64_t I = Bx.local(kc);
+                    if (I < 0 || !actB[I]) ok = false;
+                }
+        if (!ok) continue;
+        char& o = cand[g];  // a node seen by two local slabs: owned if either owns it
+        o = (char)(o || owned);
+    }
+}
+
 template <int D, typename R>
 struct Coupler : public osmpm_coupler {
     Sub<D, R>* B = nullptr;   // coarse subdomain: never decomposed (replicated on every rank)
@@ -105,11 +212,18 @@ struct Coupler : public osmpm_coupler {
         return (D == 3) ? (k[0] * s->gdims[1] + k[1]) * s->gdims[2] + k[2] : k[0] * s->gdims[1] + k[1];
     }
 
-    static double bsw(double f, int o)
+    static HostBox host_box(const Sub<D, R>* s)
     {
-        if (o == 0) return 0.5 * (1.5 - f) * (1.5 - f);
-        if (o == 1) return 0.75 - (f - 1.0) * (f - 1.0);
-        return 0.5 * (f - 0.5) * (f - 0.5);
+        HostBox h{};
+        h.d = D;
+        h.dx = s->dx;
+        for (int a = 0; a < 3; ++a) {
+            h.o[a] = s->origin[a];
+            h.gd[a] = s->gdims[a];
+            h.lo[a] = a < D ? s->box.lo[a] : 0;
+            h.nn[a] = a < D ? s->box.nn[a] : 1;
+        }
+        return h;
     }
 
     // ------------------------------------------------------------------------------------------
@@ -153,8 +267,8 @@ struct Coupler : public osmpm_coupler {
             OSMPM_CU(cudaStreamSynchronize(st()));
         }
         // fine Gamma_S candidates on every local slab's whole box (dense index -> owned?)
-        const double tol = 1e-9 * std::min(B->dx, fine_dx());
-        std::map<int64_t, char> candS;  // dense index -> owned by this rank
+        std::map<int64_t, char> candS;
+        const HostBox Bx = host_box(B);
         for (int si = 0; si < G.ns; ++si) {
             Sub<D, R>* S = G.s[si];
             std::vector<double> mS, mbS;
@@ -163,67 +277,8 @@ struct Coupler : public osmpm_coupler {
             OSMPM_TRY(d2h(mbS, S->mb.p, S->box.nnodes, st()));
             OSMPM_TRY(d2h(aS, S->act.p, S->box.nnodes, st()));
             OSMPM_CU(cudaStreamSynchronize(st()));
-            for (int64_t i = 0; i < S->box.nnodes; ++i) {
-                if (!(aS[i] && mbS[i] > tauS)) continue;
-                int64_t k[3];
-                const int64_t g = dense_of_box(S, i, k);
-                if (g < 0) continue;
-                const bool owned = i < S->nown;
-                // coincident coarse node?  ambiguous overlap node (Eq. overlap_donor): donor = larger nodal
-                // mass, ties -> B
-                bool keep = true;
-                int64_t kk[3] = {0, 0, 0};
-                bool coincide = true;
-                for (int a = 0; a < D; ++a) {
-                    const double x = S->origin[a] + S->dx * (double)k[a];
-                    const double X = (x - B->origin[a]) / B->dx;
-                    kk[a] = (int64_t)std::llround(X);
-                    if (std::fabs(X - (double)kk[a]) * B->dx > tol || kk[a] < 0 || kk[a] >= B->gdims[a]) coincide = false;
-                }
-                if (coincide) {
-                    const int64_t gI =
-                        (D == 3) ? (kk[0] * B->gdims[1] + kk[1]) * B->gdims[2] + kk[2] : kk[0] * B->gdims[1] + kk[1];
-                    const int64_t I = box_of(B, gI);
-                    if (I >= 0 && hatB[I]) {
-                        if (mB[I] >= mS[i])
-                            dropB[I] = 1;  // B donates: S receives
-                        else
-                            keep = false;  // S donates: B receives
-                    }
-                }
-                if (!keep) continue;
-                // fine receivers need an active coarse stencil (R13)
-                double f[3];
-                int64_t base[3] = {0, 0, 0};
-                for (int a = 0; a < D; ++a) {
-                    const double x = S->origin[a] + S->dx * (double)k[a];
-                    const double X = (x - B->origin[a]) / B->dx;
-                    base[a] = (int64_t)std::floor(X - 0.5);
-                    f[a] = X - (double)base[a];
-                }
-                bool ok = true;
-                for (int o0 = 0; o0 < 3 && ok; ++o0)
-                    for (int o1 = 0; o1 < 3 && ok; ++o1)
-                        for (int o2 = 0; o2 < (D == 3 ? 3 : 1) && ok; ++o2) {
-                            const int off[3] = {o0, o1, o2};
-                            double w = 1.0;
-                            for (int a = 0; a < D; ++a) w *= bsw(f[a], off[a]);
-                            if (!(w > 0.0)) continue;
-                            int64_t kc[3] = {0, 0, 0};
-                            for (int a = 0; a < D; ++a) {
-                                kc[a] = base[a] + off[a];
-                                if (kc[a] < 0 || kc[a] >= B->gdims[a]) ok = false;
-                            }
-                            if (!ok) break;
-                            const int64_t gI = (D == 3) ? (kc[0] * B->gdims[1] + kc[1]) * B->gdims[2] + kc[2]
-                                                        : kc[0] * B->gdims[1] + kc[1];
-                            const int64_t I = box_of(B, gI);
-                            if (I < 0 || !aB[I]) ok = false;
-                        }
-                if (!ok) continue;
-                char& o = candS[g];  // a node seen by two local slabs: owned if either owns it
-                o = (char)(o || owned);
-            }
+            fine_box_receivers(Bx, mB.data(), hatB.data(), aB.data(), host_box(S), S->nown, mS.data(), mbS.data(),
+                               aS.data(), tauS, dropB.data(), candS);
         }
         if (multi()) {
             OSMPM_CU(cudaMemcpyAsync(flagsB.p, dropB.data(), B->box.nnodes, cudaMemcpyHostToDevice, st()));
