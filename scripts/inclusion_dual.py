@@ -50,11 +50,11 @@ def static_settings():
 
 
 def dynamic_settings():
+    """Inexact Newton per frame (fixed 3 x 300): near equilibrium the energy decrease of a Newton step falls
+    below the round-off floor of E_h and a tolerance-driven line search stagnates (R8), while
+    the relaxation only needs each frame's solve to be good enough to keep damping the motion."""
     from paper_2605_09097_b200 import osmpm
-    # near equilibrium |g| sits at its round-off floor: an absolute floor keeps a frame from running into
-    # the Newton cap there
-    return osmpm.newton_settings(newton_rtol=1e-6, newton_atol=1e-9, cg_rtol=1e-8, max_cg=20000, max_newton=50,
-                                 energy_noise_rtol=1e-12)
+    return osmpm.newton_settings(max_newton=3, max_cg=300, fixed_iters=1)
 
 
 def mirror_bc(grid):
