@@ -25,14 +25,8 @@
 
 namespace osmpm {
 
-// Threads (= particles per streamed chunk) of a k_hvp_sw CTA.  3D: 128 -- phase 1 one thread per
-// particle (a layer of 4 x 4 cells holds 128 at 8 ppc), phase 2 96 items (cell, x-offset i, half h),
-// each accumulating ALL three components over half of the cell's particles, so that a particle record
-// loaded from shared memory serves three components.  2D: Tile<2>::NT items (cell, a, i).
-template <int D> struct HvpNT {
-    static constexpr int NT = (D == 3) ? 128 : Tile<D>::NT;
-};
-template <int D> constexpr int HVP_NW = (HvpNT<D>::NT + 31) / 32;
+// warps per HVP CTA (the per-warp curvature partials of k_hvp_sw)
+template <int D> constexpr int HVP_NW = (Tile<D>::NT + 31) / 32;
 
 template <int D, typename R> struct SWRec {
     // G row a starts at GROW(a): 3D fp64 rows padded to 4 reals (16-B aligned: one 16-B + one 8-B load
@@ -90,13 +84,11 @@ __device__ __forceinline__ void sw_stage_tile(const BoxDev& b, const int* t, con
 {
     using T = Tile<D>;
     constexpr int ROWS = T::N0 * T::N1, RL = T::N2 * D;  // 3D: rows along z are contiguous in global memory
-    if constexpr (D == 3 && NTHR >= ROWS) {
+    if constexpr (D == 3 && NTHR % ROWS == 0) {
         // thread -> (row, part): one row base address per thread, then every TPR-th element of the row
-        // with its (node, component) advanced incrementally (no per-element index divisions); threads
-        // beyond ROWS * TPR stage nothing
+        // with its (node, component) advanced incrementally (no per-element index divisions)
         constexpr int TPR = NTHR / ROWS;
         const int row = threadIdx.x / TPR, part = threadIdx.x % TPR;
-        if (row < ROWS) {
         const int c0 = row / T::N1, c1 = row % T::N1;
         const double* gs = src + box_node<D>(b, t[0] * T::T0 + c0, t[1] * T::T1 + c1, t[2] * T::T2) * D;
         const int n0 = sw_node<D>(c0, c1, 0);
@@ -114,7 +106,6 @@ __device__ __forceinline__ void sw_stage_tile(const BoxDev& b, const int* t, con
                 a -= D;
                 z += 1;
             }
-        }
         }
     } else {
         for (int idx = threadIdx.x; idx < T::NN * D; idx += NTHR) {
@@ -157,10 +148,10 @@ static inline PFN_encodeTiled encode_tiled_fn()
 // slack + NT particles, rounded to 16 B).  The x block is padded to 128 B so that both blocks are
 // destinations of 2-D tensor copies (128-B aligned shared memory; the tensor start coordinate must
 // be 16-B aligned too: measured, scripts/tma_probe.cu).
-template <int D, typename R, int NCH = HvpNT<D>::NT> struct SWIn {
+template <int D, typename R> struct SWIn {
     static constexpr int NF = D + CL<D>::NF;
     static constexpr int UE = 16 / sizeof(R);
-    static constexpr int PFS = NCH + UE;
+    static constexpr int PFS = Tile<D>::NT + UE;
     static constexpr int XB = (int)(((D * PFS * sizeof(R) + 127) / 128 * 128) / sizeof(R));
     static constexpr int TOT = XB + CL<D>::NF * PFS;
     static __host__ __device__ constexpr int off(int f) { return f < D ? f * PFS : XB + (f - D) * PFS; }
@@ -187,7 +178,7 @@ constexpr size_t hvp_sw_smem_bytes()
     using T = Tile<D>;
     return 16 + 128 /* alignment of the streamed-input block */ + ((size_t)SW<D>::NNP * SVS<D, R>::S + SW<D>::STG +
                  (size_t)SWIn<D, R>::TOT +
-                 (size_t)SWRec<D, R>::RS * HvpNT<D>::NT) *
+                 (size_t)SWRec<D, R>::RS * T::NT) *
                     sizeof(R);
 }
 
@@ -286,13 +277,13 @@ __device__ __forceinline__ void sw_emit(int cellL, int a, int i, R* acc, R* stg)
 // With DOT, the flushing thread also accumulates d_node . (this tile's partial y_node) into dot: summed
 // over all tiles that is d^T K d, the PCG curvature (no separate pass over y), from d as staged in the
 // node tile (fp64) or re-read from global memory (fp32 tiles hold d rounded).
-template <int D, typename R, bool DOT, int NTH = Tile<D>::NT>
+template <int D, typename R, bool DOT>
 __device__ __forceinline__ void sw_flush(const BoxDev& b, const int* t, int plane, const R* stg,
                                          double* __restrict__ out, double* __restrict__ tb, const R* sv,
                                          const double* __restrict__ din, double& dot)
 {
     using T = Tile<D>;
-    for (int it = threadIdx.x; it < SW<D>::NITEM; it += NTH) {
+    for (int it = threadIdx.x; it < SW<D>::NITEM; it += T::NT) {
         // slot-major staging: consecutive threads read consecutive reals (conflict-free)
         R s = stg[it];
 #pragma unroll
@@ -385,7 +376,7 @@ __device__ __forceinline__ void sw_prefetch(const R* __restrict__ P, const R* __
     using In = SWIn<D, R>;
     static_assert(In::NF <= 32, "one field per lane");
     const int lb0 = lb & ~(In::UE - 1);                       // 16-B aligned start
-    const int cnt = min(le, lb + HvpNT<D>::NT) - lb0;
+    const int cnt = min(le, lb + Tile<D>::NT) - lb0;
     const uint32_t bytes = (uint32_t)((cnt + In::UE - 1) & ~(In::UE - 1)) * sizeof(R);
     fence_async_smem();
     if (lane == 0) mbar_expect_tx(bar, bytes * In::NF);
@@ -428,7 +419,7 @@ __device__ __forceinline__ void sw_prefetch_tmap(const CUtensorMap* mx, const CU
 // 3 CTAs per SM in fp64 (128 registers; shared memory 75 KB); the fp32 variant has half the shared
 // memory (records, streamed inputs, node tile and staging in fp32) and fewer live registers: 4
 template <int D, typename R>
-__global__ void __launch_bounds__(HvpNT<D>::NT, sizeof(R) == 8 ? 3 : 4)
+__global__ void __launch_bounds__(Tile<D>::NT, sizeof(R) == 8 ? 3 : 4)
 k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, const int* __restrict__ cell_start,
          BoxDev b, const double* __restrict__ din, double* __restrict__ yout, const __grid_constant__ CUtensorMap tmx,
          const __grid_constant__ CUtensorMap tmc, int use_tmap, double* __restrict__ tbuf,
@@ -442,8 +433,6 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
     using S = SW<D>;
     using SR = SWRec<D, R>;
     constexpr int RS = SR::RS;
-    constexpr int NTH = HvpNT<D>::NT;  // threads = particles per chunk
-    constexpr bool MERGED = D == 3;    // phase-2 items (cell, i, h) over all components (HvpNT)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
     R* sv = reinterpret_cast<R*>(smem_raw + 16);
@@ -484,9 +473,9 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                 sw_prefetch<D, R>(P, cache, cap, lb0, le0, pf, bar, lane);
         }
     }
-    if constexpr (ASYNC) sw_stage_tile<D, R, NTH, false>(b, t, din, sv);
-    for (int i = threadIdx.x; i <= T::NC; i += NTH) scs[i] = cell_start[kt + i];
-    for (int k = threadIdx.x; k < S::STG; k += NTH) stg[k] = R(0);
+    if constexpr (ASYNC) sw_stage_tile<D, R, T::NT, false>(b, t, din, sv);
+    for (int i = threadIdx.x; i <= T::NC; i += T::NT) scs[i] = cell_start[kt + i];
+    for (int k = threadIdx.x; k < S::STG; k += T::NT) stg[k] = R(0);
     __syncthreads();
     if (scs[0] == scs[T::NC]) {
         if constexpr (ASYNC) asm volatile("cp.async.wait_all;" ::: "memory");
@@ -498,27 +487,15 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
     if constexpr (ASYNC)
         asm volatile("cp.async.wait_all;" ::: "memory");
     else
-        sw_stage_tile<D, R, NTH>(b, t, din, sv);
+        sw_stage_tile<D, R, T::NT>(b, t, din, sv);
     __syncthreads();
     const int it = threadIdx.x;
-    // phase-2 item: MERGED (3D) it = (cell * 3 + i) * 2 + h for it < 96, all components; else (cell, a, i)
-    constexpr int NITEMS = MERGED ? T::LC * 3 * 2 : T::ITEMS;
-    constexpr int NCOMP = MERGED ? D : 1;
-    int icell, icomp, ii, ih = 0;
-    if constexpr (MERGED) {
-        icell = it / 6;
-        ii = (it / 2) % 3;
-        ih = it & 1;
-        icomp = 0;
-    } else {
-        item_of<D>(it, icell, icomp, ii);
-    }
+    int icell, icomp, ii;
+    item_of<D>(it, icell, icomp, ii);
     uint32_t parity = 0;
-    R acc[NCOMP][S::NACC];
+    R acc[S::NACC];
 #pragma unroll
-    for (int c = 0; c < NCOMP; ++c)
-#pragma unroll
-        for (int k = 0; k < S::NACC; ++k) acc[c][k] = R(0);
+    for (int k = 0; k < S::NACC; ++k) acc[k] = R(0);
     for (int layer = 0; layer < T::NL + 2; ++layer) {
         if (layer < T::NL && !layer_empty(layer)) {
             const int lb = scs[layer * T::LC], le = scs[(layer + 1) * T::LC];
@@ -527,8 +504,8 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
             const int pf_base = lb & ~(In::UE - 1);
             const int ks = scs[layer * T::LC + icell];
             const int ke = scs[layer * T::LC + icell + 1];
-            for (int sb = lb; sb < le; sb += NTH) {
-                const int se = min(sb + NTH, le);
+            for (int sb = lb; sb < le; sb += T::NT) {
+                const int se = min(sb + T::NT, le);
                 const int q = threadIdx.x, p = sb + q;
                 const bool from_pf = sb == lb;
                 if (sb != lb) __syncthreads();  // previous chunk's records consumed
@@ -624,77 +601,34 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                                               threadIdx.x);
                     }
                 }
-                if (it < NITEMS) {
+                if (it < T::ITEMS) {
                     const int p0 = max(ks, sb), p1 = min(ke, se);
                     // (icell & 7) % len without the integer division when len >= 8 (the usual case)
                     const int len = p1 - p0, r7 = icell & 7;
                     const int rot = r7 < len ? r7 : (len > 0 ? r7 % len : 0);
-                    if constexpr (MERGED) {
-                        // half h of the cell's particles (rotated order, every second one), all components:
-                        // one record load serves three components
-#pragma unroll 2
-                        for (int k = ih; k < len; k += 2) {
-                            const RecPtr<R> r(rec, rotated(p0, len, k, rot) - sb, RS);
-                            ItemW<D, R> W;
-                            W.load(r, ii);
-#pragma unroll
-                            for (int c = 0; c < D; ++c) {
-                                R sg[D];
-#pragma unroll
-                                for (int bb = 0; bb < D; ++bb) sg[bb] = *r.at(Rec<D>::G + c * SR::GP + bb);
-                                item_linear<D, R>(sg, W, acc[c]);
-                            }
-                        }
-                    } else {
-                        constexpr int kUnroll = 4;  // (measured: 2 / 8 slower)
+                    constexpr int kUnroll = 4;  // (measured: 2 / 8 slower)
 #pragma unroll kUnroll
-                        for (int k = 0; k < len; ++k) {
-                            const RecPtr<R> r(rec, rotated(p0, len, k, rot) - sb, RS);
-                            ItemW<D, R> W;
-                            R sg[D];
-                            W.load(r, ii);
+                    for (int k = 0; k < len; ++k) {
+                        const RecPtr<R> r(rec, rotated(p0, len, k, rot) - sb, RS);
+                        ItemW<D, R> W;
+                        R s[D];
+                        W.load(r, ii);
 #pragma unroll
-                            for (int bb = 0; bb < D; ++bb) sg[bb] = *r.at(Rec<D>::G + icomp * SR::GP + bb);
-                            item_linear<D, R>(sg, W, acc[0]);
-                        }
+                        for (int bb = 0; bb < D; ++bb) s[bb] = *r.at(Rec<D>::G + icomp * SR::GP + bb);
+                        item_linear<D, R>(s, W, acc);
                     }
                 }
             }
         }
         // node plane `layer` is complete: stage it, then sum the slots and RED
-        if constexpr (MERGED) {
-            if (it < NITEMS) {
-                // the two halves of (cell, i) sit in adjacent lanes: add the partner's plane-0 values, the
-                // even lane stages them; both shift their windows
-#pragma unroll
-                for (int c = 0; c < D; ++c) {
-#pragma unroll
-                    for (int j = 0; j < 3; ++j) {
-                        const R o = __shfl_xor_sync(0xffffffffu, acc[c][j * 3 + 0], 1);
-                        acc[c][j * 3 + 0] += o;
-                    }
-                    if (ih == 0) {
-                        sw_emit<D, R>(icell, c, ii, acc[c], stg);
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 3; ++j) {
-                            acc[c][j * 3 + 0] = acc[c][j * 3 + 1];
-                            acc[c][j * 3 + 1] = acc[c][j * 3 + 2];
-                            acc[c][j * 3 + 2] = R(0);
-                        }
-                    }
-                }
-            }
-        } else {
-            if (it < T::ITEMS) sw_emit<D, R>(icell, icomp, ii, acc[0], stg);
-        }
+        if (it < T::ITEMS) sw_emit<D, R>(icell, icomp, ii, acc, stg);
         __syncthreads();
         if (pkp)
-            sw_flush<D, R, true, NTH>(b, t, layer, stg, yout, tbuf ? tbuf + (int64_t)tile * T::NN * D : nullptr, sv,
-                                      din, dkd);
+            sw_flush<D, R, true>(b, t, layer, stg, yout, tbuf ? tbuf + (int64_t)tile * T::NN * D : nullptr, sv, din,
+                                 dkd);
         else
-            sw_flush<D, R, false, NTH>(b, t, layer, stg, yout, tbuf ? tbuf + (int64_t)tile * T::NN * D : nullptr, sv,
-                                       din, dkd);
+            sw_flush<D, R, false>(b, t, layer, stg, yout, tbuf ? tbuf + (int64_t)tile * T::NN * D : nullptr, sv, din,
+                                  dkd);
         // the next emit must not overwrite slots still being summed: a non-empty next layer has its
         // records barrier in between; otherwise synchronise here
         if (pkp && layer == T::NL + 1) {
