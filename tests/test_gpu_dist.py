@@ -93,6 +93,35 @@ def test_decomposed_solve_matches_oracle_and_whole(name, slabs):
         c.close()
 
 
+@pytest.mark.parametrize("name,slabs", [("3d", 2), ("3d", 4), ("2d", 3)])
+def test_decomposed_single_reduction_pcg(name, slabs):
+    """R22 over slabs: the single-reduction PCG (one reduction -- one all-reduce across ranks -- per
+    iteration, curvature partials from every slab's HVP tiles) equals the oracle's single-reduction PCG
+    (fixed 3 x 40 at 1e-9, converged at 1e-8) and the undecomposed subdomain."""
+    from paper_2605_09097_b200 import osmpm
+    sc = synth.random_fixture(**FIX[name])
+    ref = oracle.p2g(sc)
+    act = ref.active.astype(bool)
+    for kw, tol in ((dict(max_newton=3, max_cg=40, fixed_iters=1), 1e-9),
+                    (dict(newton_rtol=1e-12, cg_rtol=1e-12, max_cg=3000), 1e-8)):
+        u_ref, st_ref = oracle.implicit_solve(sc, ref, oracle.default_settings(cg_variant=1, **kw))
+        out = []
+        for k in (slabs, 1):
+            ctx = _ctx(k)
+            sub = _sub(ctx, sc)
+            sub.p2g()
+            st = sub.implicit_solve(osmpm.newton_settings(cg_variant=1, **kw))
+            assert st.status == 0
+            if kw.get("fixed_iters"):
+                assert st.cg_iters == st_ref.cg_iters == 120
+            out.append(sub.read_grid_velocity())
+            sub.close()
+            ctx.close()
+        v_ref = np.where(act[:, None], u_ref / sc.dt, 0.0)
+        assert rel_linf(out[0], v_ref) <= tol and rel_linf(out[1], v_ref) <= tol
+        assert rel_linf(out[0], out[1]) <= tol
+
+
 @pytest.mark.parametrize("name,slabs", [("3d", 3), ("2d", 3)])
 def test_migration_conserves_and_matches_whole(name, slabs):
     """Advect every particle by ~1.3 cells along +x (uniform grid velocity) so that particles cross
