@@ -263,7 +263,9 @@ osmpm_status osmpm_newton_diag(osmpm_subdomain* sub, double* diag, osmpm_memspac
 osmpm_status osmpm_implicit_solve(osmpm_subdomain* sub, const osmpm_newton_settings* settings,
                                   osmpm_solve_stats* stats);
 /* Dense read / write of the solved grid velocity v^{n+1} (nn*d).  Writing replaces the solve's
- * result (used to drive osmpm_g2p from a given grid field). */
+ * result (used to drive osmpm_g2p from a given grid field).  After osmpm_g2p the read still returns the
+ * velocity the particles were advanced with, until the next osmpm_p2g / osmpm_restore /
+ * osmpm_set_particles (e.g. a coupler frame's last fine sub-step). */
 osmpm_status osmpm_read_grid_velocity(osmpm_subdomain* sub, double* v, osmpm_memspace space);
 osmpm_status osmpm_set_grid_velocity(osmpm_subdomain* sub, const double* v, osmpm_memspace space);
 

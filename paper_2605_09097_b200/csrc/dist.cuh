@@ -356,12 +356,16 @@ struct Dist : public osmpm_subdomain {
     }
     osmpm_status read_grid_velocity(double* v, osmpm_memspace spc) override
     {
-        OSMPM_TRY(need_grid());
-        for (auto* s : sp)
-            if (!s->have_vnew) {
-                set_error("no solved grid velocity");
-                return OSMPM_E_STATE;
-            }
+        bool last = true;
+        for (auto* s : sp) last = last && s->have_vlast;
+        if (!last) {
+            OSMPM_TRY(need_grid());
+            for (auto* s : sp)
+                if (!s->have_vnew) {
+                    set_error("no solved grid velocity");
+                    return OSMPM_E_STATE;
+                }
+        }
         return export_of([](Sub<D, R>* s) { return (const double*)s->vnew.p; }, D, v, spc);
     }
     osmpm_status set_grid_velocity(const double* v, osmpm_memspace spc) override

@@ -136,7 +136,7 @@ struct Sub : public osmpm_subdomain {
 
     // ---- node box ---------------------------------------------------------------------------
     BoxDev box{};
-    bool have_grid = false, have_lin = false, have_vnew = false;
+    bool have_grid = false, have_lin = false, have_vnew = false, have_vlast = false;
     DBuf<int> cell_start;
     DBuf<double> m, mom, vn, fsig, mb, dval, u, g, dg, xs, r, z, p, y, ut, vnew, tmp, cs;  // cs: s = H p (R22)
     DBuf<uint8_t> act, dmask, fmask;
@@ -550,6 +550,7 @@ struct Sub : public osmpm_subdomain {
         have_grid = true;
         have_lin = false;
         have_vnew = false;
+        have_vlast = false;
         return OSMPM_OK;
     }
     osmpm_status p2g() override { return group_p2g<D, R>(self_group()); }
@@ -837,10 +838,12 @@ struct Sub : public osmpm_subdomain {
 
     osmpm_status read_grid_velocity(double* v, osmpm_memspace sp) override
     {
-        OSMPM_TRY(need_grid());
-        if (!have_vnew) {
-            set_error("no solved grid velocity");
-            return OSMPM_E_STATE;
+        if (!have_vlast) {
+            OSMPM_TRY(need_grid());
+            if (!have_vnew) {
+                set_error("no solved grid velocity");
+                return OSMPM_E_STATE;
+            }
         }
         return export_dense<double>(vnew.p, D, v, sp);
     }
@@ -872,6 +875,7 @@ struct Sub : public osmpm_subdomain {
         have_grid = false;  // particles moved: the next step starts with P2G
         have_lin = false;
         have_vnew = false;
+        have_vlast = true;  // vnew stays readable (the velocity the particles moved with) until the next P2G
         return OSMPM_OK;
     }
 
@@ -926,7 +930,7 @@ struct Sub : public osmpm_subdomain {
             OSMPM_LAUNCH_CHECK();
             if (sp == OSMPM_HOST) OSMPM_CU(cudaStreamSynchronize(st()));
         }
-        have_grid = have_lin = have_vnew = false;
+        have_grid = have_lin = have_vnew = have_vlast = false;
         return OSMPM_OK;
     }
 
@@ -968,7 +972,7 @@ struct Sub : public osmpm_subdomain {
         OSMPM_CU(cudaMemcpyAsync(mat.p, matck.p, cap * sizeof(int), cudaMemcpyDeviceToDevice, st()));
         OSMPM_CU(cudaMemcpyAsync(pid.p, pidck.p, cap * sizeof(int), cudaMemcpyDeviceToDevice, st()));
         OSMPM_CU(cudaMemcpyAsync(bnd.p, bndck.p, cap, cudaMemcpyDeviceToDevice, st()));
-        have_grid = have_lin = have_vnew = false;
+        have_grid = have_lin = have_vnew = have_vlast = false;
         return OSMPM_OK;
     }
 };

@@ -364,7 +364,7 @@ def cantilever_pair(dx_coarse, r=4, ppa=3, L=1.0, H=0.2, x_fine=(0.0, 0.3), x_co
         x, vol = lattice((lo_x, y0), (hi_x, y0 + H), dx, ppa)
         bnd = (np.abs(x[:, 0] - cut) < dx).astype(np.uint8)
         p = make_particles(x, vol, rho, boundary=bnd)
-        grid = grid_around(np.vstack([x, [[lo_x - 0.3 * L, y0 - L], [hi_x, y0 + H + 0.1 * L]]]), dx, 4, 2)
+        grid = grid_around(np.vstack([x, [[lo_x - 0.3 * L, y0 - L], [hi_x + 0.1 * L, y0 + H + 0.1 * L]]]), dx, 4, 2)
         out.append(Scene(grid, p, [(E, nu)], dT if dx == dx_coarse else dT / M, (0.0, -g, 0.0),
                          meta={"config": "cantilever", "M": M}))
     return out[0], out[1]
