@@ -47,8 +47,9 @@ def parse():
                     help="skip the fp32-variant sub-run that a 1-GPU f64 run reports under `variants`")
     ap.add_argument("--no-prof", action="store_true", help="skip the per-kernel event timing (A/B of its overhead)")
     ap.add_argument("--cpu-cells", type=int, default=14, help="oracle sample cube side (cells)")
-    ap.add_argument("--cg-variant", type=int, default=0, choices=[0, 1],
-                    help="PCG variant: 0 standard, 1 single-reduction (Chronopoulos-Gear, DESIGN.md R22)")
+    ap.add_argument("--cg-variant", type=int, default=None, choices=[0, 1],
+                    help="PCG variant: 0 standard, 1 single-reduction (Chronopoulos-Gear, DESIGN.md R22: one "
+                         "all-reduce per iteration); default 0 on one GPU, 1 on several")
     ap.add_argument("--slabs", type=int, default=1,
                     help="x-slabs per GPU (>1: the decomposed path on one device, halo by device copies)")
     return ap.parse_args()
@@ -304,6 +305,8 @@ def main():
         return
 
     import torch
+    if args.cg_variant is None:
+        args.cg_variant = 1 if world > 1 else 0
     dist = None
     if world > 1:
         import torch.distributed as tdist

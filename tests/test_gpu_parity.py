@@ -401,3 +401,21 @@ def test_psd_projected_solve_parity(ctx, dim):
         assert st.psd_solves == st_ref.psd_solves and st.negcurv == st_ref.negcurv and st.cg_iters == st_ref.cg_iters
         assert rel_linf(sub.read_grid_velocity(), np.where(act[:, None], u_ref / sc.dt, 0.0)) <= 1e-8
         sub.close()
+
+
+def test_solved_velocity_readable_until_next_p2g(ctx):
+    """osmpm_read_grid_velocity after osmpm_g2p returns the velocity the particles moved with; after the
+    next P2G there is no solved velocity until the next solve (STATE)."""
+    from paper_2605_09097_b200 import osmpm
+    sc = synth.random_fixture(dim=3, cells=(4, 4, 3), seed=141)
+    sub = make_sub(ctx, sc)
+    sub.p2g()
+    sub.implicit_solve(osmpm.newton_settings(max_newton=2, max_cg=20, fixed_iters=1))
+    v0 = sub.read_grid_velocity()
+    sub.g2p()
+    np.testing.assert_array_equal(sub.read_grid_velocity(), v0)
+    sub.p2g()
+    with pytest.raises(osmpm.OsmpmError) as e:
+        sub.read_grid_velocity()
+    assert e.value.code == 11
+    sub.close()
