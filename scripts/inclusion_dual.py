@@ -140,10 +140,12 @@ def run_single(inv_h, ratio, protocol, vtol, max_frames):
     frames = 0
     while True:
         sub.p2g()
-        sub.implicit_solve(ns)
+        st = sub.implicit_solve(ns)
         v = sub.read_grid_velocity()
         sub.g2p()
         frames += 1
+        if os.environ.get("INCL_VERBOSE") and (frames < 5 or frames % 20 == 0):
+            print(f"   single frame {frames}: max|v| {np.abs(v).max():.3e} ls_fail {st.ls_failures}", flush=True)
         if protocol == "static" or np.abs(v).max() < vtol or frames >= max_frames:
             break
     sub.sync()
@@ -185,6 +187,9 @@ def run_dual(inv_h, ratio, protocol, vtol, max_frames, overlap=2):
             break
         vb = sb.read_grid_velocity()
         vs = ss.read_grid_velocity()
+        if os.environ.get("INCL_VERBOSE"):
+            print(f"   frame {frames}: schwarz {rep.iters} r_B {rep.r_B[rep.iters - 1]:.2e} r_S {rep.r_S[rep.iters - 1]:.2e} "
+                  f"max|v_B| {np.abs(vb).max():.3e} max|v_S| {np.abs(vs).max():.3e}", flush=True)
         if max(np.abs(vb).max(), np.abs(vs).max()) < vtol or frames >= max_frames:
             break
     sb.sync()
