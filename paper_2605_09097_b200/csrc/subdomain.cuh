@@ -583,7 +583,7 @@ struct Sub : public osmpm_subdomain {
             dptr = stage->p;
         }
         OSMPM_CU(cudaMemsetAsync(dptr, 0, cnt * sizeof(Tv), st()));
-        if (have_grid) {
+        if (have_grid || have_vlast) {  // have_vlast: the box of the last P2G is still the current one
             KC(); k_box_to_dense<D, Tv><<<nblk_all(box.nnodes, 256), 256, 0, st()>>>(box, nown, nc, src, dptr);
             OSMPM_LAUNCH_CHECK();
         }
