@@ -12,8 +12,9 @@
 //              totals) -> the first output slot of every (digit, tile)
 //   downsweep  per-tile stable ranks: each warp walks its 16 keys in input order, peers with the same
 //              digit found with __match_any_sync, per-warp digit counters in shared memory, then an
-//              exclusive scan of the counters across the 8 warps; scatter key and value to
-//              slot(digit, tile) + rank.
+//              exclusive scan of the counters across the 8 warps; the pairs are staged in shared memory
+//              in their sorted order within the tile and stored from there, so that the consecutive
+//              slots slot(digit, tile) + rank of one digit are written by consecutive threads.
 // Keys of a tile are read warp-striped (item i of lane l of warp w = tile base + 512 w + 32 i + l),
 // which is also the ranking order, so stability needs no extra bookkeeping.
 #pragma once
@@ -26,6 +27,7 @@ namespace osmpm {
 struct RS {
     static constexpr int BITS = 8, RADIX = 1 << BITS, THREADS = 256, WARPS = THREADS / 32, IPT = 16;
     static constexpr int TILE = THREADS * IPT;
+    static_assert(THREADS == RADIX, "the downsweep scans one digit per thread");
 };
 
 __global__ void __launch_bounds__(RS::THREADS) k_rs_upsweep(const uint32_t* __restrict__ keys, int64_t n, int shift,
@@ -105,10 +107,14 @@ __global__ void __launch_bounds__(RS::THREADS) k_rs_downsweep(const uint32_t* __
                                                               const uint32_t* __restrict__ tot, int nblk)
 {
     __shared__ uint32_t cnt[RS::WARPS][RS::RADIX];
+    __shared__ uint32_t doff[RS::RADIX];           // the tile's exclusive digit offsets
+    __shared__ uint32_t sk[RS::TILE];              // the tile's pairs in sorted order, for coalesced stores
+    __shared__ int svv[RS::TILE];
     for (int e = threadIdx.x; e < RS::WARPS * RS::RADIX; e += RS::THREADS) (&cnt[0][0])[e] = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t base = (int64_t)blockIdx.x * RS::TILE + (int64_t)w * (32 * RS::IPT) + lane;
+    const int64_t tbase = (int64_t)blockIdx.x * RS::TILE;
+    const int64_t base = tbase + (int64_t)w * (32 * RS::IPT) + lane;
     const uint32_t lt = (1u << lane) - 1u;
     uint32_t key[RS::IPT], rank[RS::IPT];
     int val[RS::IPT];
@@ -130,25 +136,53 @@ __global__ void __launch_bounds__(RS::THREADS) k_rs_downsweep(const uint32_t* __
         __syncwarp();
     }
     __syncthreads();
-    // exclusive scan of each digit's per-warp counts across the warps
-    for (int d = threadIdx.x; d < RS::RADIX; d += RS::THREADS) {
+    // per digit: exclusive scan of the per-warp counts across the warps; digit totals of the tile
+    uint32_t dtot = 0;
+    const int d0 = threadIdx.x;  // RS::THREADS == RS::RADIX: one digit per thread
+    {
         uint32_t run = 0;
 #pragma unroll
         for (int q = 0; q < RS::WARPS; ++q) {
-            const uint32_t t = cnt[q][d];
-            cnt[q][d] = run;
+            const uint32_t t = cnt[q][d0];
+            cnt[q][d0] = run;
             run += t;
         }
+        dtot = run;
+    }
+    // exclusive scan of the digit totals over the block (warp scans + warp totals)
+    {
+        __shared__ uint32_t wsum[RS::WARPS];
+        uint32_t x = dtot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += t;
+        }
+        if (lane == 31) wsum[w] = x;
+        __syncthreads();
+        uint32_t pre = 0;
+        for (int q = 0; q < w; ++q) pre += wsum[q];
+        doff[d0] = pre + x - dtot;
     }
     __syncthreads();
+    // stage the pairs at their sorted position inside the tile
 #pragma unroll
     for (int i = 0; i < RS::IPT; ++i) {
-        const int64_t k = base + 32 * i;
-        if (k >= n) continue;
+        if (base + 32 * i >= n) continue;
         const uint32_t d = (key[i] >> shift) & mask;
-        const int64_t pos = (int64_t)tot[d] + hist[(int64_t)d * nblk + blockIdx.x] + cnt[w][d] + rank[i];
-        kout[pos] = key[i];
-        vout[pos] = val[i];
+        const uint32_t pos = doff[d] + cnt[w][d] + rank[i];
+        sk[pos] = key[i];
+        svv[pos] = val[i];
+    }
+    __syncthreads();
+    // consecutive tile positions of one digit go to consecutive global slots: coalesced stores
+    const int64_t nvalid = min((int64_t)RS::TILE, n - tbase);
+    for (int pos = threadIdx.x; pos < nvalid; pos += RS::THREADS) {
+        const uint32_t kk = sk[pos];
+        const uint32_t d = (kk >> shift) & mask;
+        const int64_t g = (int64_t)tot[d] + hist[(int64_t)d * nblk + blockIdx.x] + (pos - doff[d]);
+        kout[g] = kk;
+        vout[g] = svv[pos];
     }
 }
 

@@ -109,7 +109,8 @@ def active_set(solve, gradient, sc, xs, plane, axis, gap, active_nodes, max_roun
             pen = (u[:, 1] + gap)[in_plane & active_nodes & ~on]
             print(f"   round {rounds}: |C| = {on.sum()}, release {release.sum()}, add {add.sum()}, "
                   f"min r = {r[on].min():.3e}, max r = {r[on].max():.3e}, min free clearance = "
-                  f"{pen.min() if pen.size else 0:.3e}, newton {st.newton_iters}, cg {st.cg_iters}", flush=True)
+                  f"{pen.min() if pen.size else 0:.3e}, newton {getattr(st, 'newton_iters', '-')}, "
+                  f"cg {getattr(st, 'cg_iters', '-')}", flush=True)
         if not release.any() and not add.any():
             break
         if rounds >= max_rounds:
