@@ -19,6 +19,8 @@ FIX = {
     # x-extents of several tile columns (3D tile edge 4 cells, 2D 16 cells) so that 2-4 slabs fit
     "3d": dict(dim=3, cells=(26, 7, 6), seed=301),
     "2d": dict(dim=2, cells=(70, 9, 1), seed=302),
+    # 8 slabs (G = 8): 11 tile columns
+    "3d8": dict(dim=3, cells=(44, 6, 5), seed=303),
 }
 
 
@@ -35,7 +37,7 @@ def _sub(ctx, sc, decompose=True):
     return osmpm.Subdomain(ctx, sc.grid, sc.dt, sc.particles, sc.materials, sc.gravity, decompose=decompose)
 
 
-@pytest.mark.parametrize("name,slabs", [("3d", 2), ("3d", 3), ("2d", 2), ("2d", 4)])
+@pytest.mark.parametrize("name,slabs", [("3d", 2), ("3d", 3), ("2d", 2), ("2d", 4), ("3d8", 8)])
 def test_decomposed_kernels_match_oracle(name, slabs):
     sc = synth.random_fixture(**FIX[name])
     d = sc.grid.dim
@@ -93,7 +95,7 @@ def test_decomposed_solve_matches_oracle_and_whole(name, slabs):
         c.close()
 
 
-@pytest.mark.parametrize("name,slabs", [("3d", 2), ("3d", 4), ("2d", 3)])
+@pytest.mark.parametrize("name,slabs", [("3d", 2), ("3d", 4), ("2d", 3), ("3d8", 8)])
 def test_decomposed_single_reduction_pcg(name, slabs):
     """R22 over slabs: the single-reduction PCG (one reduction -- one all-reduce across ranks -- per
     iteration, curvature partials from every slab's HVP tiles) equals the oracle's single-reduction PCG
@@ -122,7 +124,7 @@ def test_decomposed_single_reduction_pcg(name, slabs):
         assert rel_linf(out[0], out[1]) <= tol
 
 
-@pytest.mark.parametrize("name,slabs", [("3d", 3), ("2d", 3)])
+@pytest.mark.parametrize("name,slabs", [("3d", 3), ("2d", 3), ("3d8", 8)])
 def test_migration_conserves_and_matches_whole(name, slabs):
     """Advect every particle by ~1.3 cells along +x (uniform grid velocity) so that particles cross
     the cuts; particle count, mass and momentum are conserved exactly, states equal the whole
