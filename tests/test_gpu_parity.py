@@ -99,6 +99,9 @@ def test_implicit_solve_parity_converged(ctx, name):
     sub.p2g()
     st = sub.implicit_solve(osmpm.newton_settings(**kw))
     assert st.status == 0 and st_ref.status == 0
+    # converged at newton_rtol on both sides, not accepted at the round-off floor (R8)
+    assert st.floor_accept == st_ref.floor_accept == 0
+    assert st.ls_failures == st_ref.ls_failures == 0
     v = sub.read_grid_velocity()
     act = ref.active.astype(bool)
     v_ref = np.where(act[:, None], u_ref / sc.dt, 0.0)
