@@ -9,10 +9,12 @@ disk minus the box shrunk by `overlap` coarse cells at h_B = 1/64 (the paper: 1.
 particles per cell; P^∂ within one own cell of each artificial cut.  The contact patch (b = 0.05) lies
 inside Omega_S, so only the fine grid carries the contact constraints.
 
-Every active-set round solves one quasi-static Schwarz frame (dT = 10 s, M = 1; eps_conv = 1e-5) from the
-initial state (both subdomains restored, osmpm_restore); the plane reactions are the fine Newton gradient
-over all DOFs at the solved fine velocities (osmpm_newton_gradient on the restored fine state).
-Reports b (second moment), p(0) and the relative L2 distance of the pressure profile to the semi-ellipse.
+Every active-set round solves, from the initial state, `ramp` quasi-static Schwarz frames (dT = 10 s,
+M = 1; eps_conv = 1e-5) with the load stepped up to its full value; the plane reactions are the fine Newton
+gradient over all DOFs at the last frame's solved increment (osmpm_newton_gradient on the fine state
+restored to the start of that frame).  Reports b (second moment), p(0) and the relative L2 distance of the
+pressure profile to the semi-ellipse, against Hertz at the applied resultant and at the measured contact
+force (the overlap's material is weighed by both subdomains).
 
   python scripts/hertz_dual.py [--inv-hs 64 128 256]
 """
@@ -64,7 +66,7 @@ def nodes(grid):
     return np.asarray(grid.origin[:2]) + k * grid.dx
 
 
-def run(inv_hs, max_rounds=30):
+def run(inv_hs, max_rounds=30, ramp=1):
     from paper_2605_09097_b200 import osmpm
     coarse, fine = scenes(inv_hs)
     ctx = osmpm.Context(0)
@@ -88,20 +90,34 @@ def run(inv_hs, max_rounds=30):
     t0 = time.time()
     iters = []
 
+    g_full = fine.gravity[1]
+    init = [(sub, {k: np.ascontiguousarray(getattr(sc.particles, k)) for k in ("x", "v", "F", "B")})
+            for sub, sc in ((sb, coarse), (ss, fine))]
+
     def solve(sel, bits, vel):
-        sb.restore()
-        ss.restore()
-        ss.set_dirichlet(sel, bits, vel)
-        rep = cpl.step()
-        iters.append(rep.iters)
-        v = ss.read_grid_velocity()
-        return v * fine.dt, rep
+        # from the initial state, `ramp` quasi-static frames with the load (and the prescribed contact gap
+        # displacements) stepped up in equal parts, so that no frame takes the whole settlement at once;
+        # the fine state before the last frame is kept for the reactions.  The active-set test needs the
+        # total displacement of the plane nodes: ramp x the last increment (proportional loading)
+        for sub, st0 in init:
+            sub.set_particles(**st0)
+        rep = None
+        for k in range(1, ramp + 1):
+            for sub in (sb, ss):
+                sub.set_gravity((0.0, k / ramp * g_full, 0.0))
+            ss.set_dirichlet(sel, bits, vel / ramp)
+            if k == ramp:
+                ss.checkpoint()
+            rep = cpl.step()
+            iters.append(rep.iters)
+        return ss.read_grid_velocity() * fine.dt * ramp, rep
 
     def gradient(u):
+        # reactions at the last frame: the fine Newton gradient over all DOFs at its solved increment
         ss.restore()
         ss.set_dirichlet(np.zeros(0, np.int64), np.zeros(0, np.uint8), np.zeros((0, 2)))
         ss.p2g()
-        return ss.newton_gradient(u)[0]
+        return ss.newton_gradient(u / ramp)[0]
 
     try:
         res = hz.active_set(solve, gradient, fine, xsS, plane, axis, gap, act, max_rounds=max_rounds)
@@ -111,13 +127,17 @@ def run(inv_hs, max_rounds=30):
         ss.close()
         ctx.close()
     b_ref, p_ref = hz.hertz()
+    # the overlap's material is weighed by both subdomains, so the plane carries more than the applied
+    # resultant; Hertz at the measured contact force F compares the profile's shape
+    b_F, p_F = hz.hertz(res["F"])
     xc, pc = res["xc"], res["p"]
     ph = p_ref * np.sqrt(np.maximum(0.0, 1 - (xc / b_ref) ** 2))
     grid_x = np.arange(-2 * b_ref, 2 * b_ref + 1e-12, 1.0 / inv_hs)
     p_on = np.interp(grid_x, xc, pc, left=0.0, right=0.0)
     p_hz = p_ref * np.sqrt(np.maximum(0.0, 1 - (grid_x / b_ref) ** 2))
     return {"inv_hs": inv_hs, "inv_hb": INV_HB, "b": res["b"], "b_err": res["b"] / b_ref - 1, "p0": res["p0"],
-            "p0_err": res["p0"] / p_ref - 1, "F": res["F"], "profile_L2_rel": float(np.linalg.norm(p_on - p_hz)
+            "p0_err": res["p0"] / p_ref - 1, "F": res["F"], "F_over_applied": res["F"] / hz.F_LINE,
+            "b_err_at_F": res["b"] / b_F - 1, "p0_err_at_F": res["p0"] / p_F - 1, "ramp": ramp, "profile_L2_rel": float(np.linalg.norm(p_on - p_hz)
                                                                                       / np.linalg.norm(p_hz)),
             "rounds": res["rounds"], "schwarz_iters": iters, "seconds": round(time.time() - t0, 2),
             "particles_fine": int(fine.particles.n), "particles_coarse": int(coarse.particles.n),
@@ -127,6 +147,8 @@ def run(inv_hs, max_rounds=30):
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--inv-hs", type=int, nargs="+", default=[64, 128, 256])
+    ap.add_argument("--ramp", type=int, nargs="+", default=None, help="load steps per h_S (default 1, 1, 4)")
     a = ap.parse_args()
-    for n in a.inv_hs:
-        print(json.dumps(run(n)), flush=True)
+    ramps = a.ramp or [1 if n < 256 else 4 for n in a.inv_hs]
+    for n, rp in zip(a.inv_hs, ramps):
+        print(json.dumps(run(n, ramp=rp)), flush=True)
