@@ -478,6 +478,7 @@ def main():
         return
 
     peak, peak_kind = peaks()
+    fma_peak = ctx.measure_fma_peak(prec)
     hvp_bytes = hvp_algorithmic_bytes(n_local, n_active, word)  # rank 0's share per launch
     hvp_avg_ms = hv_ms / hv_n if hv_n else float("nan")
     achieved = hvp_bytes / (hvp_avg_ms * 1e-3) / 1e9 if hv_n else None
@@ -517,10 +518,11 @@ def main():
                      # the same launches against the CUDA-core floating-point peak (the
                      # fp64 HVP's compute ceiling lies at 68 % of the HBM roofline)
                      "fp_pipe": ({"achieved_tflops": n_local * HVP_FLOPS_PER_PARTICLE / (hvp_avg_ms * 1e-3) / 1e12,
-                                  "peak_tflops": FP64_PEAK_TFLOPS * (2 if word == 4 else 1),
-                                  "frac": n_local * HVP_FLOPS_PER_PARTICLE / (hvp_avg_ms * 1e-3) / 1e12
-                                  / (FP64_PEAK_TFLOPS * (2 if word == 4 else 1)),
-                                  "flops_per_particle": HVP_FLOPS_PER_PARTICLE, "peak_kind": "derived (DESIGN.md §5)"}
+                                  "peak_tflops": fma_peak,
+                                  "frac": n_local * HVP_FLOPS_PER_PARTICLE / (hvp_avg_ms * 1e-3) / 1e12 / fma_peak,
+                                  "flops_per_particle": HVP_FLOPS_PER_PARTICLE,
+                                  "peak_kind": "measured (osmpm_measure_fma_peak, independent FMA chains)",
+                                  "nominal_peak_tflops": FP64_PEAK_TFLOPS * (2 if word == 4 else 1)}
                                  if hv_n else None)},
         "kernel_ms_per_step": {f: v[1] / args.steps for f, v in fam.items()},
         "transfer_rooflines": transfer_rooflines(fam, n_local, n_active, word, peak),

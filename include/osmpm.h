@@ -338,6 +338,12 @@ osmpm_status osmpm_schwarz_substep(osmpm_coupler* cpl, int32_t m, osmpm_solve_st
 /* Whole frame t_n -> t_n+1 (Alg. 1). */
 osmpm_status osmpm_schwarz_step(osmpm_coupler* cpl, osmpm_schwarz_report* report);
 
+/* CUDA-core FMA throughput of the ctx's device in TFLOP/s (fp64 or fp32 by `prec`): 8 independent FMA
+ * chains per thread on 8 CTAs of 256 threads per SM, best of 5 event-timed launches.  The measured
+ * denominator of bench.py's `roofline.fp_pipe` (MEASURED_PEAKS.json has no CUDA-core
+ * peak).  Synchronising. */
+osmpm_status osmpm_measure_fma_peak(osmpm_ctx* ctx, osmpm_precision prec, double* tflops);
+
 /* a1 building block, exposed for testing: stable LSD radix sort (8 bits per pass) of n (key, value)
  * pairs on the low nbits bits of the keys, in place; equal keys keep their input order.  This is the
  * sort osmpm_p2g runs on the particles' tile-major cell keys every step (north_star: "block-level

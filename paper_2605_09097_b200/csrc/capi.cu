@@ -74,6 +74,24 @@ Profiler::~Profiler()
         }
 }
 
+// CUDA-core FMA throughput probe (the FP64 / FP32 vector peaks are not in
+// MEASURED_PEAKS.json): every thread runs 8 independent FMA chains of `iters` steps on registers
+template <typename T>
+__global__ void __launch_bounds__(256) k_fma_probe(int iters, T a, T b, T* out)
+{
+    T x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = (T)(threadIdx.x + k) * (T)1e-3;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+    }
+    T s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += x[k];
+    if (s == (T)-1.2345) out[0] = s;  // never true: keeps the chains alive
+}
+
 }  // namespace osmpm
 
 using namespace osmpm;
@@ -372,6 +390,44 @@ osmpm_status osmpm_sort_pairs(osmpm_ctx* ctx, uint32_t* keys, int32_t* vals, int
     OSMPM_CU(cudaStreamSynchronize(ctx->stream));
     return OSMPM_OK;
 }
+osmpm_status osmpm_measure_fma_peak(osmpm_ctx* ctx, osmpm_precision prec, double* tflops)
+{
+    CHECK_ARG(ctx && tflops, "NULL argument");
+    SET_DEVICE(ctx);
+    int sms = 0;
+    OSMPM_CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    DBuf<double> out;
+    OSMPM_TRY(out.need(1));
+    cudaEvent_t e0, e1;
+    OSMPM_CU(cudaEventCreate(&e0));
+    OSMPM_CU(cudaEventCreate(&e1));
+    auto launch = [&]() {
+        if (prec == OSMPM_F64)
+            k_fma_probe<double><<<blocks, threads, 0, ctx->stream>>>(iters, 0.999999, 1e-7, out.p);
+        else
+            k_fma_probe<float><<<blocks, threads, 0, ctx->stream>>>(iters, 0.999999f, 1e-7f, (float*)out.p);
+        ctx->launches++;
+    };
+    launch();  // warm-up
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        OSMPM_CU(cudaEventRecord(e0, ctx->stream));
+        launch();
+        OSMPM_CU(cudaEventRecord(e1, ctx->stream));
+        OSMPM_CU(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        OSMPM_CU(cudaEventElapsedTime(&ms, e0, e1));
+        best = std::min(best, ms);
+    }
+    OSMPM_LAUNCH_CHECK();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double flops = 2.0 * 8.0 * iters * (double)blocks * threads;
+    *tflops = flops / (best * 1e-3) / 1e12;
+    return OSMPM_OK;
+}
+
 osmpm_status osmpm_checkpoint(osmpm_subdomain* sub) { SUB_CALL(sub, checkpoint()); }
 osmpm_status osmpm_restore(osmpm_subdomain* sub) { SUB_CALL(sub, restore()); }
 

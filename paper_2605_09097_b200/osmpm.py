@@ -201,6 +201,12 @@ class Context:
         """Split each rank's share of decomposed subdomains into n slabs on this device."""
         _check(lib().osmpm_ctx_set_local_slabs(self._h, C.c_int(n)))
 
+    def measure_fma_peak(self, precision=F64):
+        """CUDA-core FMA throughput in TFLOP/s (osmpm_measure_fma_peak)."""
+        t = C.c_double()
+        _check(lib().osmpm_measure_fma_peak(self._h, C.c_int(precision), C.byref(t)))
+        return t.value
+
     def launch_count(self):
         n = C.c_int64()
         _check(lib().osmpm_launch_count(self._h, C.byref(n)))
