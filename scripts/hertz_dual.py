@@ -80,7 +80,7 @@ def run(inv_hs, max_rounds=30, ramp=1):
     gap = np.zeros(xsS.shape[0])
     xp = np.minimum(np.abs(xsS[plane, 0]), hz.R)
     gap[plane] = hz.R - np.sqrt(hz.R * hz.R - xp * xp)
-    ns = osmpm.newton_settings(newton_rtol=1e-9, cg_rtol=1e-10, max_cg=40000, max_newton=40, guess=1,
+    ns = osmpm.newton_settings(newton_rtol=1e-8, cg_rtol=1e-10, max_cg=60000, max_newton=60, guess=1,
                                energy_noise_rtol=1e-12)
     cpl = osmpm.Coupler(sb, ss, osmpm.schwarz_settings(M=1, eps_conv=1e-5, k_max=2000, coarse=ns, fine=ns))
     sb.checkpoint()

@@ -45,7 +45,7 @@ W_FINE = 0.15
 
 def static_settings():
     from paper_2605_09097_b200 import osmpm
-    return osmpm.newton_settings(newton_rtol=1e-7, cg_rtol=1e-10, max_cg=40000, max_newton=40, guess=1,
+    return osmpm.newton_settings(newton_rtol=1e-7, cg_rtol=1e-10, max_cg=60000, max_newton=80, guess=1,
                                  energy_noise_rtol=1e-12)
 
 
