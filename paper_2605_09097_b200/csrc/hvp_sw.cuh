@@ -29,13 +29,10 @@ namespace osmpm {
 template <int D> constexpr int HVP_NW = (Tile<D>::NT + 31) / 32;
 
 template <int D, typename R> struct SWRec {
-    // 3D fp64 (GP == 4): G row a as the 16-B pair (G_a0, G_a1) at pair(a) = G + 2a, the last entries
-    // G_02, G_12, G_22 together at third(a) = G + 6 + a (written as two 16-B stores, read as one 16-B + one
-    // 8-B load per row; the 30-real record has the room); otherwise rows packed (GP == D)
+    // G row a starts at GROW(a): 3D fp64 rows padded to 4 reals (16-B aligned: one 16-B + one 8-B load
+    // per row; the 30-real record has exactly the room), otherwise packed
     static constexpr int GP = (D == 3 && sizeof(R) == 8) ? 4 : D;
     static constexpr int RS = HvpRec<D, R>::RS;
-    static __host__ __device__ constexpr int pair(int a) { return Rec<D>::G + 2 * a; }
-    static __host__ __device__ constexpr int third(int a) { return Rec<D>::G + 6 + a; }
 };
 
 template <int D> struct SW {
@@ -561,7 +558,6 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                         }
                     const R ltr = ll * tr;
 #pragma unroll
-                    R g3[D];  // the rows' last entries (3D fp64: stored together, below)
                     for (int a = 0; a < D; ++a) {
                         R Ga[D];
 #pragma unroll
@@ -580,24 +576,12 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                             V2 g01;
                             g01.x = Ga[0];
                             g01.y = Ga[1];
-                            *reinterpret_cast<V2*>(r.at(SR::pair(a))) = g01;
-                            g3[a] = Ga[D - 1];
+                            *reinterpret_cast<V2*>(r.at(Rec<D>::G + 4 * a)) = g01;
+                            *r.at(Rec<D>::G + 4 * a + 2) = Ga[D - 1];
                         } else {
 #pragma unroll
                             for (int bb = 0; bb < D; ++bb) *r.at(Rec<D>::G + a * D + bb) = Ga[bb];
                         }
-                    }
-                    if constexpr (SR::GP == 4) {
-                        // (G02, G12) and (G22, 0) as two 16-B stores: the 8-B stores of the record stride
-                        // (30 reals) meet 4-way bank conflicts
-                        using V2 = typename Vec2<R>::type;
-                        V2 t01, t2;
-                        t01.x = g3[0];
-                        t01.y = g3[1];
-                        t2.x = g3[2];
-                        t2.y = R(0);
-                        *reinterpret_cast<V2*>(r.at(SR::third(0))) = t01;
-                        *reinterpret_cast<V2*>(r.at(SR::third(2))) = t2;
                     }
                 };
                 if (p < se) {
@@ -630,16 +614,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                         R s[D];
                         W.load(r, ii);
 #pragma unroll
-                        if constexpr (SR::GP == 4) {
-                            using V2 = typename Vec2<R>::type;
-                            const V2 g01 = *reinterpret_cast<const V2*>(r.at(SR::pair(icomp)));
-                            s[0] = g01.x;
-                            s[1] = g01.y;
-                            s[2] = *r.at(SR::third(icomp));
-                        } else {
-#pragma unroll
-                            for (int bb = 0; bb < D; ++bb) s[bb] = *r.at(Rec<D>::G + icomp * SR::GP + bb);
-                        }
+                        for (int bb = 0; bb < D; ++bb) s[bb] = *r.at(Rec<D>::G + icomp * SR::GP + bb);
                         item_linear<D, R>(s, W, acc);
                     }
                 }
