@@ -34,12 +34,17 @@ L, H, E, NU, RHO = 1.0, 0.2, 1.0e5, 0.4, 1000.0
 Y0 = 1.0
 
 
+PSD = 0
+
+
 def newton(guess=1, rtol=1e-8):
     """guess 1: u = 0 (a single load step from rest); guess 0: u = dt v^n, the previous frame's increment
-    (progressive loading: each load level starts from the previous equilibrium's increment)."""
+    (progressive loading: each load level starts from the previous equilibrium's increment).  PSD (set by
+    --psd): 1 projects the per-particle tangent blocks when a Newton direction fails the descent test,
+    2 always (R23)."""
     from paper_2605_09097_b200 import osmpm
     return osmpm.newton_settings(newton_rtol=rtol, newton_atol=0.0, cg_rtol=1e-10, max_cg=40000, max_newton=100,
-                                 guess=guess, energy_noise_rtol=1e-12)
+                                 guess=guess, energy_noise_rtol=1e-12, psd=PSD)
 
 
 def tip_mask(x0, dx):
@@ -83,7 +88,7 @@ def run_single(dx, gammas, dT=10.0, guess=1, rtol=1e-8):
         x = sub.read_particles(fields=("x",))["x"]
         W, Hh = measure(sc.particles.x, x, dx)
         out.append({"gamma": G, "W": W, "H": Hh, "newton": st.newton_iters, "cg": st.cg_iters,
-                    "floor_accept": st.floor_accept, "s": round(time.time() - t0, 2)})
+                    "floor_accept": st.floor_accept, "psd_solves": st.psd_solves, "s": round(time.time() - t0, 2)})
     sub.close()
     ctx.close()
     return out
@@ -136,7 +141,9 @@ if __name__ == "__main__":
     ap.add_argument("--no-dual", action="store_true")
     ap.add_argument("--guess", type=int, default=1)
     ap.add_argument("--rtol", type=float, default=1e-8)
+    ap.add_argument("--psd", type=int, default=0, choices=[0, 1, 2])
     a = ap.parse_args()
+    PSD = a.psd
     if a.mode == "res":
         G = [0.05]
         ref = elastica_row(0.05)

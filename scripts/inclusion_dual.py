@@ -41,6 +41,7 @@ import eshelby as es  # noqa: E402
 import synth  # noqa: E402
 
 W_FINE = 0.15
+K_MAX_DYN = 60
 
 
 def static_settings():
@@ -49,11 +50,19 @@ def static_settings():
                                  energy_noise_rtol=1e-12)
 
 
+SOLVER = "fixed"
+
+
 def dynamic_settings():
-    """Inexact Newton per frame (fixed 3 x 300): near equilibrium the energy decrease of a Newton step falls
-    below the round-off floor of E_h and a tolerance-driven line search stagnates (R8), while
-    the relaxation only needs each frame's solve to be good enough to keep damping the motion."""
+    """SOLVER "fixed": inexact Newton per frame (fixed 3 x 300): near equilibrium the energy decrease of a
+    Newton step falls below the round-off floor of E_h and a tolerance-driven line search stagnates
+    (R8), while the relaxation only needs each frame's solve to be good enough to keep damping
+    the motion.  SOLVER "tol": converged solves (relative 1e-8, energy changes within 1e-10 |E| count as
+    no increase), so that every Schwarz iteration applies the same exact subdomain maps."""
     from paper_2605_09097_b200 import osmpm
+    if SOLVER == "tol":
+        return osmpm.newton_settings(newton_rtol=1e-8, cg_rtol=1e-10, max_cg=20000, max_newton=50, guess=0,
+                                     energy_noise_rtol=1e-10)
     return osmpm.newton_settings(max_newton=3, max_cg=300, fixed_iters=1)
 
 
@@ -179,10 +188,11 @@ def run_dual(inv_h, ratio, protocol, vtol, max_frames, overlap=2):
     # dynamic frames: at most 60 Schwarz iterations (near equilibrium the relative interface residuals of
     # PAPER.md:489-491 stall around 1e-3 while the velocities themselves vanish); a frame that reaches the
     # cap is kept (the coupler has advanced both subdomains) and counted
-    cpl = osmpm.Coupler(sb, ss, osmpm.schwarz_settings(M=M, eps_conv=1e-5, k_max=3000 if protocol == "static" else 60,
+    cpl = osmpm.Coupler(sb, ss, osmpm.schwarz_settings(M=M, eps_conv=1e-5, k_max=3000 if protocol == "static" else K_MAX_DYN,
                                                        coarse=ns, fine=ns))
     t0 = time.time()
     frames, iters, capped = 0, 0, 0
+    n_recv = (0, 0)  # of the last frame that returned a report (a capped frame raises instead)
     while True:
         try:
             rep = cpl.step()
@@ -192,10 +202,12 @@ def run_dual(inv_h, ratio, protocol, vtol, max_frames, overlap=2):
             capped += 1
             rep = None
         frames += 1
-        iters += rep.iters if rep else 60
+        if rep is not None:
+            n_recv = (rep.n_recv_B, rep.n_recv_S)
+        iters += rep.iters if rep else K_MAX_DYN
         if rep is None:
             rep = osmpm.SchwarzReport()
-            rep.iters = 60
+            rep.iters = K_MAX_DYN
         if protocol == "static":
             break
         vb = sb.read_grid_velocity()
@@ -211,7 +223,7 @@ def run_dual(inv_h, ratio, protocol, vtol, max_frames, overlap=2):
     Ff = ss.read_particles(fields=("F",))["F"]
     res = measure_dual(ratio, coarse, fine, hole, Fc, Ff, h)
     res.update(seconds=t, frames=frames, schwarz_iters=iters, frames_at_cap=capped, particles_fine=int(fine.particles.n),
-               particles_coarse=int(coarse.particles.n), n_recv_B=rep.n_recv_B, n_recv_S=rep.n_recv_S)
+               particles_coarse=int(coarse.particles.n), n_recv_B=n_recv[0], n_recv_S=n_recv[1])
     cpl.close()
     sb.close()
     ss.close()
@@ -226,7 +238,11 @@ if __name__ == "__main__":
     ap.add_argument("--inv-h", type=int, nargs="+", default=[64, 128, 256])
     ap.add_argument("--vtol", type=float, default=1e-6)
     ap.add_argument("--max-frames", type=int, default=2000)
+    ap.add_argument("--solver", default="fixed", choices=["fixed", "tol"])
+    ap.add_argument("--k-max", type=int, default=60, help="Schwarz iteration cap per dynamic frame")
     a = ap.parse_args()
+    SOLVER = a.solver
+    K_MAX_DYN = a.k_max
     for ratio in a.ratio:
         for n in a.inv_h:
             s = run_single(n, ratio, a.protocol, a.vtol, a.max_frames)
