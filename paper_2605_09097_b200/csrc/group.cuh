@@ -97,6 +97,244 @@ osmpm_status halo_sum(SlabGroup<D, R> G, std::initializer_list<HField<D, R>> fie
     return OSMPM_OK;
 }
 
+// ---------------------------------------------------------------------------------------------
+// R24: the fused halo of the PCG's HVP output y (hvp_sw.cuh HaloDev).  Each slab's HVP RED-s the
+// partial sums of the planes it shares with a neighbour into the neighbour's y as well, so no halo
+// pass follows the HVP.  Neighbours on the same device are plain pointers (one stream: the kernels of
+// all slabs finish before the consumer).  Neighbours on other ranks are the peers' y buffers mapped
+// with CUDA IPC (NVLink loads / REDs): y alternates with y2 from iteration to iteration, and the last
+// CTA of each HVP bumps the neighbour's inbox word, which the neighbour's k_halo_wait consumes before
+// it reads y.  Why the alternation suffices: the HVP of iteration c + 1 on one rank starts after the
+// rank's all-reduce of iteration c, which every peer reaches only after its kernels of iteration c - 1
+// (which zeroed the buffer the HVP of c + 1 writes) -- in both PCG variants.
+// OSMPM_HALO_LOOPBACK=1 runs that protocol (alternating buffers, inbox words, waits) between the local
+// slabs of one device, so that one GPU tests it; OSMPM_FUSED_HALO=0 restores the halo pass.
+// ---------------------------------------------------------------------------------------------
+struct HaloRec {  // one rank's record of the exchange
+    cudaIpcMemHandle_t first[HaloPeer::NB], last[HaloPeer::NB];
+    int64_t nn0_first, nn0_last;
+    int32_t ok, ns;
+};
+
+static inline bool env_is(const char* k, const char* v)
+{
+    const char* e = getenv(k);
+    return e && std::string(e) == v;
+}
+
+template <int D, typename R>
+osmpm_status halo_setup(SlabGroup<D, R> G, bool& fused)
+{
+    HaloState& h = G.gb->halo;
+    fused = false;
+    h.alt = false;
+    if (env_is("OSMPM_FUSED_HALO", "0")) return OSMPM_OK;
+    if (G.ns == 1 && !G.multi()) return OSMPM_OK;
+    for (int i = 0; i < G.ns; ++i)
+        if (G.s[i]->det_mode()) return OSMPM_OK;
+    if (h.ndone != G.ns) {
+        OSMPM_TRY(h.done.need(G.ns));
+        OSMPM_TRY(h.inbox.need(2 * G.ns));
+        OSMPM_CU(cudaMemsetAsync(h.done.p, 0, G.ns * sizeof(unsigned), G.st));
+        OSMPM_CU(cudaMemsetAsync(h.inbox.p, 0, 2 * G.ns * sizeof(unsigned), G.st));
+        h.ndone = G.ns;
+        h.rounds = 0;
+    }
+    const bool loop = G.ns > 1 && env_is("OSMPM_HALO_LOOPBACK", "1");
+    const bool alt = G.multi() || loop;
+    if (alt)
+        for (int i = 0; i < G.ns; ++i) OSMPM_TRY(G.s[i]->y2.need(G.s[i]->box.nnodes * D));
+    h.L.assign(G.ns, HaloLink{});
+    h.R.assign(G.ns, HaloLink{});
+    if (loop) {
+        for (int i = 0; i < G.ns; ++i) {
+            if (i > 0) {
+                Sub<D, R>* n = G.s[i - 1];
+                h.L[i] = HaloLink{{n->y.p, n->y2.p}, h.inbox.p + 2 * (i - 1) + 1, n->box.nn[0], true};
+            }
+            if (i + 1 < G.ns) {
+                Sub<D, R>* n = G.s[i + 1];
+                h.R[i] = HaloLink{{n->y.p, n->y2.p}, h.inbox.p + 2 * (i + 1) + 0, n->box.nn[0], true};
+            }
+        }
+    }
+    if (G.multi()) {
+        const GroupComm& gc = *G.gc;
+        HaloRec me{};
+        me.ok = 1;
+        me.ns = G.ns;
+        Sub<D, R>* f = G.s[0];
+        Sub<D, R>* l = G.s[G.ns - 1];
+        void* fb[HaloPeer::NB] = {f->y.p, f->y2.p, h.inbox.p};
+        void* lb[HaloPeer::NB] = {l->y.p, l->y2.p, h.inbox.p};
+        for (int k = 0; k < HaloPeer::NB; ++k) {
+            if (cudaIpcGetMemHandle(&me.first[k], fb[k]) != cudaSuccess) me.ok = 0;
+            if (cudaIpcGetMemHandle(&me.last[k], lb[k]) != cudaSuccess) me.ok = 0;
+        }
+        cudaGetLastError();
+        me.nn0_first = f->box.nn[0];
+        me.nn0_last = l->box.nn[0];
+        std::vector<HaloRec> all(gc.nranks);
+        OSMPM_TRY(G.gb->halo_tmp.need((sizeof(HaloRec) * (gc.nranks + 1) + 7) / 8));
+        unsigned char* dev = reinterpret_cast<unsigned char*>(G.gb->halo_tmp.p);
+        OSMPM_CU(cudaMemcpyAsync(dev, &me, sizeof(HaloRec), cudaMemcpyHostToDevice, G.st));
+        OSMPM_NCCL(ncclAllGather(dev, dev + sizeof(HaloRec), sizeof(HaloRec), ncclChar, gc.comm, G.st));
+        OSMPM_CU(cudaMemcpyAsync(all.data(), dev + sizeof(HaloRec), sizeof(HaloRec) * gc.nranks, cudaMemcpyDeviceToHost,
+                                 G.st));
+        OSMPM_CU(cudaStreamSynchronize(G.st));
+        // map the neighbours' buffers (re-opened only when a handle changed)
+        auto map = [&](HaloPeer& pr, const cudaIpcMemHandle_t* hs, int64_t nn0) -> bool {
+            pr.nn0 = nn0;
+            bool ok = true;
+            for (int k = 0; k < HaloPeer::NB; ++k) {
+                if (pr.p[k] && std::memcmp(&pr.h[k], &hs[k], sizeof(cudaIpcMemHandle_t)) == 0) continue;
+                if (pr.p[k]) cudaIpcCloseMemHandle(pr.p[k]);
+                pr.p[k] = nullptr;
+                pr.h[k] = hs[k];
+                if (cudaIpcOpenMemHandle(&pr.p[k], hs[k], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                    pr.p[k] = nullptr;
+                    ok = false;
+                }
+            }
+            cudaGetLastError();
+            return ok;
+        };
+        int ok = me.ok;
+        for (const HaloRec& r : all) ok = ok && r.ok;
+        if (ok && gc.rank > 0) ok = map(h.left, all[gc.rank - 1].last, all[gc.rank - 1].nn0_last);
+        if (ok && gc.rank + 1 < gc.nranks) ok = map(h.right, all[gc.rank + 1].first, all[gc.rank + 1].nn0_first);
+        // every rank takes the same path
+        double v = ok ? 1.0 : 0.0;
+        OSMPM_CU(cudaMemcpyAsync(G.gb->gsum.p, &v, sizeof(double), cudaMemcpyHostToDevice, G.st));
+        OSMPM_NCCL(ncclAllReduce(G.gb->gsum.p, G.gb->gsum.p, 1, ncclDouble, ncclMin, gc.comm, G.st));
+        OSMPM_CU(cudaMemcpyAsync(&v, G.gb->gsum.p, sizeof(double), cudaMemcpyDeviceToHost, G.st));
+        OSMPM_CU(cudaStreamSynchronize(G.st));
+        if (v < 1.0) return OSMPM_OK;
+        if (gc.rank > 0) {
+            const int nsl = all[gc.rank - 1].ns;  // the left rank's last slab, "from the right" word
+            h.L[0] = HaloLink{{static_cast<double*>(h.left.p[0]), static_cast<double*>(h.left.p[1])},
+                              static_cast<unsigned*>(h.left.p[2]) + 2 * (nsl - 1) + 1, h.left.nn0, true};
+        }
+        if (gc.rank + 1 < gc.nranks)  // the right rank's first slab, "from the left" word
+            h.R[G.ns - 1] = HaloLink{{static_cast<double*>(h.right.p[0]), static_cast<double*>(h.right.p[1])},
+                                     static_cast<unsigned*>(h.right.p[2]), h.right.nn0, true};
+    }
+    h.alt = alt;
+    h.phase = 0;
+    fused = true;
+    return OSMPM_OK;
+}
+
+// HaloDev of local slab i for the current iteration: protocol sides use the neighbour's buffer of the
+// iteration's parity and signal; plain sides point at the neighbour slab's current y
+template <int D, typename R>
+HaloDev halo_dev(SlabGroup<D, R> G, int i)
+{
+    HaloState& h = G.gb->halo;
+    Sub<D, R>* q = G.s[i];
+    const int64_t plane = q->plane_nodes();
+    const int par = h.phase & 1;
+    HaloDev d{};
+    d.done = h.done.p + i;
+    const HaloLink& l = h.L[i];
+    const HaloLink& r = h.R[i];
+    if (l.on) {
+        d.yL = l.y[par];
+        d.sigL = l.sig;
+        d.offL = (l.nn0 - 2) * plane;
+    } else if (i > 0) {
+        d.yL = G.s[i - 1]->y.p;
+        d.offL = (G.s[i - 1]->box.nn[0] - 2) * plane;
+    }
+    if (r.on) {
+        d.yR = r.y[par];
+        d.sigR = r.sig;
+    } else if (i + 1 < G.ns) {
+        d.yR = G.s[i + 1]->y.p;
+    }
+    if (d.yR) {
+        d.offR = -(int64_t)(q->box.nn[0] - 2) * plane;
+        d.ixR = q->box.nn[0] - 2;
+    }
+    return d;
+}
+
+// launches the HVP of every slab with its halo (fused) -- halo_hvp_launch -- then completes the halo:
+// the halo pass when not fused; in the alternating protocol each slab waits for its neighbours' signals
+// of this round (halo_hvp_finish)
+template <int D, typename R>
+osmpm_status halo_hvp_launch(SlabGroup<D, R> G, bool fused, DBuf<double> Sub<D, R>::* din, double* pkp)
+{
+    const bool use = fused && !G.s[0]->psd_active;
+    int64_t hoff = 0;
+    for (int i = 0; i < G.ns; ++i) {
+        Sub<D, R>* q = G.s[i];
+        if (use) {
+            const HaloDev d = halo_dev<D, R>(G, i);
+            OSMPM_TRY(q->launch_hvp((q->*din).p, q->y.p, pkp ? pkp + hoff : nullptr, &d));
+        } else {
+            OSMPM_TRY(q->launch_hvp((q->*din).p, q->y.p, pkp ? pkp + hoff : nullptr));
+        }
+        hoff += q->box.ntiles;
+    }
+    return OSMPM_OK;
+}
+template <int D, typename R>
+osmpm_status halo_hvp_finish(SlabGroup<D, R> G, bool fused)
+{
+    HaloState& h = G.gb->halo;
+    if (!fused || G.s[0]->psd_active) return halo_sum<D, R>(G, {{&Sub<D, R>::y, D}});
+    if (h.alt) {
+        h.rounds++;
+        for (int i = 0; i < G.ns; ++i) {
+            if (!h.L[i].on && !h.R[i].on) continue;
+            G.s[i]->KC();
+            k_halo_wait<<<1, 32, 0, G.st>>>(h.inbox.p + 2 * i, h.L[i].on ? h.rounds : 0u, h.R[i].on ? h.rounds : 0u,
+                                            G.s[i]->err.p);
+        }
+        OSMPM_LAUNCH_CHECK();
+    }
+    return OSMPM_OK;
+}
+
+// end of a fused PCG iteration (its y consumed and zeroed): the alternating protocol moves every slab
+// to its other buffer
+template <int D, typename R>
+void halo_next(SlabGroup<D, R> G, bool fused)
+{
+    HaloState& h = G.gb->halo;
+    if (!fused || !h.alt || G.s[0]->psd_active) return;
+    for (int i = 0; i < G.ns; ++i) {
+        std::swap(G.s[i]->y.p, G.s[i]->y2.p);
+        std::swap(G.s[i]->y.cap, G.s[i]->y2.cap);
+    }
+    h.phase++;
+}
+
+// start of a fused PCG run: the buffer of the first odd iteration must be zero too; end of the run:
+// back to the setup's buffer identities (so that the next exchange finds the same handles)
+template <int D, typename R>
+osmpm_status halo_run_begin(SlabGroup<D, R> G, bool fused)
+{
+    HaloState& h = G.gb->halo;
+    if (!fused || !h.alt || G.s[0]->psd_active) return OSMPM_OK;
+    for (int i = 0; i < G.ns; ++i)
+        OSMPM_CU(cudaMemsetAsync(G.s[i]->y2.p, 0, G.s[i]->box.nnodes * D * sizeof(double), G.st));
+    return OSMPM_OK;
+}
+template <int D, typename R>
+void halo_run_end(SlabGroup<D, R> G, bool fused)
+{
+    HaloState& h = G.gb->halo;
+    if (!fused || !h.alt) return;
+    if (h.phase & 1)
+        for (int i = 0; i < G.ns; ++i) {
+            std::swap(G.s[i]->y.p, G.s[i]->y2.p);
+            std::swap(G.s[i]->y.cap, G.s[i]->y2.cap);
+        }
+    h.phase = 0;
+}
+
 // in-place sum of n doubles across ranks (no-op on one rank)
 template <int D, typename R>
 osmpm_status group_allreduce(SlabGroup<D, R> G, double* d, int n)
@@ -233,12 +471,15 @@ osmpm_status group_energy(SlabGroup<D, R> G, bool trial)
 template <int D, typename R>
 osmpm_status group_hvp(SlabGroup<D, R> G)
 {
-    for (int i = 0; i < G.ns; ++i) {
-        Sub<D, R>* s = G.s[i];
-        OSMPM_CU(cudaMemsetAsync(s->y.p, 0, s->box.nnodes * D * sizeof(double), G.st));
-        OSMPM_TRY(s->launch_hvp(s->p.p, s->y.p));
-    }
-    OSMPM_TRY(halo_sum<D, R>(G, {{&Sub<D, R>::y, D}}));
+    // the fused halo between the slabs of this device (R24); across ranks the halo pass (this entry point
+    // is not a timed path)
+    bool fused = false;
+    if (!G.multi()) OSMPM_TRY(halo_setup<D, R>(G, fused));
+    for (int i = 0; i < G.ns; ++i)
+        OSMPM_CU(cudaMemsetAsync(G.s[i]->y.p, 0, G.s[i]->box.nnodes * D * sizeof(double), G.st));
+    OSMPM_TRY(halo_hvp_launch<D, R>(G, fused, &Sub<D, R>::p, nullptr));
+    OSMPM_TRY(halo_hvp_finish<D, R>(G, fused));
+    halo_run_end<D, R>(G, fused);
     for (int i = 0; i < G.ns; ++i) {
         Sub<D, R>* s = G.s[i];
         const int64_t nn = s->box.nnodes;
@@ -324,6 +565,8 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
     const int64_t nbM = nbd_tot;
     OSMPM_TRY(gb.partH.need((size_t)std::max<int64_t>(nbH, 1)));
     const bool remote = G.multi();
+    bool fused = false;  // the PCG's HVPs carry the halo of y (R24)
+    OSMPM_TRY(halo_setup<D, R>(G, fused));
     double g0 = 0.0, gref = 0.0;
     // Line search by gradient evaluations (default): each trial point's energy comes from the
     // gradient kernel, whose gradient, Jacobi diagonal and linearisation cache then serve the next
@@ -390,6 +633,7 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
         // the Newton direction (R6, R7, R22, R23): PCG with the exact tangent, or with the
         // PSD-projected one always (psd = 2) / when the first direction fails the descent check (psd = 1)
         auto run_pcg = [&](int variant) -> osmpm_status {
+        OSMPM_TRY(halo_run_begin<D, R>(G, fused));
         if (variant == 1) {
             // single-reduction PCG (Chronopoulos-Gear, R22): one reduction / all-reduce per iteration
             int64_t off = 0;
@@ -409,13 +653,9 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
             while (done_it < s->max_cg) {
                 const int cnt = std::min(chunk, s->max_cg - done_it);
                 for (int c = 0; c < cnt; ++c) {
-                    int64_t hoff = 0;
-                    for (int i = 0; i < G.ns; ++i) {
-                        OSMPM_TRY(G.s[i]->launch_hvp(G.s[i]->z.p, G.s[i]->y.p, gb.partH.p + hoff));
-                        hoff += G.s[i]->box.ntiles;
-                    }
+                    OSMPM_TRY(halo_hvp_launch<D, R>(G, fused, &Sub<D, R>::z, gb.partH.p));
                     if (pf.on) pf.begin("cg", st);
-                    OSMPM_TRY(halo_sum<D, R>(G, {{&Sub<D, R>::y, D}}));
+                    OSMPM_TRY(halo_hvp_finish<D, R>(G, fused));
                     if (!remote) {
                         s0->KC();
                         k_cgs_scalar<<<1, 1024, 0, st>>>(gb.partB.p, (int)nbM, gb.partH.p, (int)nbH, gb.cgs.p);
@@ -438,6 +678,7 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
                                                                          gb.partB.p + off * 3);
                         off += nblk(ndof, 256);
                     }
+                    halo_next<D, R>(G, fused);
                     if (pf.on) pf.end("cg", st);
                     OSMPM_LAUNCH_CHECK();
                 }
@@ -476,9 +717,9 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
         while (done_it < s->max_cg) {
             const int cnt = std::min(chunk, s->max_cg - done_it);
             for (int c = 0; c < cnt; ++c) {
-                for (int i = 0; i < G.ns; ++i) OSMPM_TRY(G.s[i]->launch_hvp(G.s[i]->p.p, G.s[i]->y.p));
+                OSMPM_TRY(halo_hvp_launch<D, R>(G, fused, &Sub<D, R>::p, nullptr));
                 if (pf.on) pf.begin("cg", st);
-                OSMPM_TRY(halo_sum<D, R>(G, {{&Sub<D, R>::y, D}}));
+                OSMPM_TRY(halo_hvp_finish<D, R>(G, fused));
                 int64_t off = 0;
                 for (int i = 0; i < G.ns; ++i) {
                     Sub<D, R>* q = G.s[i];
@@ -524,6 +765,7 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
                     q->KC();
                     k_cg_p<<<nblk(ndof, 256), 256, 0, st>>>(ndof, q->fmask.p, q->z.p, q->p.p, q->y.p, gb.cgs.p);
                 }
+                halo_next<D, R>(G, fused);
                 if (pf.on) pf.end("cg", st);
                 OSMPM_LAUNCH_CHECK();
             }
@@ -535,6 +777,7 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
             }
         }
         }  // standard PCG
+        halo_run_end<D, R>(G, fused);
         OSMPM_CU(cudaMemcpyAsync(gb.h_cgs, gb.cgs.p, sizeof(CGScalars), cudaMemcpyDeviceToHost, st));
         OSMPM_CU(cudaStreamSynchronize(st));
         sts->cg_iters += gb.h_cgs->it + (gb.h_cgs->done == 2 ? 1 : 0);
@@ -651,6 +894,9 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
         q->have_vnew = true;
         q->have_lin = false;  // the cache now refers to an intermediate point
     }
+    // a neighbour that never signalled (fused halo across ranks) is latched by k_halo_wait
+    if (rc == OSMPM_OK && gb.halo.alt)
+        for (int i = 0; i < G.ns; ++i) OSMPM_TRY(G.s[i]->check_err());
     return rc;
 }
 

@@ -60,10 +60,47 @@ static inline int nblk_all(int64_t n, int bs)
 // fixed-order final sum reduces the whole group (deterministic); across ranks the sums are
 // ncclAllReduce'd before use.
 struct CGScalars;
+// Host state of the fused HVP halo (R24, hvp_sw.cuh HaloDev): per-slab CTA completion
+// counters, this rank's inbox words (bumped by the neighbouring ranks' HVPs) and the neighbouring
+// ranks' y buffers and inboxes mapped over NVLink with CUDA IPC (cached by handle).
+struct HaloPeer {
+    static constexpr int NB = 3;  // y at the exchange, its double buffer, the inbox words
+    cudaIpcMemHandle_t h[NB];
+    void* p[NB] = {nullptr, nullptr, nullptr};
+    int64_t nn0 = 0;  // x node planes of the peer's box (its slab next to this rank)
+    void close()
+    {
+        for (int k = 0; k < NB; ++k)
+            if (p[k]) cudaIpcCloseMemHandle(p[k]);
+        for (int k = 0; k < NB; ++k) p[k] = nullptr;
+    }
+};
+struct HaloLink {  // one side of a local slab
+    double* y[2] = {nullptr, nullptr};  // alternating protocol: the neighbour's y / y2 at the setup
+    unsigned* sig = nullptr;            // the neighbour's inbox word this slab bumps
+    int64_t nn0 = 0;                    // the neighbour's x node planes
+    bool on = false;                    // the protocol runs on this side (else: plain pointer or none)
+};
+struct HaloState {
+    DBuf<unsigned> done;   // one completion counter per local slab (zero between launches)
+    DBuf<unsigned> inbox;  // per local slab: [2i] bumped by the left neighbour, [2i + 1] by the right one
+    int ndone = 0;
+    bool alt = false;      // some side runs the alternating protocol in this solve
+    unsigned rounds = 0;   // protocol HVP rounds since the inbox words were zeroed
+    int phase = 0;         // y / y2 swaps since the setup (selects the neighbours' buffer)
+    std::vector<HaloLink> L, R;
+    HaloPeer left, right;
+    ~HaloState()
+    {
+        left.close();
+        right.close();
+    }
+};
 struct GroupBufs {
     DBuf<double> partA, partB, partH, scal, gsum, halo_tmp;  // partH: the HVP's d^T K d partials (R22)
     DBuf<CGScalars> cgs;
     DBuf<int> gbounds;
+    HaloState halo;
     double* h_scal = nullptr;  // pinned
     CGScalars* h_cgs = nullptr;
     int* h_bounds = nullptr;
@@ -139,6 +176,7 @@ struct Sub : public osmpm_subdomain {
     bool have_grid = false, have_lin = false, have_vnew = false, have_vlast = false;
     DBuf<int> cell_start;
     DBuf<double> m, mom, vn, fsig, mb, dval, u, g, dg, xs, r, z, p, y, ut, vnew, tmp, cs;  // cs: s = H p (R22)
+    DBuf<double> y2;  // second HVP output buffer, alternated with y between ranks (fused halo, R24)
     DBuf<uint8_t> act, dmask, fmask;
     DirList dir_user, dir_cpl;
     DBuf<double> stage_io;  // persistent host-I/O staging buffer
@@ -698,7 +736,9 @@ struct Sub : public osmpm_subdomain {
     }
 
     // a5: the sliding-window tiled HVP (hvp_sw.cuh)
-    osmpm_status launch_hvp(const double* din, double* yout, double* pkp = nullptr)
+    // halo (optional): the fused halo of a slab group (R24); only the tiled fp64/fp32 kernel carries it
+    // (the caller falls back to halo_sum when psd_active or in deterministic mode)
+    osmpm_status launch_hvp(const double* din, double* yout, double* pkp = nullptr, const HaloDev* halo = nullptr)
     {
         auto& pf = ctx->prof;
         if (pf.on) pf.begin("hvp", st());
@@ -730,7 +770,8 @@ struct Sub : public osmpm_subdomain {
         const bool det = det_mode();
         if (det) OSMPM_TRY(det_a.need((size_t)box.ntiles * T::NN * D));
         KC(); k_hvp_sw<D, R><<<box.ntiles, T::NT, hvp_sw_smem_bytes<D, R>(), st()>>>(
-            P.p, cache.p, cap, cell_start.p, box, din, yout, tm_x, tm_c, tm_ok ? 1 : 0, det ? det_a.p : nullptr, pkp);
+            P.p, cache.p, cap, cell_start.p, box, din, yout, tm_x, tm_c, tm_ok ? 1 : 0, det ? det_a.p : nullptr, pkp,
+            (halo && !det) ? *halo : HaloDev{});
         if (det) {
             OSMPM_LAUNCH_CHECK();
             OSMPM_TRY(det_gather(det_a.p, yout));

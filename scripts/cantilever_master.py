@@ -35,6 +35,7 @@ Y0 = 1.0
 
 
 PSD = 0
+MAX_NEWTON = 100
 
 
 def newton(guess=1, rtol=1e-8):
@@ -43,7 +44,7 @@ def newton(guess=1, rtol=1e-8):
     --psd): 1 projects the per-particle tangent blocks when a Newton direction fails the descent test,
     2 always (R23)."""
     from paper_2605_09097_b200 import osmpm
-    return osmpm.newton_settings(newton_rtol=rtol, newton_atol=0.0, cg_rtol=1e-10, max_cg=40000, max_newton=100,
+    return osmpm.newton_settings(newton_rtol=rtol, newton_atol=0.0, cg_rtol=1e-10, max_cg=40000, max_newton=MAX_NEWTON,
                                  guess=guess, energy_noise_rtol=1e-12, psd=PSD)
 
 
@@ -142,8 +143,10 @@ if __name__ == "__main__":
     ap.add_argument("--guess", type=int, default=1)
     ap.add_argument("--rtol", type=float, default=1e-8)
     ap.add_argument("--psd", type=int, default=0, choices=[0, 1, 2])
+    ap.add_argument("--max-newton", type=int, default=100)
     a = ap.parse_args()
     PSD = a.psd
+    MAX_NEWTON = a.max_newton
     if a.mode == "res":
         G = [0.05]
         ref = elastica_row(0.05)

@@ -183,3 +183,40 @@ def test_decomposed_projection_matches_whole():
         f.close()
         ctx.close()
     assert rel_linf(res[0], res[1]) <= 1e-12
+
+
+@pytest.mark.parametrize("mode", ["fused", "pass", "loopback"])
+@pytest.mark.parametrize("name,slabs", [("3d", 3), ("2d", 4), ("3d8", 8)])
+def test_halo_modes(monkeypatch, mode, name, slabs):
+    """R24: the HVP's fused halo (every slab RED-s the planes it shares with a neighbour into the
+    neighbour's y too), the halo pass it replaces (OSMPM_FUSED_HALO=0), and the alternating-buffer /
+    inbox-signal protocol of the multi-rank halo run between local slabs (OSMPM_HALO_LOOPBACK=1) give the
+    oracle's HVP at 1e-11 and the oracle's fixed-iteration solves (both PCG variants) at 1e-9."""
+    from paper_2605_09097_b200 import osmpm
+    if mode == "pass":
+        monkeypatch.setenv("OSMPM_FUSED_HALO", "0")
+    if mode == "loopback":
+        monkeypatch.setenv("OSMPM_HALO_LOOPBACK", "1")
+    sc = synth.random_fixture(**FIX[name])
+    d = sc.grid.dim
+    ref = oracle.p2g(sc)
+    act = ref.active.astype(bool)
+    ctx = _ctx(slabs)
+    sub = _sub(ctx, sc)
+    sub.p2g()
+    u = random_u(ref.active, d, 2e-3 * sc.grid.dx, 11)
+    sub.newton_gradient(u)
+    dv = np.random.default_rng(12).normal(size=u.shape)
+    assert rel_linf(sub.newton_hvp(dv), oracle.hvp(sc, ref, u, dv)) <= TOL
+    kw = dict(max_newton=3, max_cg=41, fixed_iters=1)  # odd: the alternating buffers end on y2
+    for variant in (0, 1):
+        u_ref, st_ref = oracle.implicit_solve(sc, ref, oracle.default_settings(cg_variant=variant, **kw))
+        for rep in range(2):  # the second solve reuses the halo state (inbox counts, buffer identities)
+            sub.set_particles(x=sc.particles.x)
+            sub.p2g()
+            st = sub.implicit_solve(osmpm.newton_settings(cg_variant=variant, **kw))
+            assert st.status == 0 and st.cg_iters == st_ref.cg_iters
+            v = sub.read_grid_velocity()
+            assert rel_linf(v, np.where(act[:, None], u_ref / sc.dt, 0.0)) <= 1e-9, (variant, rep)
+    sub.close()
+    ctx.close()
