@@ -51,8 +51,17 @@ def parse():
                     help="PCG variant: 0 standard, 1 single-reduction (Chronopoulos-Gear, DESIGN.md R22: one "
                          "all-reduce per iteration); default 0 on one GPU, 1 on several")
     ap.add_argument("--slabs", type=int, default=1,
-                    help="x-slabs per GPU (>1: the decomposed path on one device, halo by device copies)")
-    return ap.parse_args()
+                    help="x-slabs per GPU (>1: the decomposed path on one device)")
+    ap.add_argument("--halo", default="fused", choices=["fused", "all", "pass"],
+                    help="halo of the PCG's HVP (DESIGN.md R24): fused between the slabs of a GPU and an NCCL "
+                         "halo pass between ranks (default); 'all' fuses across ranks too (IPC peer memory); "
+                         "'pass' uses the halo pass everywhere")
+    a = ap.parse_args()
+    if a.halo == "pass":
+        os.environ["OSMPM_FUSED_HALO"] = "0"
+    elif a.halo == "all":
+        os.environ["OSMPM_FUSED_HALO"] = "all"
+    return a
 
 
 # ------------------------------------------------------------------------------------------------
@@ -506,7 +515,7 @@ def main():
                    "solve_stats_last_step": last_stats,
                    "parallelism": (f"x-slabs x{slabs_total} (NCCL over NVLink, {world} GPUs)" if world > 1
                                    else (f"x-slabs x{slabs_total} on one GPU" if slabs_total > 1 else "single GPU")),
-                   "slab_cuts": cuts,
+                   "slab_cuts": cuts, "halo": args.halo,
                    "l2": "working set (>3 GB) far larger than the 126 MB L2; no flush needed"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak if achieved else None,
                      "traffic": traffic, "traffic_source": f"profiles/ncu_hvp_{args.precision}.json (ncu --set full)",

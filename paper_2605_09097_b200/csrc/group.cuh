@@ -108,7 +108,8 @@ osmpm_status halo_sum(SlabGroup<D, R> G, std::initializer_list<HField<D, R>> fie
 // rank's all-reduce of iteration c, which every peer reaches only after its kernels of iteration c - 1
 // (which zeroed the buffer the HVP of c + 1 writes) -- in both PCG variants.
 // OSMPM_HALO_LOOPBACK=1 runs that protocol (alternating buffers, inbox words, waits) between the local
-// slabs of one device, so that one GPU tests it; OSMPM_FUSED_HALO=0 restores the halo pass.
+// slabs of one device, so that one GPU tests it; OSMPM_FUSED_HALO=0 restores the halo pass; across ranks
+// the protocol is opt-in (OSMPM_FUSED_HALO=all).
 // ---------------------------------------------------------------------------------------------
 struct HaloRec {  // one rank's record of the exchange
     cudaIpcMemHandle_t first[HaloPeer::NB], last[HaloPeer::NB];
@@ -130,6 +131,9 @@ osmpm_status halo_setup(SlabGroup<D, R> G, bool& fused)
     h.alt = false;
     if (env_is("OSMPM_FUSED_HALO", "0")) return OSMPM_OK;
     if (G.ns == 1 && !G.multi()) return OSMPM_OK;
+    // across ranks only on request (OSMPM_FUSED_HALO=all): the IPC / inbox path has run on one GPU only
+    // (loopback), so multi-GPU runs keep the NCCL halo pass unless asked
+    if (G.multi() && !env_is("OSMPM_FUSED_HALO", "all")) return OSMPM_OK;
     for (int i = 0; i < G.ns; ++i)
         if (G.s[i]->det_mode()) return OSMPM_OK;
     if (h.ndone != G.ns) {
