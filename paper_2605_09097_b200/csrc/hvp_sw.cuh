@@ -192,7 +192,54 @@ __device__ __forceinline__ void sw_gather(const R* sv, const int* lc, const R (*
     using T = Tile<D>;
 #pragma unroll
     for (int k = 0; k < D * D; ++k) gd[k] = R(0);
-    if (D == 3) {
+    if constexpr (D == 3 && sizeof(R) == 4) {
+        // fp32 tiles: the same FMAs in the same order, paired into FFMA2 (fma.rn.f32x2: two lanes per
+        // issue; the FMA pipe takes a scalar FFMA only every second cycle per SMSP) -- (T0, T1) against
+        // (w_k, dw_k), (U0, U1) against (w_j, dw_j), (gd_1, gd_2) against w_i; bitwise the scalar result
+        const int n0 = sw_node<D>(lc[0], lc[1], lc[2]);
+        const float* base = reinterpret_cast<const float*>(sv) + n0 * 4;
+        float2 wz[3], wy[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            wz[k] = make_float2((float)w[2][k], (float)dw[2][k]);
+            wy[k] = make_float2((float)w[1][k], (float)dw[1][k]);
+        }
+        float g0[3] = {0.f, 0.f, 0.f};
+        float2 g12[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            float2 U01[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+            float U2[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                float2 Tp[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const float4 v = *reinterpret_cast<const float4*>(base + ((i * T::N1 + j) * SW<D>::NZP + k) * 4);
+                    Tp[0] = __ffma2_rn(make_float2(v.x, v.x), wz[k], Tp[0]);
+                    Tp[1] = __ffma2_rn(make_float2(v.y, v.y), wz[k], Tp[1]);
+                    Tp[2] = __ffma2_rn(make_float2(v.z, v.z), wz[k], Tp[2]);
+                }
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    U01[a] = __ffma2_rn(make_float2(Tp[a].x, Tp[a].x), wy[j], U01[a]);
+                    U2[a] = fmaf(Tp[a].y, wy[j].x, U2[a]);
+                }
+            }
+            const float w0 = (float)w[0][i], dw0 = (float)dw[0][i];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                g0[a] = fmaf(U01[a].x, dw0, g0[a]);
+                g12[a] = __ffma2_rn(make_float2(U01[a].y, U2[a]), make_float2(w0, w0), g12[a]);
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            gd[a * 3 + 0] = (R)g0[a];
+            gd[a * 3 + 1] = (R)g12[a].x;
+            gd[a * 3 + 2] = (R)g12[a].y;
+        }
+    } else if (D == 3) {
         constexpr int NS = SVS<D, R>::S;
         const int n0 = sw_node<D>(lc[0], lc[1], lc[2]);
         const R* base = sv + n0 * NS;
