@@ -21,6 +21,15 @@ void set_error(const char* fmt, ...)
     va_end(ap);
     g_err = buf;
 }
+void prefix_error(const char* fmt, ...)
+{
+    char buf[256];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = std::string(buf) + g_err;
+}
 
 cudaEvent_t Profiler::begin(const std::string& name, cudaStream_t s)
 {

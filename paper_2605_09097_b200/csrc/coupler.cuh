@@ -381,7 +381,13 @@ struct Coupler : public osmpm_coupler {
         // every local slab gets this rank's receiver list (each keeps the nodes of its own box)
         for (int i = 0; i < G.ns; ++i)
             OSMPM_TRY(G.s[i]->set_dirlist(G.s[i]->dir_cpl, nS, dS.p, maskS.p, vbc.p, OSMPM_DEVICE));
-        OSMPM_TRY(fine->implicit_solve(&set.fine, stats));
+        {
+            const osmpm_status rc = fine->implicit_solve(&set.fine, stats);
+            if (rc != OSMPM_OK) {
+                prefix_error("fine solve, sub-step %d: ", m);
+                return rc;
+            }
+        }
         if (m == set.M) {
             // v_GammaB^(k+1) = Pi(last sub-step's solved fine velocities) (R16)
             const int64_t nnB = B->dense_nodes();
@@ -434,12 +440,24 @@ struct Coupler : public osmpm_coupler {
             // Step 1: coarse solve with Dirichlet Gamma-hat_B <- v_GammaB^(k) (Eq. implicit_solve_coarse),
             // restarting from the frozen step-0 coarse grid (R14)
             OSMPM_TRY(B->set_dirlist(B->dir_cpl, nB, dB.p, maskB.p, vGB.p, OSMPM_DEVICE));
-            OSMPM_TRY(B->implicit_solve(&set.coarse, nullptr));
+            {
+                const osmpm_status rc = B->implicit_solve(&set.coarse, nullptr);
+                if (rc != OSMPM_OK) {
+                    prefix_error("coarse solve, Schwarz iteration %d: ", k + 1);
+                    return rc;
+                }
+            }
             // Step 2: restore the fine particles (Alg. 1) and sub-cycle
             OSMPM_TRY(fine->restore());
             OSMPM_TRY(fine->p2g());
             for (int m = 1; m <= set.M; ++m) {
-                OSMPM_TRY(substep(m, nullptr));
+                {
+                    const osmpm_status rc = substep(m, nullptr);
+                    if (rc != OSMPM_OK) {
+                        prefix_error("Schwarz iteration %d, ", k + 1);
+                        return rc;
+                    }
+                }
                 RP->fine_substeps++;
             }
             // Step 3: interface residuals (Eqs. convergence_residuals / criterion); r_S over this rank's

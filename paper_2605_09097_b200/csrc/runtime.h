@@ -14,6 +14,7 @@
 namespace osmpm {
 
 void set_error(const char* fmt, ...);
+void prefix_error(const char* fmt, ...);  // prepends context to the current message
 
 #define OSMPM_CU(call)                                                                              \
     do {                                                                                            \

@@ -80,8 +80,10 @@ def run(inv_hs, max_rounds=30, ramp=1):
     gap = np.zeros(xsS.shape[0])
     xp = np.minimum(np.abs(xsS[plane, 0]), hz.R)
     gap[plane] = hz.R - np.sqrt(hz.R * hz.R - xp * xp)
-    ns = osmpm.newton_settings(newton_rtol=1e-8, cg_rtol=1e-10, max_cg=60000, max_newton=60, guess=1,
-                               energy_noise_rtol=1e-12)
+    # at 1/256 the relative 1e-8 sits below E_h's round-off floor (Newton stalls near 6e-5 of |g0|): the
+    # fine solves stop at 1e-6 of |g0| there, far below the nodal reactions the pressure is read from
+    ns = osmpm.newton_settings(newton_rtol=1e-8 if inv_hs < 256 else 1e-6, cg_rtol=1e-10, max_cg=60000,
+                               max_newton=60, guess=1, energy_noise_rtol=1e-12 if inv_hs < 256 else 1e-9)
     cpl = osmpm.Coupler(sb, ss, osmpm.schwarz_settings(M=1, eps_conv=1e-5, k_max=2000, coarse=ns, fine=ns))
     sb.checkpoint()
     ss.checkpoint()
