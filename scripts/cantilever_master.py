@@ -144,6 +144,7 @@ if __name__ == "__main__":
     ap.add_argument("--rtol", type=float, default=1e-8)
     ap.add_argument("--psd", type=int, default=0, choices=[0, 1, 2])
     ap.add_argument("--max-newton", type=int, default=100)
+    ap.add_argument("--no-single", action="store_true")
     a = ap.parse_args()
     PSD = a.psd
     MAX_NEWTON = a.max_newton
@@ -160,7 +161,7 @@ if __name__ == "__main__":
     else:
         for dxb in a.dxb:
             line = {"mode": "curve", "dx_B": dxb, "elastica": [elastica_row(G) for G in a.gammas],
-                    "single": run_single(dxb, a.gammas, a.dT, guess=a.guess, rtol=a.rtol)}
+                    "single": [] if a.no_single else run_single(dxb, a.gammas, a.dT, guess=a.guess, rtol=a.rtol)}
             print(json.dumps(line), flush=True)
             if not a.no_dual:
                 line["dual"] = run_dual(dxb, a.gammas, dT=a.dT, guess=a.guess, rtol=a.rtol)

@@ -82,8 +82,9 @@ def run(inv_hs, max_rounds=30, ramp=1):
     gap[plane] = hz.R - np.sqrt(hz.R * hz.R - xp * xp)
     # at 1/256 the relative 1e-8 sits below E_h's round-off floor (Newton stalls near 6e-5 of |g0|): the
     # fine solves stop at 1e-6 of |g0| there, far below the nodal reactions the pressure is read from
-    ns = osmpm.newton_settings(newton_rtol=1e-8 if inv_hs < 256 else 1e-6, cg_rtol=1e-10, max_cg=60000,
-                               max_newton=60, guess=1, energy_noise_rtol=1e-12 if inv_hs < 256 else 1e-9)
+    fine_h = inv_hs >= 256
+    ns = osmpm.newton_settings(newton_rtol=1e-6 if fine_h else 1e-8, cg_rtol=1e-10, max_cg=100000 if fine_h else 60000,
+                               max_newton=200 if fine_h else 60, guess=1, energy_noise_rtol=1e-9 if fine_h else 1e-12)
     cpl = osmpm.Coupler(sb, ss, osmpm.schwarz_settings(M=1, eps_conv=1e-5, k_max=2000, coarse=ns, fine=ns))
     sb.checkpoint()
     ss.checkpoint()
@@ -149,8 +150,8 @@ def run(inv_hs, max_rounds=30, ramp=1):
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--inv-hs", type=int, nargs="+", default=[64, 128, 256])
-    ap.add_argument("--ramp", type=int, nargs="+", default=None, help="load steps per h_S (default 1, 1, 4)")
+    ap.add_argument("--ramp", type=int, nargs="+", default=None, help="load steps per h_S (default 1, 1, 8)")
     a = ap.parse_args()
-    ramps = a.ramp or [1 if n < 256 else 4 for n in a.inv_hs]
+    ramps = a.ramp or [1 if n < 256 else 8 for n in a.inv_hs]
     for n, rp in zip(a.inv_hs, ramps):
         print(json.dumps(run(n, ramp=rp)), flush=True)
