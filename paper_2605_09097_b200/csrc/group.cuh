@@ -569,6 +569,8 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
     const int64_t nbM = nbd_tot;
     OSMPM_TRY(gb.partH.need((size_t)std::max<int64_t>(nbH, 1)));
     const bool remote = G.multi();
+    // one slab, no exchange: the standard PCG's alpha / beta are set by the last block of its vector kernels
+    const bool cg_last = G.ns == 1 && !remote;
     bool fused = false;  // the PCG's HVPs carry the halo of y (R24)
     OSMPM_TRY(halo_setup<D, R>(G, fused));
     double g0 = 0.0, gref = 0.0;
@@ -724,6 +726,22 @@ osmpm_status group_solve(SlabGroup<D, R> G, const osmpm_newton_settings* s, osmp
                 OSMPM_TRY(halo_hvp_launch<D, R>(G, fused, &Sub<D, R>::p, nullptr));
                 if (pf.on) pf.begin("cg", st);
                 OSMPM_TRY(halo_hvp_finish<D, R>(G, fused));
+                if (cg_last) {
+                    Sub<D, R>* q = s0;
+                    const int64_t nn = q->box.nnodes, ndof = nn * D;
+                    q->KC();
+                    k_cg_q_alpha<D><<<nblk(nn, 256), 256, 0, st>>>(nn, q->nown, q->fmask.p, q->m.p, idt2, q->p.p,
+                                                                   q->y.p, gb.cgs.p, gb.partB.p, gb.tick.p);
+                    q->KC();
+                    k_cg_update_beta<D><<<nblk(ndof, 256), 256, 0, st>>>(ndof, q->nown * D, q->fmask.p, q->m.p, idt2,
+                                                                         q->p.p, q->y.p, q->dg.p, q->xs.p, q->r.p,
+                                                                         q->z.p, gb.cgs.p, gb.partB.p, gb.tick.p + 1);
+                    q->KC();
+                    k_cg_p<<<nblk(ndof, 256), 256, 0, st>>>(ndof, q->fmask.p, q->z.p, q->p.p, q->y.p, gb.cgs.p);
+                    if (pf.on) pf.end("cg", st);
+                    OSMPM_LAUNCH_CHECK();
+                    continue;
+                }
                 int64_t off = 0;
                 for (int i = 0; i < G.ns; ++i) {
                     Sub<D, R>* q = G.s[i];

@@ -520,6 +520,88 @@ __global__ void k_cg_p(int64_t ndof, const uint8_t* __restrict__ fm, const doubl
 }
 
 // ---------------------------------------------------------------------------------------------
+// Standard PCG of one slab (no exchange between the partial sums and the scalars): 3 vector kernels
+// per iteration instead of 3 + 2 single-block ones.  The last block of k_cg_q_alpha / k_cg_update_beta
+// to finish (an atomic ticket after each block's partial is fenced) reduces all block partials in the
+// fixed order of final_sum and sets alpha / beta itself.  k_cg_q_alpha only reduces p.q; the update
+// recomputes q = y + m/dt^2 p with the same expression instead of reading it back (one vector write
+// less per iteration).  Same scalars and vectors as k_cg_q / k_cg_alpha / k_cg_update / k_cg_beta.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ bool last_block_ticket(unsigned* counter)
+{
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    return last;
+}
+
+template <int D>
+__global__ void k_cg_q_alpha(int64_t nn, int64_t nown, const uint8_t* __restrict__ fm, const double* __restrict__ m,
+                             double idt2, const double* __restrict__ p, const double* __restrict__ y, CGScalars* s,
+                             double* __restrict__ partials, unsigned* counter)
+{
+    if (s->done) return;
+    double red[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const int64_t k = i * D + a;
+            if (!fm[k]) continue;
+            const double q = y[k] + m[i] * idt2 * p[k];
+            if (i < nown) red[0] += p[k] * q;
+        }
+    }
+    block_reduce_store<1>(red, partials);
+    if (last_block_ticket(counter)) {
+        double v[1];
+        final_sum<1>(partials, gridDim.x, v);
+        if (threadIdx.x == 0) {
+            cg_alpha(v, s);
+            *counter = 0u;
+        }
+    }
+}
+
+template <int D>
+__global__ void k_cg_update_beta(int64_t ndof, int64_t nown_dof, const uint8_t* __restrict__ fm,
+                                 const double* __restrict__ m, double idt2, const double* __restrict__ p,
+                                 const double* __restrict__ y, const double* __restrict__ dg, double* __restrict__ x,
+                                 double* __restrict__ r, double* __restrict__ z, CGScalars* s,
+                                 double* __restrict__ partials, unsigned* counter)
+{
+    if (s->done) return;
+    const double al = s->alpha;
+    double red[2] = {0.0, 0.0};
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ndof; k += (int64_t)gridDim.x * blockDim.x) {
+        if (!fm[k]) continue;
+        const double q = y[k] + m[k / D] * idt2 * p[k];
+        const double xk = x[k] + al * p[k];
+        const double rk = r[k] - al * q;
+        const double zk = rk / dg[k];
+        x[k] = xk;
+        r[k] = rk;
+        z[k] = zk;
+        if (k < nown_dof) {
+            red[0] += rk * zk;
+            red[1] += rk * rk;
+        }
+    }
+    block_reduce_store<2>(red, partials);
+    if (last_block_ticket(counter)) {
+        double v[2];
+        final_sum<2>(partials, gridDim.x, v);
+        if (threadIdx.x == 0) {
+            cg_beta(v, s);
+            *counter = 0u;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Single-reduction Jacobi PCG (Chronopoulos & Gear; R22), one reduction per iteration:
 //   init      r = -g, u = diag^-1 r, x = p = s = 0, y = 0;  partials {r.u, r.r, u^T M u / dt^2}
 //   HVP(u)    y = K u; per-CTA partials u^T K u

@@ -99,6 +99,7 @@ struct HaloState {
 struct GroupBufs {
     DBuf<double> partA, partB, partH, scal, gsum, halo_tmp;  // partH: the HVP's d^T K d partials (R22)
     DBuf<CGScalars> cgs;
+    DBuf<unsigned> tick;  // last-block tickets of k_cg_q_alpha / k_cg_update_beta (reset by the last block)
     DBuf<int> gbounds;
     HaloState halo;
     double* h_scal = nullptr;  // pinned
@@ -113,6 +114,8 @@ struct GroupBufs {
         OSMPM_TRY(scal.need(64));
         OSMPM_TRY(gsum.need(8));
         OSMPM_TRY(cgs.need(1));
+        OSMPM_TRY(tick.need(2));
+        OSMPM_CU(cudaMemset(tick.p, 0, 2 * sizeof(unsigned)));
         OSMPM_TRY(gbounds.need(8));
         return OSMPM_OK;
     }
