@@ -27,8 +27,16 @@
 
 namespace osmpm {
 
+// threads of an HVP CTA.  3D: 128 = 16 cells x 8 (component, x-offset) items, four full warps; the
+// ninth item (component 2, x-offset 2) of each cell is split over the cell's eight lanes, one particle
+// each (SPLIT9), and its emitted plane is summed over them with shuffles -- instead of a fifth,
+// half-populated warp that idles through phase 1 and runs its FP64 work at half width.  2D: 96.
+template <int D> struct HvpT {
+    static constexpr int NT = (D == 3) ? 128 : Tile<D>::NT;
+    static constexpr bool SPLIT9 = D == 3;
+};
 // warps per HVP CTA (the per-warp curvature partials of k_hvp_sw)
-template <int D> constexpr int HVP_NW = (Tile<D>::NT + 31) / 32;
+template <int D> constexpr int HVP_NW = (HvpT<D>::NT + 31) / 32;
 
 template <int D, typename R> struct SWRec {
     // G row a starts at GROW(a): 3D fp64 rows padded to 4 reals (16-B aligned: one 16-B + one 8-B load
@@ -86,27 +94,30 @@ __device__ __forceinline__ void sw_stage_tile(const BoxDev& b, const int* t, con
 {
     using T = Tile<D>;
     constexpr int ROWS = T::N0 * T::N1, RL = T::N2 * D;  // 3D: rows along z are contiguous in global memory
-    if constexpr (D == 3 && NTHR % ROWS == 0) {
+    if constexpr (D == 3 && NTHR >= ROWS) {
         // thread -> (row, part): one row base address per thread, then every TPR-th element of the row
-        // with its (node, component) advanced incrementally (no per-element index divisions)
+        // with its (node, component) advanced incrementally (no per-element index divisions); threads
+        // beyond TPR * ROWS stay idle
         constexpr int TPR = NTHR / ROWS;
         const int row = threadIdx.x / TPR, part = threadIdx.x % TPR;
-        const int c0 = row / T::N1, c1 = row % T::N1;
-        const double* gs = src + box_node<D>(b, t[0] * T::T0 + c0, t[1] * T::T1 + c1, t[2] * T::T2) * D;
-        const int n0 = sw_node<D>(c0, c1, 0);
-        int z = part / D, a = part % D;
+        if (row < ROWS) {
+            const int c0 = row / T::N1, c1 = row % T::N1;
+            const double* gs = src + box_node<D>(b, t[0] * T::T0 + c0, t[1] * T::T1 + c1, t[2] * T::T2) * D;
+            const int n0 = sw_node<D>(c0, c1, 0);
+            int z = part / D, a = part % D;
 #pragma unroll
-        for (int e = part; e < RL; e += TPR) {
-            R* dst = sv + sv_elem<D, R>(n0 + z, a, SW<D>::NNP);
-            if constexpr (sizeof(R) == 8)
-                cp_async_8(dst, gs + e);
-            else
-                *dst = (R)gs[e];
-            a += TPR % D;
-            z += TPR / D;
-            if (a >= D) {
-                a -= D;
-                z += 1;
+            for (int e = part; e < RL; e += TPR) {
+                R* dst = sv + sv_elem<D, R>(n0 + z, a, SW<D>::NNP);
+                if constexpr (sizeof(R) == 8)
+                    cp_async_8(dst, gs + e);
+                else
+                    *dst = (R)gs[e];
+                a += TPR % D;
+                z += TPR / D;
+                if (a >= D) {
+                    a -= D;
+                    z += 1;
+                }
             }
         }
     } else {
@@ -153,12 +164,12 @@ static inline PFN_encodeTiled encode_tiled_fn()
 template <int D, typename R> struct SWIn {
     static constexpr int NF = D + CL<D>::NF;
     static constexpr int UE = 16 / sizeof(R);
-    static constexpr int PFS = Tile<D>::NT + UE;
+    static constexpr int PFS = HvpT<D>::NT + UE;
     static constexpr int XB = (int)(((D * PFS * sizeof(R) + 127) / 128 * 128) / sizeof(R));
     static constexpr int TOT = XB + CL<D>::NF * PFS;
     static __host__ __device__ constexpr int off(int f) { return f < D ? f * PFS : XB + (f - D) * PFS; }
 };
-static_assert(Tile<3>::NT % 4 == 0 && Tile<2>::NT % 4 == 0, "NT a multiple of the 16-B unit");
+static_assert(HvpT<3>::NT % 4 == 0 && HvpT<2>::NT % 4 == 0, "NT a multiple of the 16-B unit");
 
 template <typename R>
 static inline bool encode_fields_map(CUtensorMap* m, const R* base, int nfields, int64_t cap, int box_particles)
@@ -180,7 +191,7 @@ constexpr size_t hvp_sw_smem_bytes()
     using T = Tile<D>;
     return 16 + 128 /* alignment of the streamed-input block */ + ((size_t)SW<D>::NNP * SVS<D, R>::S + SW<D>::STG +
                  (size_t)SWIn<D, R>::TOT +
-                 (size_t)SWRec<D, R>::RS * T::NT) *
+                 (size_t)SWRec<D, R>::RS * HvpT<D>::NT) *
                     sizeof(R);
 }
 
@@ -392,10 +403,11 @@ __global__ void k_halo_wait(const unsigned* inbox, unsigned expL, unsigned expR,
 template <int D, typename R, bool DOT>
 __device__ __forceinline__ void sw_flush(const BoxDev& b, const int* t, int plane, const R* stg,
                                          double* __restrict__ out, double* __restrict__ tb, const R* sv,
-                                         const double* __restrict__ din, double& dot, const HaloDev* hl = nullptr)
+                                         const double* __restrict__ din, double& dot, const HaloDev* hl = nullptr,
+                                         int nthr = Tile<D>::NT)
 {
     using T = Tile<D>;
-    for (int it = threadIdx.x; it < SW<D>::NITEM; it += T::NT) {
+    for (int it = threadIdx.x; it < SW<D>::NITEM; it += nthr) {
         // slot-major staging: consecutive threads read consecutive reals (conflict-free)
         R s = stg[it];
 #pragma unroll
@@ -495,7 +507,7 @@ __device__ __forceinline__ void sw_prefetch(const R* __restrict__ P, const R* __
     using In = SWIn<D, R>;
     static_assert(In::NF <= 32, "one field per lane");
     const int lb0 = lb & ~(In::UE - 1);                       // 16-B aligned start
-    const int cnt = min(le, lb + Tile<D>::NT) - lb0;
+    const int cnt = min(le, lb + HvpT<D>::NT) - lb0;
     const uint32_t bytes = (uint32_t)((cnt + In::UE - 1) & ~(In::UE - 1)) * sizeof(R);
     fence_async_smem();
     if (lane == 0) mbar_expect_tx(bar, bytes * In::NF);
@@ -535,10 +547,10 @@ __device__ __forceinline__ void sw_prefetch_tmap(const CUtensorMap* mx, const CU
     }
 }
 
-// 3 CTAs per SM in fp64 (128 registers; shared memory 75 KB); the fp32 variant has half the shared
-// memory (records, streamed inputs, node tile and staging in fp32) and fewer live registers: 4
+// 3 CTAs per SM in fp64 (shared memory ~71 KB); the fp32 variant has half the shared memory (records,
+// streamed inputs, node tile and staging in fp32): 4
 template <int D, typename R>
-__global__ void __launch_bounds__(Tile<D>::NT, sizeof(R) == 8 ? 3 : 4)
+__global__ void __launch_bounds__(HvpT<D>::NT, sizeof(R) == 8 ? 3 : 4)
 k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, const int* __restrict__ cell_start,
          BoxDev b, const double* __restrict__ din, double* __restrict__ yout, const __grid_constant__ CUtensorMap tmx,
          const __grid_constant__ CUtensorMap tmc, int use_tmap, double* __restrict__ tbuf,
@@ -552,6 +564,8 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
     using S = SW<D>;
     using SR = SWRec<D, R>;
     constexpr int RS = SR::RS;
+    constexpr int NTH = HvpT<D>::NT;
+    constexpr bool SPLIT9 = HvpT<D>::SPLIT9;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
     R* sv = reinterpret_cast<R*>(smem_raw + 16);
@@ -592,9 +606,9 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                 sw_prefetch<D, R>(P, cache, cap, lb0, le0, pf, bar, lane);
         }
     }
-    if constexpr (ASYNC) sw_stage_tile<D, R, T::NT, false>(b, t, din, sv);
-    for (int i = threadIdx.x; i <= T::NC; i += T::NT) scs[i] = cell_start[kt + i];
-    for (int k = threadIdx.x; k < S::STG; k += T::NT) stg[k] = R(0);
+    if constexpr (ASYNC) sw_stage_tile<D, R, NTH, false>(b, t, din, sv);
+    for (int i = threadIdx.x; i <= T::NC; i += NTH) scs[i] = cell_start[kt + i];
+    for (int k = threadIdx.x; k < S::STG; k += NTH) stg[k] = R(0);
     __syncthreads();
     if (scs[0] == scs[T::NC]) {
         if constexpr (ASYNC) asm volatile("cp.async.wait_all;" ::: "memory");
@@ -608,15 +622,15 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
     if constexpr (ASYNC)
         asm volatile("cp.async.wait_all;" ::: "memory");
     else
-        sw_stage_tile<D, R, T::NT>(b, t, din, sv);
+        sw_stage_tile<D, R, NTH>(b, t, din, sv);
     __syncthreads();
     const int it = threadIdx.x;
     int icell, icomp, ii;
     item_of<D>(it, icell, icomp, ii);
     uint32_t parity = 0;
-    R acc[S::NACC];
+    R acc[S::NACC], acc9[S::NACC];  // acc9: this lane's share of its cell's ninth item (SPLIT9)
 #pragma unroll
-    for (int k = 0; k < S::NACC; ++k) acc[k] = R(0);
+    for (int k = 0; k < S::NACC; ++k) acc[k] = acc9[k] = R(0);
     for (int layer = 0; layer < T::NL + 2; ++layer) {
         if (layer < T::NL && !layer_empty(layer)) {
             const int lb = scs[layer * T::LC], le = scs[(layer + 1) * T::LC];
@@ -625,8 +639,8 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
             const int pf_base = lb & ~(In::UE - 1);
             const int ks = scs[layer * T::LC + icell];
             const int ke = scs[layer * T::LC + icell + 1];
-            for (int sb = lb; sb < le; sb += T::NT) {
-                const int se = min(sb + T::NT, le);
+            for (int sb = lb; sb < le; sb += NTH) {
+                const int se = min(sb + NTH, le);
                 const int q = threadIdx.x, p = sb + q;
                 const bool from_pf = sb == lb;
                 if (sb != lb) __syncthreads();  // previous chunk's records consumed
@@ -727,7 +741,10 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                     // (icell & 7) % len without the integer division when len >= 8 (the usual case)
                     const int len = p1 - p0, r7 = icell & 7;
                     const int rot = r7 < len ? r7 : (len > 0 ? r7 % len : 0);
-                    constexpr int kUnroll = 4;  // (measured: 2 / 8 slower)
+#ifndef OSMPM_P2_UNROLL
+#define OSMPM_P2_UNROLL 8
+#endif
+                    constexpr int kUnroll = OSMPM_P2_UNROLL;  // 128-thread CTAs: 8 (measured 1.3022 ms vs 1.3043 at 4, 1.3103 at 2)
 #pragma unroll kUnroll
                     for (int k = 0; k < len; ++k) {
                         const RecPtr<R> r(rec, rotated(p0, len, k, rot) - sb, RS);
@@ -738,25 +755,60 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                         for (int bb = 0; bb < D; ++bb) s[bb] = *r.at(Rec<D>::G + icomp * SR::GP + bb);
                         item_linear<D, R>(s, W, acc);
                     }
+                    if constexpr (SPLIT9) {
+                        // the cell's ninth item: particles pr, pr + 8, ... of the cell in this chunk
+#pragma unroll 1
+                        for (int k = it & 7; k < len; k += 8) {
+                            const RecPtr<R> r(rec, p0 + k - sb, RS);
+                            ItemW<D, R> W;
+                            R s[D];
+                            W.load(r, 2);
+#pragma unroll
+                            for (int bb = 0; bb < D; ++bb) s[bb] = *r.at(Rec<D>::G + 2 * SR::GP + bb);
+                            item_linear<D, R>(s, W, acc9);
+                        }
+                    }
                 }
             }
         }
         // node plane `layer` is complete: stage it, then sum the slots and RED
         if (it < T::ITEMS) sw_emit<D, R>(icell, icomp, ii, acc, stg);
+        if constexpr (SPLIT9) {
+            // the ninth item's plane: the eight lanes' shares summed over the quarter warp (fixed
+            // butterfly order), staged by its first lane; every lane shifts its own window
+            R e9[3];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                e9[j] = acc9[j * 3 + 0];
+#pragma unroll
+                for (int o = 4; o > 0; o >>= 1) e9[j] += __shfl_xor_sync(0xffffffffu, e9[j], o);
+            }
+            if ((it & 7) == 0) {
+#pragma unroll
+                for (int j = 0; j < 3; ++j) acc9[j * 3 + 0] = e9[j];
+                sw_emit<D, R>(icell, 2, 2, acc9, stg);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    acc9[j * 3 + 0] = acc9[j * 3 + 1];
+                    acc9[j * 3 + 1] = acc9[j * 3 + 2];
+                    acc9[j * 3 + 2] = R(0);
+                }
+            }
+        }
         __syncthreads();
         {
             double* tbl = tbuf ? tbuf + (int64_t)tile * T::NN * D : nullptr;
             const HaloDev* hl = fused ? &halo : nullptr;
             if (pkp)
-                sw_flush<D, R, true>(b, t, layer, stg, yout, tbl, sv, din, dkd, hl);
+                sw_flush<D, R, true>(b, t, layer, stg, yout, tbl, sv, din, dkd, hl, NTH);
             else
-                sw_flush<D, R, false>(b, t, layer, stg, yout, tbl, sv, din, dkd, hl);
+                sw_flush<D, R, false>(b, t, layer, stg, yout, tbl, sv, din, dkd, hl, NTH);
         }
         // the next emit must not overwrite slots still being summed: a non-empty next layer has its
         // records barrier in between; otherwise synchronise here
         if (pkp && layer == T::NL + 1) {
-            // warp partials of the curvature into shared memory before the closing barrier (the last
-            // warp of a 144-thread CTA has 16 lanes)
+            // warp partials of the curvature into shared memory before the closing barrier
             const unsigned mask = __activemask();
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) dkd += __shfl_xor_sync(mask, dkd, o);

@@ -772,7 +772,7 @@ struct Sub : public osmpm_subdomain {
         }
         const bool det = det_mode();
         if (det) OSMPM_TRY(det_a.need((size_t)box.ntiles * T::NN * D));
-        KC(); k_hvp_sw<D, R><<<box.ntiles, T::NT, hvp_sw_smem_bytes<D, R>(), st()>>>(
+        KC(); k_hvp_sw<D, R><<<box.ntiles, HvpT<D>::NT, hvp_sw_smem_bytes<D, R>(), st()>>>(
             P.p, cache.p, cap, cell_start.p, box, din, yout, tm_x, tm_c, tm_ok ? 1 : 0, det ? det_a.p : nullptr, pkp,
             (halo && !det) ? *halo : HaloDev{});
         if (det) {
