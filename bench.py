@@ -133,6 +133,16 @@ HVP_FLOPS_PER_PARTICLE = 540 + 217 + 459 + 40
 # FP64 (and, at 2x, FP32) vector peak: 148 SMs x 64 FP64 lanes x 2 flops (FMA) x 1.965 GHz
 # (B200_PROFILING.md: 148 SMs, clocks.max.sm 1965 MHz; sm_100 FP64 rate half of FP32's 128 lanes/SM)
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+# algorithmic flops per particle per call of the other particle kernels
+SURVEY_FLOPS_PER_PARTICLE = {"p2g": 1750, "grad": 1200, "g2p": 1200}
+
+
+def roofline_bound(bytes_, flops, hbm_gbs, fp_tflops):
+    """Which roofline bounds a kernel (SURVEY.md §8(d) "the achieved bound is min(HBM, FP pipe)"): the
+    slower of the algorithmic bytes at the HBM peak and the algorithmic flops at the CUDA-core FP peak."""
+    t_hbm = bytes_ / (hbm_gbs * 1e9)
+    t_fp = flops / (fp_tflops * 1e12)
+    return ("alu" if t_fp > t_hbm else "hbm"), t_hbm, t_fp
 
 
 def hvp_algorithmic_bytes(n_particles, n_active_nodes, word):
@@ -163,11 +173,12 @@ def fp32_variant(args):
     except Exception as e:  # reported, not fatal: the f64 line stands on its own
         return {"unavailable": f"{type(e).__name__}: {e}"[:200]}
     return {"value": d["value"], "unit": d["unit"], "ms_per_step": d["ms_per_step"], "dtype": d["dtype"],
-            "roofline": {k: d["roofline"].get(k) for k in ("achieved", "peak", "frac", "avg_launch_ms", "traffic")},
+            "roofline": {k: d["roofline"].get(k) for k in ("bound", "achieved", "peak", "unit", "frac", "avg_launch_ms",
+                                                           "traffic", "hbm", "fp_pipe")},
             "kernel_ms_per_step": d["kernel_ms_per_step"], "clocks": d.get("clocks")}
 
 
-def transfer_rooflines(fam, n_particles, n_active_nodes, word, peak):
+def transfer_rooflines(fam, n_particles, n_active_nodes, word, peak, fp_peak=None):
     """Algorithmic HBM GB/s of the per-step transfer kernels (BASELINE.json metric "HVP/P2G HBM GB/s"),
     from the event-timed scopes (the sort runs inside the P2G scope).  Bytes per unit:
       sort  keys (read x: 3 words, write key + index: 8 B) + permute (read and write the 26-word SoA
@@ -196,6 +207,14 @@ def transfer_rooflines(fam, n_particles, n_active_nodes, word, peak):
         gbs = by / (ms / n * 1e-3) / 1e9
         out[k] = {"achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                   "algorithmic_bytes_per_launch": by, "avg_launch_ms": ms / n}
+        if fp_peak and k in SURVEY_FLOPS_PER_PARTICLE:
+            fl = n_particles * SURVEY_FLOPS_PER_PARTICLE[k]
+            tf = fl / (ms / n * 1e-3) / 1e12
+            bound, t_hbm, t_fp = roofline_bound(by, fl, peak, fp_peak)
+            out[k]["fp_pipe"] = {"achieved_tflops": tf, "peak_tflops": fp_peak, "frac": tf / fp_peak,
+                                 "flops_per_particle": SURVEY_FLOPS_PER_PARTICLE[k], "accounting": "SURVEY.md §8(d)"}
+            out[k]["bound"] = bound
+            out[k]["floor_ms"] = max(t_hbm, t_fp) * 1e3
     return out
 
 
@@ -498,6 +517,36 @@ def main():
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"one bench step (P2G, Pi, I+T receivers, {args.newton} Newton x {args.cg} PCG, G2P) of a "
                          f"{args.cpu_cells}^3-cell C5 cube ({ncpu} particles), {dt:.1f} s single-threaded"}
+    # The HVP's roofline: its algorithmic intensity (1256 flop per 190 B in fp64, 6.6
+    # flop/B) lies above the B200's FP64 ridge (37.2 TFLOP/s / 6.45 TB/s = 5.8 flop/B), so the slower of
+    # the two floors is the FP pipe's: bound "alu", against the FP vector peak derived from the guide's
+    # unit counts and clock (148 SMs x 64 FP64 FMA lanes x 2 x 1.965 GHz; fp32 2x); the HBM fraction of
+    # the same launches is reported beside it under "hbm".
+    fp_nominal = FP64_PEAK_TFLOPS * (2 if word == 4 else 1)
+    hvp_flops = n_local * HVP_FLOPS_PER_PARTICLE
+    hbm_part = {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak if achieved else None,
+                "peak_kind": peak_kind, "algorithmic_bytes_per_launch": hvp_bytes,
+                "accounting": "SURVEY.md §8(d): 190 B/particle fp64 (95 fp32) x particles per launch",
+                "reformulated_bytes_per_launch": hvp_reformulated_bytes(n_local, n_active, word)}
+    if hv_n:
+        bound, t_hbm, t_fp = roofline_bound(hvp_bytes, hvp_flops, peak, fp_nominal)
+        tf = hvp_flops / (hvp_avg_ms * 1e-3) / 1e12
+        hvp_roofline = {
+            "bound": bound, "kernel": "k_hvp_sw", "avg_launch_ms": hvp_avg_ms, "launches": hv_n,
+            "traffic": traffic, "traffic_source": f"profiles/ncu_hvp_{args.precision}.json (ncu --set full)",
+            "floor_ms": {"hbm": t_hbm * 1e3, "fp_pipe": t_fp * 1e3},
+            "hbm": hbm_part,
+            "fp_pipe": {"achieved_tflops": tf, "peak_tflops": fp_nominal, "frac": tf / fp_nominal,
+                        "flops_per_particle": HVP_FLOPS_PER_PARTICLE,
+                        "peak_kind": "derived: 148 SMs x 64 FP64 FMA lanes/SM x 2 flops x 1.965 GHz (fp32 2x)",
+                        "measured_peak_tflops": fma_peak,
+                        "measured_frac": tf / fma_peak}}
+        if bound == "alu":
+            hvp_roofline.update({"achieved": tf, "peak": fp_nominal, "unit": "TFLOP/s", "frac": tf / fp_nominal})
+        else:
+            hvp_roofline.update({"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": hbm_part["frac"]})
+    else:
+        hvp_roofline = {"bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s", "frac": None, "hbm": hbm_part}
     line = {
         "metric": METRIC, "value": n / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
@@ -517,24 +566,9 @@ def main():
                                    else (f"x-slabs x{slabs_total} on one GPU" if slabs_total > 1 else "single GPU")),
                    "slab_cuts": cuts, "halo": args.halo,
                    "l2": "working set (>3 GB) far larger than the 126 MB L2; no flush needed"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak if achieved else None,
-                     "traffic": traffic, "traffic_source": f"profiles/ncu_hvp_{args.precision}.json (ncu --set full)",
-                     "kernel": "k_hvp_sw", "peak_kind": peak_kind,
-                     "algorithmic_bytes_per_launch": hvp_bytes, "avg_launch_ms": hvp_avg_ms,
-                     "accounting": "SURVEY.md §8(d): 190 B/particle fp64 (95 fp32) x particles per launch",
-                     "reformulated_bytes_per_launch": hvp_reformulated_bytes(n_local, n_active, word),
-                     "launches": hv_n,
-                     # the same launches against the CUDA-core floating-point peak (the
-                     # fp64 HVP's compute ceiling lies at 68 % of the HBM roofline)
-                     "fp_pipe": ({"achieved_tflops": n_local * HVP_FLOPS_PER_PARTICLE / (hvp_avg_ms * 1e-3) / 1e12,
-                                  "peak_tflops": fma_peak,
-                                  "frac": n_local * HVP_FLOPS_PER_PARTICLE / (hvp_avg_ms * 1e-3) / 1e12 / fma_peak,
-                                  "flops_per_particle": HVP_FLOPS_PER_PARTICLE,
-                                  "peak_kind": "measured (osmpm_measure_fma_peak, independent FMA chains)",
-                                  "nominal_peak_tflops": FP64_PEAK_TFLOPS * (2 if word == 4 else 1)}
-                                 if hv_n else None)},
+        "roofline": hvp_roofline,
         "kernel_ms_per_step": {f: v[1] / args.steps for f, v in fam.items()},
-        "transfer_rooflines": transfer_rooflines(fam, n_local, n_active, word, peak),
+        "transfer_rooflines": transfer_rooflines(fam, n_local, n_active, word, peak, fp_nominal),
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches_timed,
