@@ -182,9 +182,12 @@ osmpm_status osmpm_launch_count(osmpm_ctx* ctx, int64_t* launches);
  * keeps the particles whose base node lies in its slabs, ghost node planes are exchanged after every
  * scatter, reductions are all-reduced, and particles migrate across the cuts after G2P.
  * osmpm_ctx_set_local_slabs splits each rank's share further into n slabs ON THE SAME DEVICE (halo
- * exchange by device copies): the same decomposition testable on one GPU.
+ * exchange by device copies): the same decomposition testable on one GPU.  nranks == 1 also creates
+ * a (one-rank) communicator: the ctx's decomposed subdomains then run the multi-rank code path, every
+ * all-reduce / all-gather / broadcast through NCCL, neighbour exchanges finding no neighbour.
  * Reads of a decomposed subdomain fill only this rank's particles / owned nodes (others untouched
- * for particles, zero for dense node vectors); sum over ranks to assemble. */
+ * for particles, zero for dense node vectors); sum over ranks to assemble.
+ * Errors: INVALID_ARG (rank / nranks out of range, a second init on one ctx), NCCL (init failed). */
 osmpm_status osmpm_comm_unique_id(uint8_t id[128]);
 osmpm_status osmpm_ctx_init_comm(osmpm_ctx* ctx, int rank, int nranks, const uint8_t id[128]);
 osmpm_status osmpm_ctx_set_local_slabs(osmpm_ctx* ctx, int n);

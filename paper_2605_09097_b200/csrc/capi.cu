@@ -202,11 +202,12 @@ osmpm_status osmpm_ctx_init_comm(osmpm_ctx* ctx, int rank, int nranks, const uin
     SET_DEVICE(ctx);
     ctx->gc.rank = rank;
     ctx->gc.nranks = nranks;
-    if (nranks > 1) {
-        ncclUniqueId u;
-        std::memcpy(&u, id, 128);
-        OSMPM_NCCL(ncclCommInitRank(&ctx->gc.comm, nranks, u, rank));
-    }
+    // a communicator of one rank too: the subdomains of this ctx then take the multi-rank code path
+    // (NCCL all-reduces, all-gather, broadcast; neighbour exchanges find no neighbour), which is how
+    // the NCCL calls run on a one-GPU box (tests/test_gpu_nccl1.py)
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    OSMPM_NCCL(ncclCommInitRank(&ctx->gc.comm, nranks, u, rank));
     return OSMPM_OK;
 }
 
@@ -258,7 +259,7 @@ osmpm_status osmpm_subdomain_create_ex(osmpm_ctx* ctx, const osmpm_grid_desc* gr
     SET_DEVICE(ctx);
     osmpm_subdomain* s = nullptr;
     osmpm_status rc;
-    const bool dist = decompose && (ctx->gc.nranks > 1 || ctx->gc.local_slabs > 1);
+    const bool dist = decompose && (ctx->gc.multi() || ctx->gc.local_slabs > 1);
 #define MAKE(DD, RR)                                                                                \
     if (dist) {                                                                                     \
         auto* q = new Dist<DD, RR>();                                                               \

@@ -60,7 +60,7 @@ struct GroupComm {
     ncclComm_t comm = nullptr;
     int rank = 0, nranks = 1;
     int local_slabs = 1;
-    bool multi() const { return nranks > 1; }
+    bool multi() const { return comm != nullptr; }  // joined a communicator (of one or more ranks)
 };
 
 // CUDA-event timing of kernel families on the ctx stream

@@ -131,7 +131,7 @@ template <int D, typename R> struct Sub;
 template <int D, typename R> struct SlabGroup {
     Sub<D, R>* const* s;  // local slabs, ordered along x
     int ns;
-    GroupComm* gc;        // nullptr or nranks == 1: no inter-rank exchange
+    GroupComm* gc;        // nullptr or no communicator: no inter-rank exchange
     GroupBufs* gb;
     cudaStream_t st;
     osmpm_ctx* ctx;

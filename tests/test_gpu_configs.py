@@ -190,19 +190,25 @@ def test_c4_fp32_frame(ctx):
             assert np.abs(out[k] - rr).max() <= bound, k
 
 
-@pytest.mark.parametrize("name,slabs", [("c4", 2), ("c4", 3), ("c3", 2), ("c3", 4)])
-def test_config_frame_parity_decomposed_fine(name, slabs):
+@pytest.mark.parametrize("name,slabs,nccl", [("c4", 2, False), ("c4", 3, False), ("c3", 2, False), ("c3", 4, False),
+                                             ("c3", 2, True), ("c4", 1, True)])
+def test_config_frame_parity_decomposed_fine(name, slabs, nccl):
     """The Schwarz frame with the FINE subdomain split into x-slabs (here `slabs` local
     slabs on one GPU: the same slab layout, halo sums, Gamma_S / arbitration over owned + ghost nodes,
     Pi partial sums and residual reductions as the multi-rank path, minus NCCL) and the coarse
-    subdomain whole (decompose = 0): equal to the oracle frame at 1e-8 with the same receiver sets."""
+    subdomain whole (decompose = 0): equal to the oracle frame at 1e-8 with the same receiver sets.
+    `nccl`: on a one-rank NCCL communicator, so that the coupler's Gamma_B broadcast, the OR of the
+    taken-over coarse nodes, the Pi partial sums and the residual norms go through NCCL."""
     from paper_2605_09097_b200 import osmpm
     coarse, fine = CONFIGS[name]()
     M = coarse.meta["M"]
     dT = coarse.dt
     ref = _oracle_frame(name, 2)
     ctx = osmpm.Context(0)
-    ctx.set_local_slabs(slabs)
+    if nccl:
+        ctx.init_comm(0, 1, osmpm.comm_unique_id())
+    if slabs > 1:
+        ctx.set_local_slabs(slabs)
     sb = osmpm.Subdomain(ctx, coarse.grid, coarse.dt, coarse.particles, coarse.materials, coarse.gravity,
                          decompose=False)
     ss = osmpm.Subdomain(ctx, fine.grid, fine.dt, fine.particles, fine.materials, fine.gravity)

@@ -4,7 +4,12 @@ The fine subdomain is split into G x-slabs ON ONE GPU (osmpm_ctx_set_local_slabs
 layout, ghost-plane halo exchange, owned-node reductions and particle migration as the multi-GPU
 path, with device copies in place of NCCL).  Every kernel output must equal the oracle at the
 per-kernel tolerance, and the decomposed solve / G2P / migration must reproduce the undecomposed
-subdomain (only the fp atomic order differs)."""
+subdomain (only the fp atomic order differs).
+
+Cases marked `nccl` join a one-rank NCCL communicator first (osmpm_ctx_init_comm with nranks = 1): the
+subdomain then takes the multi-rank code path, so the all-reduces of the PCG scalars and of the
+Newton / migration bounds, the all-gather of the halo records and the coupler's broadcast and
+all-reduces run through NCCL on the GPU (neighbour exchanges find no neighbour)."""
 import numpy as np
 import pytest
 
@@ -24,9 +29,11 @@ FIX = {
 }
 
 
-def _ctx(slabs):
+def _ctx(slabs, nccl=False):
     from paper_2605_09097_b200 import osmpm
     c = osmpm.Context(0)
+    if nccl:
+        c.init_comm(0, 1, osmpm.comm_unique_id())
     if slabs > 1:
         c.set_local_slabs(slabs)
     return c
@@ -37,11 +44,12 @@ def _sub(ctx, sc, decompose=True):
     return osmpm.Subdomain(ctx, sc.grid, sc.dt, sc.particles, sc.materials, sc.gravity, decompose=decompose)
 
 
-@pytest.mark.parametrize("name,slabs", [("3d", 2), ("3d", 3), ("2d", 2), ("2d", 4), ("3d8", 8)])
-def test_decomposed_kernels_match_oracle(name, slabs):
+@pytest.mark.parametrize("name,slabs,nccl", [("3d", 2, False), ("3d", 3, False), ("2d", 2, False), ("2d", 4, False),
+                                             ("3d8", 8, False), ("3d", 1, True), ("3d", 3, True), ("2d", 2, True)])
+def test_decomposed_kernels_match_oracle(name, slabs, nccl):
     sc = synth.random_fixture(**FIX[name])
     d = sc.grid.dim
-    ctx = _ctx(slabs)
+    ctx = _ctx(slabs, nccl)
     sub = _sub(ctx, sc)
     st, sl, fs, nl, cuts = sub.decomp()
     assert (st, sl, fs, nl) == (slabs, slabs, 0, sc.particles.n)
@@ -64,14 +72,14 @@ def test_decomposed_kernels_match_oracle(name, slabs):
     ctx.close()
 
 
-@pytest.mark.parametrize("name,slabs", [("3d", 3), ("2d", 2)])
-def test_decomposed_solve_matches_oracle_and_whole(name, slabs):
+@pytest.mark.parametrize("name,slabs,nccl", [("3d", 3, False), ("2d", 2, False), ("3d", 3, True), ("2d", 1, True)])
+def test_decomposed_solve_matches_oracle_and_whole(name, slabs, nccl):
     from paper_2605_09097_b200 import osmpm
     sc = synth.random_fixture(**FIX[name])
     act = oracle.p2g(sc).active.astype(bool)
     kw = dict(newton_rtol=1e-12, cg_rtol=1e-12, max_cg=3000)
     # converged: against the oracle's Newton-PCG
-    ctx = _ctx(slabs)
+    ctx = _ctx(slabs, nccl)
     sub = _sub(ctx, sc)
     sub.p2g()
     st = sub.implicit_solve(osmpm.newton_settings(**kw))
@@ -95,8 +103,9 @@ def test_decomposed_solve_matches_oracle_and_whole(name, slabs):
         c.close()
 
 
-@pytest.mark.parametrize("name,slabs", [("3d", 2), ("3d", 4), ("2d", 3), ("3d8", 8)])
-def test_decomposed_single_reduction_pcg(name, slabs):
+@pytest.mark.parametrize("name,slabs,nccl", [("3d", 2, False), ("3d", 4, False), ("2d", 3, False), ("3d8", 8, False),
+                                             ("3d", 2, True)])
+def test_decomposed_single_reduction_pcg(name, slabs, nccl):
     """R22 over slabs: the single-reduction PCG (one reduction -- one all-reduce across ranks -- per
     iteration, curvature partials from every slab's HVP tiles) equals the oracle's single-reduction PCG
     (fixed 3 x 40 at 1e-9, converged at 1e-8) and the undecomposed subdomain."""
@@ -109,7 +118,7 @@ def test_decomposed_single_reduction_pcg(name, slabs):
         u_ref, st_ref = oracle.implicit_solve(sc, ref, oracle.default_settings(cg_variant=1, **kw))
         out = []
         for k in (slabs, 1):
-            ctx = _ctx(k)
+            ctx = _ctx(k, nccl and k == slabs)
             sub = _sub(ctx, sc)
             sub.p2g()
             st = sub.implicit_solve(osmpm.newton_settings(cg_variant=1, **kw))
@@ -124,8 +133,8 @@ def test_decomposed_single_reduction_pcg(name, slabs):
         assert rel_linf(out[0], out[1]) <= tol
 
 
-@pytest.mark.parametrize("name,slabs", [("3d", 3), ("2d", 3), ("3d8", 8)])
-def test_migration_conserves_and_matches_whole(name, slabs):
+@pytest.mark.parametrize("name,slabs,nccl", [("3d", 3, False), ("2d", 3, False), ("3d8", 8, False), ("3d", 3, True)])
+def test_migration_conserves_and_matches_whole(name, slabs, nccl):
     """Advect every particle by ~1.3 cells along +x (uniform grid velocity) so that particles cross
     the cuts; particle count, mass and momentum are conserved exactly, states equal the whole
     subdomain's, and the next P2G is unchanged by the decomposition."""
@@ -135,7 +144,7 @@ def test_migration_conserves_and_matches_whole(name, slabs):
     shift = 1.3 * sc.grid.dx
     outs = []
     for slabs_ in (slabs, 1):
-        ctx = _ctx(slabs_)
+        ctx = _ctx(slabs_, nccl and slabs_ == slabs)
         s = _sub(ctx, sc)
         s.p2g()
         nn = int(np.prod(sc.grid.dims[:d]))
