@@ -43,6 +43,11 @@ template <int D, typename R> struct SWRec {
     // per row; the 30-real record has exactly the room), otherwise packed
     static constexpr int GP = (D == 3 && sizeof(R) == 8) ? 4 : D;
     static constexpr int RS = HvpRec<D, R>::RS;
+    // Records of the particles of layer cell c start SK reals (16 B) per cell further on: the quarter
+    // warps of phase 2 (one cell each) read their cells' k-th records at bank-group offsets 15k + 121c
+    // (mod 8, fp64, 8 particles per cell) -- distinct without rotating each cell's particle order, so
+    // the record addresses are per-thread bases plus compile-time offsets (no per-particle index math)
+    static constexpr int SK = 16 / sizeof(R);
 };
 
 template <int D> struct SW {
@@ -191,7 +196,7 @@ constexpr size_t hvp_sw_smem_bytes()
     using T = Tile<D>;
     return 16 + 128 /* alignment of the streamed-input block */ + ((size_t)SW<D>::NNP * SVS<D, R>::S + SW<D>::STG +
                  (size_t)SWIn<D, R>::TOT +
-                 (size_t)SWRec<D, R>::RS * HvpT<D>::NT) *
+                 (size_t)SWRec<D, R>::RS * HvpT<D>::NT + (size_t)T::LC * SWRec<D, R>::SK) *
                     sizeof(R);
 }
 
@@ -618,7 +623,12 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
     }
     const bool fused = halo.yL || halo.yR;
     double dkd = 0.0;  // this thread's flushed nodes' d . y_tile
-    auto layer_empty = [&](int l) { return scs[l * T::LC] == scs[(l + 1) * T::LC]; };
+    // non-empty layers as a bit mask (one shared-memory pass instead of re-reading the cell ranges)
+    unsigned nem = 0;
+#pragma unroll
+    for (int l = 0; l < T::NL; ++l)
+        if (scs[l * T::LC] != scs[(l + 1) * T::LC]) nem |= 1u << l;
+    auto layer_empty = [&](int l) { return ((nem >> l) & 1u) == 0u; };
     if constexpr (ASYNC)
         asm volatile("cp.async.wait_all;" ::: "memory");
     else
@@ -635,7 +645,10 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
         if (layer < T::NL && !layer_empty(layer)) {
             const int lb = scs[layer * T::LC], le = scs[(layer + 1) * T::LC];
             int next = layer + 1;
-            while (next < T::NL && layer_empty(next)) ++next;
+            {
+                const unsigned later = nem >> (layer + 1);
+                next = later ? layer + __ffs(later) : T::NL;
+            }
             const int pf_base = lb & ~(In::UE - 1);
             const int ks = scs[layer * T::LC + icell];
             const int ke = scs[layer * T::LC + icell + 1];
@@ -669,7 +682,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                     R w[3][3], dw[3][3];
                     int lc[3] = {0, 0, 0};
                     weights_at<D, R>(x, b, t, lc, w, dw);
-                    const RecPtr<R> r(rec, q, RS);
+                    const RecPtr<R> r(rec + (D == 3 ? lc[0] * T::T1 + lc[1] : lc[0]) * SR::SK, q, RS);
                     store_weights<D, R>(r, w, dw);
                     R gd[D * D];
                     sw_gather<D, R>(sv, lc, w, dw, gd);
@@ -738,16 +751,15 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                 }
                 if (it < T::ITEMS) {
                     const int p0 = max(ks, sb), p1 = min(ke, se);
-                    // (icell & 7) % len without the integer division when len >= 8 (the usual case)
-                    const int len = p1 - p0, r7 = icell & 7;
-                    const int rot = r7 < len ? r7 : (len > 0 ? r7 % len : 0);
+                    const int len = p1 - p0;
+                    R* const cbase = rec + icell * SR::SK + (p0 - sb) * RS;  // this cell's first record
 #ifndef OSMPM_P2_UNROLL
 #define OSMPM_P2_UNROLL 8
 #endif
                     constexpr int kUnroll = OSMPM_P2_UNROLL;  // 128-thread CTAs: 8 (measured 1.3022 ms vs 1.3043 at 4, 1.3103 at 2)
 #pragma unroll kUnroll
                     for (int k = 0; k < len; ++k) {
-                        const RecPtr<R> r(rec, rotated(p0, len, k, rot) - sb, RS);
+                        const RecPtr<R> r(cbase, k, RS);
                         ItemW<D, R> W;
                         R s[D];
                         W.load(r, ii);
@@ -759,7 +771,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                         // the cell's ninth item: particles pr, pr + 8, ... of the cell in this chunk
 #pragma unroll 1
                         for (int k = it & 7; k < len; k += 8) {
-                            const RecPtr<R> r(rec, p0 + k - sb, RS);
+                            const RecPtr<R> r(cbase, k, RS);
                             ItemW<D, R> W;
                             R s[D];
                             W.load(r, 2);
