@@ -24,7 +24,8 @@ template <int D, typename R>
 constexpr size_t grad_sw_smem_bytes()
 {
     using T = Tile<D>;
-    return 16 + ((size_t)SW<D>::NNP * SVS<D, double>::S + 2 * SW<D>::STG + (size_t)GradRec<D>::RS * T::NT) *
+    return 16 + ((size_t)SW<D>::NNP * SVS<D, double>::S + 2 * SW<D>::STG + (size_t)GradRec<D>::RS * T::NT +
+                 (size_t)T::LC * 2 /* per-cell record skew, hvp_sw.cuh SWRec::SK */) *
                     sizeof(double) +
            (size_t)GradIn<D, R>::NF * GradIn<D, R>::PFS * sizeof(R);
 }
@@ -64,7 +65,7 @@ k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int
     Rd* stg = sv + S::NNP * SVS<D, Rd>::S;
     Rd* stgd = stg + S::STG;
     Rd* rec = stgd + S::STG;
-    R* pf = reinterpret_cast<R*>(rec + RS * T::NT);
+    R* pf = reinterpret_cast<R*>(rec + RS * T::NT + T::LC * 2);
     const int tile = blockIdx.x;
     const int64_t kt = (int64_t)tile * T::NC;
     double red[3] = {0.0, 0.0, 0.0};
@@ -85,6 +86,7 @@ k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int
     }
     int t[3];
     tile_coords<D>(b, tile, t);
+    const FlushItem<D, Rd> fli(b, t, nullptr);
     sw_stage_tile<D, Rd, T::NT>(b, t, uin, sv);
     for (int k = threadIdx.x; k < 2 * S::STG; k += T::NT) stg[k] = 0.0;
     __syncthreads();
@@ -119,7 +121,7 @@ k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int
 #pragma unroll
                     for (int a = 0; a < D; ++a) x[a] = in(a);
                     weights_at<D, Rd>(x, b, t, lc, w, dw);
-                    const RecPtr<Rd> r(rec, q, RS);
+                    const RecPtr<Rd> r(rec + (D == 3 ? lc[0] * T::T1 + lc[1] : lc[0]) * 2, q, RS);
                     store_weights<D, Rd>(r, w, dw);
                     Rd Mx[D * D];
                     sw_gather<D, Rd>(sv, lc, w, dw, Mx);
@@ -187,9 +189,10 @@ k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int
                 }
                 if (it < T::ITEMS) {
                     const int p0 = max(ks, sb), p1 = min(ke, se);
-                    const int len = p1 - p0, rot = len > 0 ? (icell & 7) % len : 0;
+                    const int len = p1 - p0;
+                    Rd* const cbase = rec + icell * 2 + (p0 - sb) * RS;  // per-cell skew (hvp_sw.cuh SWRec)
                     for (int k = 0; k < len; ++k) {
-                        const RecPtr<Rd> r(rec, rotated(p0, len, k, rot) - sb, RS);
+                        const RecPtr<Rd> r(cbase, k, RS);
                         ItemW<D, Rd> W;
                         W.load(r, ii);
                         Rd sg[D], Ar[D], Q[Sym<D>::N];
@@ -216,10 +219,10 @@ k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int
         }
         __syncthreads();
         double nodot = 0.0;
-        sw_flush<D, Rd, false>(b, t, layer, stg, gout, tbg ? tbg + (int64_t)tile * T::NN * D : nullptr, nullptr,
-                               nullptr, nodot);
-        sw_flush<D, Rd, false>(b, t, layer, stgd, dout, tbd ? tbd + (int64_t)tile * T::NN * D : nullptr, nullptr,
-                               nullptr, nodot);
+        fli.template flush<false>(layer, stg, gout, tbg ? tbg + (int64_t)tile * T::NN * D : nullptr, nullptr, nullptr,
+                                  nodot, nullptr);
+        fli.template flush<false>(layer, stgd, dout, tbd ? tbd + (int64_t)tile * T::NN * D : nullptr, nullptr, nullptr,
+                                  nodot, nullptr);
         if (layer + 1 >= T::NL || layer_empty(layer + 1)) __syncthreads();
     }
     block_reduce_store<3>(red, partials);

@@ -394,7 +394,7 @@ __global__ void k_halo_wait(const unsigned* inbox, unsigned expL, unsigned expR,
     }
 }
 
-// fixed-order NSLOT-term sums of plane `plane` (tile-local last-axis node index) -> one RED each
+// Plane flush: fixed-order NSLOT-term sums of plane `plane` (tile-local last-axis node index) -> one RED each
 //
 // Deterministic mode (tb != nullptr, OSMPM_DETERMINISTIC=1): instead of the RED, every sum (zeros
 // included) is stored to the tile's own block of node values tb[tile-local node][component]; the node
@@ -405,49 +405,69 @@ __global__ void k_halo_wait(const unsigned* inbox, unsigned expL, unsigned expR,
 // node tile (fp64) or re-read from global memory (fp32 tiles hold d rounded).
 // With a HaloDev (fused halo, R24), sums of nodes on planes shared with a neighbouring slab also go to
 // the neighbour's copy.
-template <int D, typename R, bool DOT>
-__device__ __forceinline__ void sw_flush(const BoxDev& b, const int* t, int plane, const R* stg,
-                                         double* __restrict__ out, double* __restrict__ tb, const R* sv,
-                                         const double* __restrict__ din, double& dot, const HaloDev* hl = nullptr,
-                                         int nthr = Tile<D>::NT)
-{
-    using T = Tile<D>;
-    for (int it = threadIdx.x; it < SW<D>::NITEM; it += nthr) {
-        // slot-major staging: consecutive threads read consecutive reals (conflict-free)
+// The thread's flush item is fixed for the whole tile (NITEM <= threads): its node / component,
+// global node index, node-tile element, tile-block index and halo targets are computed once per tile and
+// advance by one node per plane (x slowest, the last axis fastest in both the box and the node tile), so
+// a plane's flush is the fixed-order slot sum, the RED and nothing else.  Same sums, same order.
+template <int D, typename R>
+struct FlushItem {
+    bool valid = false, toR = false, toL = false;
+    int a = 0, it = 0, ln0 = 0, tb0 = 0;
+    int64_t g0 = 0;
+    __device__ __forceinline__ FlushItem(const BoxDev& b, const int* t, const HaloDev* hl)
+    {
+        using T = Tile<D>;
+        static_assert(SW<D>::NITEM <= Tile<D>::NT && SW<D>::NITEM <= HvpT<D>::NT, "one flush item per thread");
+        it = threadIdx.x;
+        valid = it < SW<D>::NITEM;
+        a = it % D;
+        const int nxy = it / D;
+        const int l0 = (D == 3) ? nxy / T::N1 : nxy, l1 = (D == 3) ? nxy % T::N1 : 0;
+        if (D == 3) {
+            g0 = box_node<D>(b, t[0] * T::T0 + l0, t[1] * T::T1 + l1, t[2] * T::T2);
+            ln0 = sw_node<D>(l0, l1, 0);
+            tb0 = nxy * T::N2;
+        } else {
+            g0 = box_node<D>(b, t[0] * T::T0 + l0, t[1] * T::T1, 0);
+            ln0 = sw_node<D>(l0, 0, 0);
+            tb0 = nxy * T::N1;
+        }
+        if (hl) {
+            const int ix = t[0] * T::T0 + l0;
+            toR = hl->yR && ix >= hl->ixR;
+            toL = hl->yL && ix < 2;
+        }
+    }
+    template <bool DOT>
+    __device__ __forceinline__ void flush(int plane, const R* stg, double* __restrict__ out, double* __restrict__ tb,
+                                          const R* sv, const double* __restrict__ din, double& dot,
+                                          const HaloDev* hl) const
+    {
+        if (!valid) return;
         R s = stg[it];
 #pragma unroll
         for (int k = 1; k < SW<D>::NSLOT; ++k) s += stg[k * SW<D>::NITEM + it];
-        const int a = it % D, nxy = it / D;
-        if (tb) {
-            tb[((D == 3) ? nxy * T::N2 + plane : nxy * T::N1 + plane) * D + a] = (double)s;
-        }
+        if (tb) tb[(tb0 + plane) * D + a] = (double)s;
         if (s != R(0) && (tb == nullptr || DOT)) {
-            int64_t g;
-            if (D == 3)
-                g = box_node<D>(b, t[0] * T::T0 + nxy / T::N1, t[1] * T::T1 + nxy % T::N1, t[2] * T::T2 + plane);
-            else
-                g = box_node<D>(b, t[0] * T::T0 + nxy, t[1] * T::T1 + plane, 0);
+            const int64_t g = g0 + plane;
             if (!tb) {
                 red_add(&out[g * D + a], (double)s);
                 if (hl) {
-                    const int ix = t[0] * T::T0 + ((D == 3) ? nxy / T::N1 : nxy);
-                    if (hl->yR && ix >= hl->ixR) red_add(&hl->yR[(g + hl->offR) * D + a], (double)s);
-                    if (hl->yL && ix < 2) red_add(&hl->yL[(g + hl->offL) * D + a], (double)s);
+                    if (toR) red_add(&hl->yR[(g + hl->offR) * D + a], (double)s);
+                    if (toL) red_add(&hl->yL[(g + hl->offL) * D + a], (double)s);
                 }
             }
             if constexpr (DOT) {
                 double dv;
-                if constexpr (sizeof(R) == 8) {
-                    const int ln = (D == 3) ? sw_node<D>(nxy / T::N1, nxy % T::N1, plane) : sw_node<D>(nxy, plane, 0);
-                    dv = (double)sv[sv_elem<D, R>(ln, a, SW<D>::NNP)];
-                } else {
+                if constexpr (sizeof(R) == 8)
+                    dv = (double)sv[sv_elem<D, R>(ln0 + plane, a, SW<D>::NNP)];
+                else
                     dv = din[g * D + a];
-                }
                 dot = fma(dv, (double)s, dot);
             }
         }
     }
-}
+};
 
 // out[node] = sum over the non-empty tiles covering the node, in increasing tile order per axis, of
 // the tile blocks written by sw_flush in deterministic mode (all nodes of the box, plain stores)
@@ -562,7 +582,7 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
          double* __restrict__ pkp, const __grid_constant__ HaloDev halo)
 {
     // pkp (optional): per-CTA partials of d^T K d = sum over tiles of d . (the tile's partial y), the
-    // curvature the PCG step length needs, accumulated by the plane flushes (sw_flush)
+    // curvature the PCG step length needs, accumulated by the plane flushes (FlushItem)
     using T = Tile<D>;
     using C = CL<D>;
     using In = HvpIn<D, R>;
@@ -623,6 +643,9 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
     }
     const bool fused = halo.yL || halo.yR;
     double dkd = 0.0;  // this thread's flushed nodes' d . y_tile
+    double* const tbl = tbuf ? tbuf + (int64_t)tile * T::NN * D : nullptr;
+    const HaloDev* const hl = fused ? &halo : nullptr;
+    const FlushItem<D, R> fli(b, t, hl);
     // non-empty layers as a bit mask (one shared-memory pass instead of re-reading the cell ranges)
     unsigned nem = 0;
 #pragma unroll
@@ -809,14 +832,10 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
             }
         }
         __syncthreads();
-        {
-            double* tbl = tbuf ? tbuf + (int64_t)tile * T::NN * D : nullptr;
-            const HaloDev* hl = fused ? &halo : nullptr;
-            if (pkp)
-                sw_flush<D, R, true>(b, t, layer, stg, yout, tbl, sv, din, dkd, hl, NTH);
-            else
-                sw_flush<D, R, false>(b, t, layer, stg, yout, tbl, sv, din, dkd, hl, NTH);
-        }
+        if (pkp)
+            fli.template flush<true>(layer, stg, yout, tbl, sv, din, dkd, hl);
+        else
+            fli.template flush<false>(layer, stg, yout, tbl, sv, din, dkd, hl);
         // the next emit must not overwrite slots still being summed: a non-empty next layer has its
         // records barrier in between; otherwise synchronise here
         if (pkp && layer == T::NL + 1) {
