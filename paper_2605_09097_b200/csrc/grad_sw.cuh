@@ -5,7 +5,7 @@
 //   V0 Psi = 1/2 (tr(M S' M^T) - V0 mu d) - V0 mu ln J + V0 lam/2 ln^2 J
 // (PAPER.md:151-164 Eq. discrete_energy, 186-191 Eq. F_update, 205-210 Newton).
 // Structure of k_hvp_sw (hvp_sw.cuh): per layer, phase 1 (thread per particle) with the particle
-// inputs x, F^n, V0 streamed by TMA bulk copies, phase 2 (thread per (cell, a, i)) accumulating the
+// inputs x, F^n, V0 read from the sorted SoA, phase 2 (thread per (cell, a, i)) accumulating the
 // gradient and the diagonal in two 3-plane register windows, plane-wise staged fixed-order sums and
 // one fp64 RED per node; fp64 arithmetic for every particle precision (R14).
 #pragma once
@@ -13,40 +13,26 @@
 
 namespace osmpm {
 
-template <int D, typename R> struct GradIn {
-    static constexpr int NF = D + D * D + 1;  // x, F^n, V0
-    static constexpr int UE = 16 / sizeof(R);
-    static constexpr int PFS = Tile<D>::NT + 2 * UE;
+// particle inputs of phase 1: x, F^n, V0 (13 fields in 3D), read straight from the sorted SoA (coalesced)
+template <int D> struct GradIn {
+    static constexpr int NF = D + D * D + 1;
     __device__ static int field(int f) { return f < D ? PL<D>::X + f : (f < D + D * D ? PL<D>::F + f - D : PL<D>::VOL); }
 };
 
+// [mbarrier slot 16 B][node tile][gradient and diagonal staging][records, per-cell skew].  75 KB in 3D:
+// three 144-thread CTAs per SM.  (Streaming the 13 input fields by TMA needs 15 KB more per CTA, i.e.
+// two CTAs per SM: measured 34.1 ms per C5 sub-step against 33.0 ms for three CTAs with direct loads.)
 template <int D, typename R>
 constexpr size_t grad_sw_smem_bytes()
 {
     using T = Tile<D>;
     return 16 + ((size_t)SW<D>::NNP * SVS<D, double>::S + 2 * SW<D>::STG + (size_t)GradRec<D>::RS * T::NT +
                  (size_t)T::LC * 2 /* per-cell record skew, hvp_sw.cuh SWRec::SK */) *
-                    sizeof(double) +
-           (size_t)GradIn<D, R>::NF * GradIn<D, R>::PFS * sizeof(R);
+                    sizeof(double);
 }
 
 template <int D, typename R>
-__device__ __forceinline__ void grad_prefetch(const R* __restrict__ P, int64_t cap, int lb, int le, R* pf, uint64_t* bar,
-                                              int lane)
-{
-    using In = GradIn<D, R>;
-    static_assert(In::NF <= 32, "one field per lane");
-    const int lb0 = lb & ~(In::UE - 1);
-    const int cnt = min(le, lb + Tile<D>::NT) - lb0;
-    const uint32_t bytes = (uint32_t)((cnt + In::UE - 1) & ~(In::UE - 1)) * sizeof(R);
-    fence_async_smem();
-    if (lane == 0) mbar_expect_tx(bar, bytes * In::NF);
-    __syncwarp();
-    if (lane < In::NF) bulk_g2s(pf + lane * In::PFS, P + (int64_t)In::field(lane) * cap + lb0, bytes, bar);
-}
-
-template <int D, typename R>
-__global__ void __launch_bounds__(Tile<D>::NT, 2)
+__global__ void __launch_bounds__(Tile<D>::NT, 3)
 k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int* __restrict__ mat,
           const int* __restrict__ cell_start, BoxDev b, MatTable mt, const double* __restrict__ uin,
           double* __restrict__ gout, double* __restrict__ dout, double* __restrict__ partials,
@@ -55,17 +41,15 @@ k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int
     using T = Tile<D>;
     using GR = GradRec<D>;
     using C = CL<D>;
-    using In = GradIn<D, R>;
+    using In = GradIn<D>;
     using S = SW<D>;
     using Rd = double;
     constexpr int RS = GR::RS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
     Rd* sv = reinterpret_cast<Rd*>(smem_raw + 16);
     Rd* stg = sv + S::NNP * SVS<D, Rd>::S;
     Rd* stgd = stg + S::STG;
     Rd* rec = stgd + S::STG;
-    R* pf = reinterpret_cast<R*>(rec + RS * T::NT + T::LC * 2);
     const int tile = blockIdx.x;
     const int64_t kt = (int64_t)tile * T::NC;
     double red[3] = {0.0, 0.0, 0.0};
@@ -77,13 +61,6 @@ k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int
         return;
     }
     auto layer_empty = [&](int l) { return scs[l * T::LC] == scs[(l + 1) * T::LC]; };
-    int first = 0;
-    while (layer_empty(first)) ++first;
-    if (threadIdx.x < 32) {
-        if (threadIdx.x == 0) mbar_init(bar, 1);
-        __syncwarp();
-        grad_prefetch<D, R>(P, cap, scs[first * T::LC], scs[(first + 1) * T::LC], pf, bar, threadIdx.x);
-    }
     int t[3];
     tile_coords<D>(b, tile, t);
     const FlushItem<D, Rd> fli(b, t, nullptr);
@@ -93,29 +70,20 @@ k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int
     const int it = threadIdx.x;
     int icell, icomp, ii;
     item_of<D>(it, icell, icomp, ii);
-    uint32_t parity = 0;
     Rd acc[S::NACC], accd[S::NACC];
 #pragma unroll
     for (int k = 0; k < S::NACC; ++k) acc[k] = accd[k] = 0.0;
     for (int layer = 0; layer < T::NL + 2; ++layer) {
         if (layer < T::NL && !layer_empty(layer)) {
             const int lb = scs[layer * T::LC], le = scs[(layer + 1) * T::LC];
-            int next = layer + 1;
-            while (next < T::NL && layer_empty(next)) ++next;
-            const int pf_base = lb & ~(In::UE - 1);
             const int ks = scs[layer * T::LC + icell];
             const int ke = scs[layer * T::LC + icell + 1];
             for (int sb = lb; sb < le; sb += T::NT) {
                 const int se = min(sb + T::NT, le);
                 const int q = threadIdx.x, p = sb + q;
-                const bool from_pf = (sb == lb);
                 if (sb != lb) __syncthreads();
-                if (from_pf) mbar_wait(bar, parity);
                 if (p < se) {
-                    const R* s = pf + (p - pf_base);
-                    auto in = [&](int f) -> Rd {
-                        return (Rd)(from_pf ? s[f * In::PFS] : P[(int64_t)In::field(f) * cap + p]);
-                    };
+                    auto in = [&](int f) -> Rd { return (Rd)P[(int64_t)In::field(f) * cap + p]; };
                     Rd x[3], w[3][3], dw[3][3];
                     int lc[3] = {0, 0, 0};
 #pragma unroll
@@ -181,12 +149,7 @@ k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int
                     cache[C::L * cap + p] = (R)ll;
                     *r.at(GR::CL) = cc + ll;
                 }
-                __syncthreads();  // records ready; the streamed buffer is free
-                if (from_pf) {
-                    parity ^= 1u;
-                    if (threadIdx.x < 32 && next < T::NL)
-                        grad_prefetch<D, R>(P, cap, scs[next * T::LC], scs[(next + 1) * T::LC], pf, bar, threadIdx.x);
-                }
+                __syncthreads();  // records ready
                 if (it < T::ITEMS) {
                     const int p0 = max(ks, sb), p1 = min(ke, se);
                     const int len = p1 - p0;

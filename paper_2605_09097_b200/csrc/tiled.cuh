@@ -118,7 +118,7 @@ template <int D, typename R> struct HvpRec {
 };
 template <int D> struct GradRec {
     static constexpr int S = Rec<D>::X, A = S + Sym<D>::N, CL = A + D * D;
-    static constexpr int RS = (D == 3) ? 46 : 26;
+    static constexpr int RS = (D == 3) ? 44 : 26;  // 43 used; even for the 16-B weight pairs
 };
 
 template <typename R>
