@@ -512,7 +512,7 @@ def main():
     achieved = hvp_bytes / (hvp_avg_ms * 1e-3) / 1e9 if hv_n else None
     traffic = load_traffic(args.precision)
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # the oracle baseline: rank 0 at N = 1 only
         rate, dt, ncpu = oracle_substep_rate(args.cpu_cells, args.newton, args.cg)
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"one bench step (P2G, Pi, I+T receivers, {args.newton} Newton x {args.cg} PCG, G2P) of a "
