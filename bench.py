@@ -50,6 +50,10 @@ def parse():
     ap.add_argument("--cg-variant", type=int, default=None, choices=[0, 1],
                     help="PCG variant: 0 standard, 1 single-reduction (Chronopoulos-Gear, DESIGN.md R22: one "
                          "all-reduce per iteration); default 0 on one GPU, 1 on several")
+    ap.add_argument("--comm", action="store_true",
+                    help="at N = 1: still initialise torch.distributed (NCCL) and a one-rank osmpm communicator, "
+                         "so that the multi-rank code path (decomposed subdomain, NCCL collectives, max over "
+                         "ranks) runs on one GPU -- a functional check, not a bench line")
     ap.add_argument("--slabs", type=int, default=1,
                     help="x-slabs per GPU (>1: the decomposed path on one device)")
     ap.add_argument("--halo", default="fused", choices=["fused", "all", "pass"],
@@ -334,10 +338,12 @@ def main():
 
     import torch
     if args.cg_variant is None:
-        args.cg_variant = 1 if world > 1 else 0
+        args.cg_variant = 1 if world > 1 or args.comm else 0
     dist = None
-    if world > 1:
+    if world > 1 or args.comm:
         import torch.distributed as tdist
+        for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29517"), ("RANK", "0"), ("WORLD_SIZE", "1")):
+            os.environ.setdefault(k, v)
         torch.cuda.set_device(local_rank)
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         dist = tdist
@@ -351,7 +357,7 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     ctx = osmpm.Context(local_rank, stream.cuda_stream)
-    if world > 1:
+    if world > 1 or args.comm:
         ctx.init_comm(rank, world, share_unique_id(dist, rank, osmpm.comm_unique_id))
     if args.slabs > 1:
         ctx.set_local_slabs(args.slabs)
