@@ -777,9 +777,11 @@ k_hvp_sw(const R* __restrict__ P, const R* __restrict__ cache, int64_t cap, cons
                     const int len = p1 - p0;
                     R* const cbase = rec + icell * SR::SK + (p0 - sb) * RS;  // this cell's first record
 #ifndef OSMPM_P2_UNROLL
-#define OSMPM_P2_UNROLL 8
+#define OSMPM_P2_UNROLL 4
 #endif
-                    constexpr int kUnroll = OSMPM_P2_UNROLL;  // 128-thread CTAs: 8 (measured 1.3022 ms vs 1.3043 at 4, 1.3103 at 2)
+                    // with the skewed records (constant offsets): 4 (C5 fp64 1.249 ms vs 1.256 at 8, 1.262 at
+                    // 2, 1.269 at 1; fp32 unchanged); with the earlier rotated order 8 was best
+                    constexpr int kUnroll = OSMPM_P2_UNROLL;
 #pragma unroll kUnroll
                     for (int k = 0; k < len; ++k) {
                         const RecPtr<R> r(cbase, k, RS);
