@@ -14,7 +14,10 @@ namespace osmpm {
 // Inside a tile, cells are ordered LAYER-MAJOR along the last axis (z in 3D, y in 2D): a layer
 // is the LC = T0 (x T1) cells with one last-axis index; the tiled kernels walk the layers in order.
 #ifndef OSMPM_T2
-#define OSMPM_T2 8  // layers per 3D tile (cells along z)
+// layers per 3D tile (cells along z).  C5 step, ms (HVP per step): 8 -> 748.1 (624.3), 10 -> 734.1 (612.8),
+// 12 -> 734.5 (612.1), 14 -> 798.4 (672.4); deeper tiles amortise the two tail planes and the tile
+// prologue over more layers until the node tile no longer leaves room for three HVP CTAs per SM
+#define OSMPM_T2 12
 #endif
 template <int D> struct Tile;
 template <> struct Tile<3> {

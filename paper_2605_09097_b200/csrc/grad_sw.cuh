@@ -19,16 +19,22 @@ template <int D> struct GradIn {
     __device__ static int field(int f) { return f < D ? PL<D>::X + f : (f < D + D * D ? PL<D>::F + f - D : PL<D>::VOL); }
 };
 
-// [mbarrier slot 16 B][node tile][gradient and diagonal staging][records, per-cell skew].  75 KB in 3D:
-// three 144-thread CTAs per SM.  (Streaming the 13 input fields by TMA needs 15 KB more per CTA, i.e.
-// two CTAs per SM: measured 34.1 ms per C5 sub-step against 33.0 ms for three CTAs with direct loads.)
+// [16 B][node tile][gradient and diagonal staging][records, per-cell skew].  75 KB in 3D with 8-layer
+// tiles: three 144-thread CTAs per SM.  (Streaming the 13 input fields by TMA needs 15 KB more per CTA,
+// i.e. two CTAs per SM: measured 34.1 ms per C5 sub-step against 33.0 ms for three CTAs with direct
+// loads.)  When deeper tiles would push it past the three-CTA budget, the gradient and the diagonal
+// share one staging buffer (flushed one after the other, two more barriers per layer).
+template <int D> struct GradLay {
+    using T = Tile<D>;
+    static constexpr size_t BODY = (size_t)SW<D>::NNP * SVS<D, double>::S + (size_t)GradRec<D>::RS * T::NT +
+                                   (size_t)T::LC * 2 /* per-cell record skew, hvp_sw.cuh SWRec::SK */;
+    static constexpr bool ONE_STG = 16 + (BODY + 2 * (size_t)SW<D>::STG) * sizeof(double) > 76000;
+    static constexpr int NSTG = ONE_STG ? 1 : 2;
+};
 template <int D, typename R>
 constexpr size_t grad_sw_smem_bytes()
 {
-    using T = Tile<D>;
-    return 16 + ((size_t)SW<D>::NNP * SVS<D, double>::S + 2 * SW<D>::STG + (size_t)GradRec<D>::RS * T::NT +
-                 (size_t)T::LC * 2 /* per-cell record skew, hvp_sw.cuh SWRec::SK */) *
-                    sizeof(double);
+    return 16 + (GradLay<D>::BODY + (size_t)GradLay<D>::NSTG * SW<D>::STG) * sizeof(double);
 }
 
 template <int D, typename R>
@@ -48,8 +54,9 @@ k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Rd* sv = reinterpret_cast<Rd*>(smem_raw + 16);
     Rd* stg = sv + S::NNP * SVS<D, Rd>::S;
-    Rd* stgd = stg + S::STG;
-    Rd* rec = stgd + S::STG;
+    constexpr bool ONE = GradLay<D>::ONE_STG;
+    Rd* stgd = ONE ? stg : stg + S::STG;
+    Rd* rec = stg + GradLay<D>::NSTG * S::STG;
     const int tile = blockIdx.x;
     const int64_t kt = (int64_t)tile * T::NC;
     double red[3] = {0.0, 0.0, 0.0};
@@ -65,7 +72,7 @@ k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int
     tile_coords<D>(b, tile, t);
     const FlushItem<D, Rd> fli(b, t, nullptr);
     sw_stage_tile<D, Rd, T::NT>(b, t, uin, sv);
-    for (int k = threadIdx.x; k < 2 * S::STG; k += T::NT) stg[k] = 0.0;
+    for (int k = threadIdx.x; k < GradLay<D>::NSTG * S::STG; k += T::NT) stg[k] = 0.0;
     __syncthreads();
     const int it = threadIdx.x;
     int icell, icomp, ii;
@@ -176,16 +183,26 @@ k_grad_sw(const R* __restrict__ P, R* __restrict__ cache, int64_t cap, const int
                 }
             }
         }
-        if (it < T::ITEMS) {
-            sw_emit<D, Rd>(icell, icomp, ii, acc, stg);
-            sw_emit<D, Rd>(icell, icomp, ii, accd, stgd);
-        }
-        __syncthreads();
         double nodot = 0.0;
-        fli.template flush<false>(layer, stg, gout, tbg ? tbg + (int64_t)tile * T::NN * D : nullptr, nullptr, nullptr,
-                                  nodot, nullptr);
-        fli.template flush<false>(layer, stgd, dout, tbd ? tbd + (int64_t)tile * T::NN * D : nullptr, nullptr, nullptr,
-                                  nodot, nullptr);
+        double* const tbgl = tbg ? tbg + (int64_t)tile * T::NN * D : nullptr;
+        double* const tbdl = tbd ? tbd + (int64_t)tile * T::NN * D : nullptr;
+        if constexpr (ONE) {
+            if (it < T::ITEMS) sw_emit<D, Rd>(icell, icomp, ii, acc, stg);
+            __syncthreads();
+            fli.template flush<false>(layer, stg, gout, tbgl, nullptr, nullptr, nodot, nullptr);
+            __syncthreads();
+            if (it < T::ITEMS) sw_emit<D, Rd>(icell, icomp, ii, accd, stgd);
+            __syncthreads();
+            fli.template flush<false>(layer, stgd, dout, tbdl, nullptr, nullptr, nodot, nullptr);
+        } else {
+            if (it < T::ITEMS) {
+                sw_emit<D, Rd>(icell, icomp, ii, acc, stg);
+                sw_emit<D, Rd>(icell, icomp, ii, accd, stgd);
+            }
+            __syncthreads();
+            fli.template flush<false>(layer, stg, gout, tbgl, nullptr, nullptr, nodot, nullptr);
+            fli.template flush<false>(layer, stgd, dout, tbdl, nullptr, nullptr, nodot, nullptr);
+        }
         if (layer + 1 >= T::NL || layer_empty(layer + 1)) __syncthreads();
     }
     block_reduce_store<3>(red, partials);
