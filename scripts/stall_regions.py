@@ -59,14 +59,15 @@ def main():
         return None
     g0 = find("void sw_gather")
     e0 = find("void sw_emit")
-    f0 = find("void sw_flush")
+    f0 = find("void sw_flush") or find("struct FlushItem")  # the flush became FlushItem::flush
     k0 = find("k_hvp_sw(")
     c0 = find("// M2 = A gd^T")
     c1 = find("__syncthreads();  // records ready")
     p2 = next(i for i, t in sorted(lines.items()) if i > c1 and "if (it < T::ITEMS) {" in t)
     em = find("node plane `layer` is complete")
     pf0 = find("void sw_prefetch")
-    REGIONS_SW.extend([(pf0, pf0 + 18, "TMA issue (sw_prefetch)"), (g0, e0 - 1, "phase1 gather"), (e0, f0 - 1, "emit"), (f0, f0 + 25, "flush"),
+    REGIONS_SW.extend([(pf0, pf0 + 18, "TMA issue (sw_prefetch)"), (g0, e0 - 1, "phase1 gather"), (e0, f0 - 1, "emit"), (f0, f0 + 60, "flush"),
+                       (find("void sw_prefetch_tmap"), find("void sw_prefetch_tmap") + 20, "TMA issue (tensor map)"),
                        (c0, c1 - 1, "phase1 constitutive+store G"), (c1, p2 - 1, "records barrier + TMA issue"),
                        (p2, em - 1, "phase2 loop control"), (em, em + 10, "emit/flush barriers"),
                        (k0, c0 - 1, "tile setup + phase1 loads")])
